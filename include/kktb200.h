@@ -1,0 +1,208 @@
+/*
+ * kktb200.h — C ABI of the B200-native KKT refactor / solve / FGMRES-IR hot path.
+ *
+ * One shared library, libkktb200.so, built from
+ *   paper_2401_13926_b200/csrc/analyze.cpp   (host: ordering + first pivoted LU, bit-exact)
+ *   paper_2401_13926_b200/csrc/device.cu     (sm_100a kernels + device handle)
+ *
+ * Plain C types only (no torch, no STL) so any FFI (ctypes, cffi, cgo, JNI) can bind it.
+ * Every entry point returns an int status (KKT_OK == 0); kkt_last_error() gives the
+ * thread-local message of the last failure.  The Python facade maps the codes 1:1 to the
+ * reference's exception classes.
+ *
+ * Reference interfaces replaced (paths relative to the reference package
+ * pkg/src/kktsolve/):
+ *   kkt_analyze            <- direct_lu.factorize(A, pivot_tol)          direct_lu.py:116
+ *                             (+ ordering.min_degree_order               ordering.py:19)
+ *   kkt_symbolic_export    <- the LuFactors hand-off object               direct_lu.py:51-81
+ *   kkt_dev_refactor       <- direct_lu.refactorize(factors, A_new)      direct_lu.py:297
+ *   kkt_dev_solve          <- direct_lu.lu_solve(factors, b)             direct_lu.py:359
+ *   kkt_dev_spmv           <- sparsecore.spmv(K, x)                      sparsecore.py:284
+ *   kkt_dev_residual_norms <- refine.nsr / nrbe / needs_refinement       refine.py:62-92
+ *   kkt_dev_fgmres         <- krylov.fgmres(K, M=lu_solve, b, x0, cfg)   krylov.py:117
+ *   kkt_dev_refine_fgmres  <- refine.refine_fgmres(K, f, x0, r, cfg)     refine.py:103
+ */
+#ifndef KKTB200_H
+#define KKTB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mirrored by the facade's exception mapping) ---- */
+enum {
+  KKT_OK = 0,
+  KKT_ERR_SINGULAR = 1,         /* SingularMatrixError        direct_lu.py:35  */
+  KKT_ERR_PATTERN_MISMATCH = 2, /* PatternMismatchError       direct_lu.py:39  */
+  KKT_ERR_BAD_SHAPE = 3,        /* ValueError (shape / argument)               */
+  KKT_ERR_NONFINITE = 4,        /* OperatorOutputError        krylov.py:28     */
+  KKT_ERR_CUDA = 5,             /* CUDA runtime failure                        */
+  KKT_ERR_OOM = 6,              /* allocation failure                          */
+  KKT_ERR_BAD_ARG = 7           /* ValueError (config validation)              */
+};
+
+const char *kkt_last_error(void);
+int kkt_abi_version(void);
+
+/* ======================================================================
+ * Host analysis (stays on the CPU, bit-exact with the reference).
+ * ====================================================================== */
+typedef struct kkt_symbolic kkt_symbolic;
+
+/* Sizes reported by kkt_symbolic_sizes(), in this order. */
+enum {
+  KKT_SZ_N = 0,   /* n                                   */
+  KKT_SZ_NNZ_A,   /* nnz of the general input pattern    */
+  KKT_SZ_NNZ_L,   /* strict L entries  (_Li/_Lx)         */
+  KKT_SZ_NNZ_U,   /* strict U entries  (_Ui/_Ux)         */
+  KKT_SZ_NSO,     /* replay schedule   (_so_data)        */
+  KKT_SZ_NAP,     /* A-scatter map     (_a_src/_a_tgt)   */
+  KKT_SZ_COUNT
+};
+
+/* factorize(): A is GENERAL CSR (row_ptr[n+1], col_idx[nnz] sorted+unique per row,
+ * values[nnz]).  Runs min_degree_order + left-looking Gilbert-Peierls LU with threshold
+ * partial pivoting (pivot_tol in (0,1]) exactly as direct_lu.py:116-294.
+ * On KKT_ERR_SINGULAR, *out is NULL and kkt_last_error() names the column. */
+int kkt_analyze(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                const double *values, double pivot_tol, kkt_symbolic **out);
+
+/* Ordering only: min_degree_order(A) (ordering.py:19-59) -> perm[n]. */
+int kkt_min_degree_order(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                         int64_t *perm_out);
+
+void kkt_symbolic_free(kkt_symbolic *s);
+int kkt_symbolic_sizes(const kkt_symbolic *s, int64_t sizes[KKT_SZ_COUNT]);
+
+/* Copy the LuFactors arrays out (caller allocates with the reported sizes).
+ * Any pointer may be NULL to skip that array. */
+int kkt_symbolic_export(const kkt_symbolic *s, int64_t *row_perm, int64_t *col_perm,
+                        int64_t *Lp, int64_t *Li, double *Lx,
+                        int64_t *Up, int64_t *Ui, double *Ux, double *Udiag,
+                        int64_t *so_ptr, int64_t *so_data,
+                        int64_t *ap_ptr, int64_t *a_src, int64_t *a_tgt);
+
+/* LuDiagnostics of the first factorization: {max|u_jj|, min|u_jj|, patched, growth}. */
+int kkt_symbolic_diag(const kkt_symbolic *s, double diag[4]);
+
+/* Schedule statistics: {refactor levels, L-solve levels, U-solve levels,
+ * refactor update pairs (F/2), max |so(j)|, max L col, max U col, max L row, max U row}. */
+int kkt_symbolic_stats(const kkt_symbolic *s, int64_t stats[9]);
+
+/* ======================================================================
+ * Device handle: one GPU, one stream, all buffers allocated once.
+ * ====================================================================== */
+typedef struct kkt_device kkt_device;
+
+/* Input value layout for kkt_dev_refactor / operator values. */
+enum { KKT_LAYOUT_GENERAL = 0, KKT_LAYOUT_SYMMETRIC_LOWER = 1 };
+
+typedef struct {
+  int device;             /* CUDA ordinal                                  */
+  int batch;              /* number of same-pattern systems held (>=1)     */
+  int restart_m;          /* FGMRES restart length the workspace is sized for */
+  int trisolve_mode;      /* 0 = ordered (bitwise with lu_solve), 1 = fast */
+  int flags;              /* reserved, 0                                   */
+} kkt_device_opts;
+
+/* Create the device handle from the host analysis.  A_row_ptr/A_col_idx repeat the
+ * general pattern that was analysed (checked).  lower_nnz / gen_src (optional, may be
+ * 0 / NULL) describe the symmetric-lower storage of the same matrix: general entry e holds
+ * lower value gen_src[e] (the to_general map, sparsecore.py:263-273).  With it, values may
+ * be passed in KKT_LAYOUT_SYMMETRIC_LOWER (half the upload) and the operator is applied in
+ * the reference's symmetric-lower spmv order (sparsecore.py:296-302). */
+int kkt_dev_create(const kkt_symbolic *s, const int64_t *A_row_ptr, const int64_t *A_col_idx,
+                   int64_t lower_nnz, const int64_t *gen_src, const kkt_device_opts *opts,
+                   kkt_device **out);
+void kkt_dev_destroy(kkt_device *d);
+
+/* Raw CUDA stream (cudaStream_t) the handle launches on. */
+void *kkt_dev_stream(kkt_device *d);
+
+/* Upload new values (host or device pointer; nnz doubles of the given layout) and
+ * refactorize on the frozen schedule (direct_lu.py:297-356).  The same values become the
+ * operator of kkt_dev_spmv / fgmres (general layout => general spmv order).
+ * diag_out (host, may be NULL) receives {max|u|, min|u|, patched, growth}. */
+int kkt_dev_refactor(kkt_device *d, const double *values_in, int layout, int values_on_device,
+                     double *diag_out);
+
+/* Operator-only value update (SpMV / FGMRES operator) without refactorizing. */
+int kkt_dev_set_operator_values(kkt_device *d, const double *values_in, int layout,
+                                int values_on_device);
+
+/* x = lu_solve(b) (direct_lu.py:359-379).  b, x: n*batch doubles, device pointers. */
+int kkt_dev_solve(kkt_device *d, const double *b_dev, double *x_dev);
+
+/* y = K x on the operator values (sparsecore.py:284-305).  Device pointers. */
+int kkt_dev_spmv(kkt_device *d, const double *x_dev, double *y_dev);
+
+/* Residual statistics for r - K x (device pointers, batch systems):
+ * out[batch][6] = {||r-Kx||_2, ||r-Kx||_inf, ||x||_2, ||x||_inf, ||r||_2, ||K||_inf}. */
+int kkt_dev_residual_norms(kkt_device *d, const double *r_dev, const double *x_dev,
+                           double *out_host);
+
+typedef struct {
+  int m;                  /* restart length                  (krylov.py:61) */
+  int max_outer;          /* restart cycles                  (krylov.py:62) */
+  double tol;             /* relative tolerance              (krylov.py:63) */
+  double delta_tol;       /* refinement trigger (refine only; refine.py:35) */
+} kkt_krylov_cfg;
+
+typedef struct {
+  int iterations;         /* KrylovResult.iterations          */
+  int converged;          /* KrylovResult.converged           */
+  int precond_applications;
+  int restarts;           /* number of restart cycles run      */
+  double beta0;           /* est_residual_history[0]           */
+  double est_final;       /* est_residual_history[-1]          */
+  double true_final;      /* KrylovResult.true_final_residual  */
+  int triggered;          /* refine only                       */
+  int nonfinite;          /* a NaN/Inf was produced            */
+} kkt_krylov_report;
+
+/* FGMRES(m) with CGS2, K = operator values, M = lu_solve with the current factors
+ * (krylov.py:117-208).  Device pointers; batch==1.  history_host (may be NULL) gets
+ * up to hist_cap estimated residuals (est_residual_history). */
+int kkt_dev_fgmres(kkt_device *d, const double *b_dev, const double *x0_dev, double *x_dev,
+                   const kkt_krylov_cfg *cfg, kkt_krylov_report *rep,
+                   double *history_host, int hist_cap);
+
+/* refine_fgmres (refine.py:103-132): trigger on ||r-Kx0||_2 > delta*||r||_2, then
+ * FGMRES with tol = delta_tol.  Device pointers. */
+int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_dev,
+                          double *x_dev, const kkt_krylov_cfg *cfg, kkt_krylov_report *rep);
+
+/* The whole per-system hot path of harness._run_direct_family (harness.py:223-245):
+ * refactor(values) -> x0 = solve(r) -> refine_fgmres.  values/r on host or device. */
+int kkt_dev_step(kkt_device *d, const double *values_in, int layout, const double *r_in,
+                 double *x_out, int io_on_device, const kkt_krylov_cfg *cfg,
+                 kkt_krylov_report *rep, double *diag_out);
+
+/* Download the current factor values in the LuFactors layout (_Lx, _Ux, _Udiag). */
+int kkt_dev_download_factors(kkt_device *d, double *Lx, double *Ux, double *Udiag);
+
+/* ======================================================================
+ * Standalone operator (sparsecore.spmv / refine.nsr / refine.nrbe on a bare matrix).
+ * row_ptr/col_idx: CSR as stored (symmetric_lower != 0 => lower triangle incl. diagonal,
+ * applied with both halves exactly like sparsecore.py:296-302).
+ * ====================================================================== */
+typedef struct kkt_operator kkt_operator;
+int kkt_op_create(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                  int symmetric_lower, int device, kkt_operator **out);
+void kkt_op_destroy(kkt_operator *op);
+void *kkt_op_stream(kkt_operator *op);
+int kkt_op_set_values(kkt_operator *op, const double *values, int values_on_device);
+int kkt_op_spmv(kkt_operator *op, const double *x_dev, double *y_dev);
+/* out6 as kkt_dev_residual_norms */
+int kkt_op_residual_norms(kkt_operator *op, const double *r_dev, const double *x_dev,
+                          double *out_host);
+
+/* Kernel launches issued by this handle since creation (evidence counter). */
+int64_t kkt_dev_launch_count(kkt_device *d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KKTB200_H */

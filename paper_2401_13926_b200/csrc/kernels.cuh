@@ -1,0 +1,60 @@
+// sm_100a kernels of the per-system hot path.  FP64 CUDA-core work (there is no dense
+// contraction anywhere on this path, so tcgen05/TMEM do not apply).  All arithmetic that the
+// reference performs as numpy elementwise ops is written with explicit round-to-nearest
+// intrinsics and the TU is compiled with --fmad=false, so products and differences round
+// separately exactly like numpy's `x - (l*xk)`.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kkt {
+
+constexpr int WARP = 32;
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
+
+__device__ __forceinline__ unsigned long long dbits(double v) {
+  return (unsigned long long)__double_as_longlong(v);
+}
+
+// Max / min of non-negative doubles via their (monotone) bit patterns.
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long *a, double v) {
+  if (v > 0.0) atomicMax(a, dbits(v));
+}
+__device__ __forceinline__ void atomic_min_nonneg(unsigned long long *a, double v) {
+  atomicMin(a, dbits(v));
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Fixed-shape (deterministic) block sum of `v` across blockDim.x threads.
+template <int BLOCK>
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = (l < BLOCK / 32) ? sh[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  return r;  // valid in thread 0
+}
+
+}  // namespace kkt

@@ -1,0 +1,185 @@
+// Host-side construction of the device execution plan from the analysis (one-time, part of
+// kkt_dev_create).  Everything here is integer bookkeeping over the frozen pattern:
+//   * refactor: column dispatch order (by DAG level), per-column workspace slots, the
+//     relative slot of every update pair (uint16), A-scatter slots, CSC->CSR value maps;
+//   * trisolves: CSR of L (ascending columns) and U (descending columns, so the reference's
+//     descending-j accumulation order is a forward walk), row dispatch order by level;
+//   * SpMV: split point of each general row so the reference's symmetric-lower bincount
+//     order (sparsecore.py:296-302) is reproduced.
+#include "plan.h"
+
+#include <algorithm>
+#include <numeric>
+
+namespace kkt {
+
+static std::vector<int32_t> order_by_level(const std::vector<int32_t> &lev) {
+  const int64_t n = (int64_t)lev.size();
+  int32_t nl = 0;
+  for (int32_t l : lev) nl = std::max(nl, l + 1);
+  std::vector<int64_t> cnt(nl + 1, 0);
+  for (int32_t l : lev) cnt[l + 1]++;
+  for (int32_t l = 0; l < nl; ++l) cnt[l + 1] += cnt[l];
+  std::vector<int32_t> out(n);
+  for (int64_t i = 0; i < n; ++i) out[cnt[lev[i]]++] = (int32_t)i;  // stable: ascending within level
+  return out;
+}
+
+int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int64_t in_nnz,
+               const int64_t *gen_src, HostPlan &P) {
+  const int64_t n = S.n;
+  if (n >= (int64_t)INT32_MAX / 2) return set_error(KKT_ERR_BAD_SHAPE, "n too large for int32 plan");
+  P = HostPlan();
+  P.n = (int32_t)n;
+  const int64_t nnz = S.nnz_a;
+  for (int64_t i = 0; i <= n; ++i)
+    if (A_rp[i] != S.A_row_ptr[i])
+      return set_error(KKT_ERR_PATTERN_MISMATCH, "operator pattern differs from the analysed one");
+  for (int64_t p = 0; p < nnz; ++p)
+    if (A_ci[p] != S.A_col_idx[p])
+      return set_error(KKT_ERR_PATTERN_MISMATCH, "operator pattern differs from the analysed one");
+  P.nnz_a = nnz;
+  P.in_nnz = in_nnz;
+  P.A_rp.assign(A_rp, A_rp + n + 1);
+  P.A_ci.assign(A_ci, A_ci + nnz);
+  P.gen_src.assign(nnz, 0);
+  P.has_lower = gen_src != nullptr && in_nnz > 0;
+  if (P.has_lower) {
+    for (int64_t e = 0; e < nnz; ++e) {
+      if (gen_src[e] < 0 || gen_src[e] >= in_nnz)
+        return set_error(KKT_ERR_BAD_SHAPE, "gen_src index out of range");
+      P.gen_src[e] = gen_src[e];
+    }
+  } else {
+    P.in_nnz = 0;
+  }
+  // SpMV split: first entry with col > row (symmetric-lower operators sum the halves apart).
+  P.A_split.resize(n);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t p = A_rp[i];
+    while (p < A_rp[i + 1] && A_ci[p] <= i) ++p;
+    P.A_split[i] = p;
+  }
+
+  // ---------------- refactor ----------------
+  const int64_t nL = (int64_t)S.Li.size(), nU = (int64_t)S.Ui.size();
+  P.Lp.assign(S.Lp.begin(), S.Lp.end());
+  P.Up.assign(S.Up.begin(), S.Up.end());
+  P.row_perm.assign(S.row_perm.begin(), S.row_perm.end());
+  P.col_perm.assign(S.col_perm.begin(), S.col_perm.end());
+  P.nnz_L = nL;
+  P.nnz_U = nU;
+  // column workspace = U rows (ascending), the diagonal, L rows (ascending): sorted positions
+  std::vector<int32_t> pos2slot(n, -1);
+  P.so_ptr.assign(S.so_ptr.begin(), S.so_ptr.end());
+  const int64_t nso = (int64_t)S.so_data.size();
+  P.so_data.resize(nso);
+  P.so_slot.resize(nso);
+  P.upd_ptr.resize(nso + 1);
+  int64_t pairs = 0;
+  for (int64_t t = 0; t < nso; ++t) {
+    int64_t k = S.so_data[t];
+    pairs += S.Lp[k + 1] - S.Lp[k];
+  }
+  if (pairs >= (int64_t)INT32_MAX) return set_error(KKT_ERR_BAD_SHAPE, "too many update pairs");
+  P.upd_slot.resize(pairs);
+  P.ap_ptr.assign(S.ap_ptr.begin(), S.ap_ptr.end());
+  P.a_src.resize(S.a_src.size());
+  P.a_slot.resize(S.a_src.size());
+  int32_t maxpat = 1;
+  int64_t u = 0;
+  std::vector<int32_t> lev(n, 0);
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t nu = S.Up[j + 1] - S.Up[j], nl = S.Lp[j + 1] - S.Lp[j];
+    const int64_t np = nu + 1 + nl;
+    if (np > 65535) return set_error(KKT_ERR_BAD_SHAPE, "column pattern exceeds 65535 slots");
+    maxpat = std::max<int32_t>(maxpat, (int32_t)np);
+    for (int64_t s = 0; s < nu; ++s) pos2slot[S.Ui[S.Up[j] + s]] = (int32_t)s;
+    pos2slot[j] = (int32_t)nu;
+    for (int64_t s = 0; s < nl; ++s) pos2slot[S.Li[S.Lp[j] + s]] = (int32_t)(nu + 1 + s);
+    int32_t l = 0;
+    for (int64_t t = S.so_ptr[j]; t < S.so_ptr[j + 1]; ++t) {
+      const int64_t k = S.so_data[t];
+      l = std::max(l, lev[k] + 1);
+      P.so_data[t] = (int32_t)k;
+      P.so_slot[t] = (uint16_t)pos2slot[k];
+      P.upd_ptr[t] = (int32_t)u;
+      for (int64_t p = S.Lp[k]; p < S.Lp[k + 1]; ++p) {
+        int32_t s = pos2slot[S.Li[p]];
+        if (s < 0) return set_error(KKT_ERR_BAD_SHAPE, "replay schedule leaves column pattern");
+        P.upd_slot[u++] = (uint16_t)s;
+      }
+    }
+    lev[j] = l;
+    for (int64_t q = S.ap_ptr[j]; q < S.ap_ptr[j + 1]; ++q) {
+      P.a_src[q] = (int32_t)S.a_src[q];
+      int32_t s = pos2slot[S.a_tgt[q]];
+      if (s < 0) return set_error(KKT_ERR_BAD_SHAPE, "A entry outside column pattern");
+      P.a_slot[q] = (uint16_t)s;
+    }
+    for (int64_t s = 0; s < nu; ++s) pos2slot[S.Ui[S.Up[j] + s]] = -1;
+    pos2slot[j] = -1;
+    for (int64_t s = 0; s < nl; ++s) pos2slot[S.Li[S.Lp[j] + s]] = -1;
+  }
+  P.upd_ptr[nso] = (int32_t)u;
+  P.maxpat = maxpat;
+  P.col_order = order_by_level(lev);
+  P.refactor_levels = 0;
+  for (int32_t l : lev) P.refactor_levels = std::max(P.refactor_levels, l + 1);
+
+  // ---------------- trisolves: CSR of L (ascending cols) and U (descending cols) -------
+  P.Lrp.assign(n + 1, 0);
+  P.Urp.assign(n + 1, 0);
+  for (int64_t p = 0; p < nL; ++p) P.Lrp[S.Li[p] + 1]++;
+  for (int64_t p = 0; p < nU; ++p) P.Urp[S.Ui[p] + 1]++;
+  for (int64_t i = 0; i < n; ++i) {
+    P.Lrp[i + 1] += P.Lrp[i];
+    P.Urp[i + 1] += P.Urp[i];
+  }
+  P.Lci.resize(nL);
+  P.Lmap.resize(nL);
+  P.Uci.resize(nU);
+  P.Umap.resize(nU);
+  {
+    std::vector<int32_t> fill(P.Lrp.begin(), P.Lrp.end() - 1);
+    for (int64_t j = 0; j < n; ++j)  // ascending j => ascending columns per row
+      for (int64_t p = S.Lp[j]; p < S.Lp[j + 1]; ++p) {
+        int32_t q = fill[S.Li[p]]++;
+        P.Lci[q] = (int32_t)j;
+        P.Lmap[p] = q;
+      }
+    std::vector<int32_t> ufill(P.Urp.begin(), P.Urp.end() - 1);
+    for (int64_t j = n - 1; j >= 0; --j)  // descending j => descending columns per row
+      for (int64_t p = S.Up[j]; p < S.Up[j + 1]; ++p) {
+        int32_t q = ufill[S.Ui[p]]++;
+        P.Uci[q] = (int32_t)j;
+        P.Umap[p] = q;
+      }
+  }
+  // levels: L row r after every column j<r it references; U row r after every j>r.
+  std::vector<int32_t> levL(n, 0), levU(n, 0);
+  for (int64_t r = 0; r < n; ++r) {
+    int32_t l = 0;
+    for (int32_t p = P.Lrp[r]; p < P.Lrp[r + 1]; ++p) l = std::max(l, levL[P.Lci[p]] + 1);
+    levL[r] = l;
+  }
+  for (int64_t r = n - 1; r >= 0; --r) {
+    int32_t l = 0;
+    for (int32_t p = P.Urp[r]; p < P.Urp[r + 1]; ++p) l = std::max(l, levU[P.Uci[p]] + 1);
+    levU[r] = l;
+  }
+  P.L_order = order_by_level(levL);
+  P.U_order = order_by_level(levU);
+  P.L_levels = 0;
+  P.U_levels = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    P.L_levels = std::max(P.L_levels, levL[i] + 1);
+    P.U_levels = std::max(P.U_levels, levU[i] + 1);
+  }
+  P.Lx0.assign(S.Lx.begin(), S.Lx.end());
+  P.Ux0.assign(S.Ux.begin(), S.Ux.end());
+  P.Udiag0.assign(S.Udiag.begin(), S.Udiag.end());
+  return KKT_OK;
+}
+
+}  // namespace kkt

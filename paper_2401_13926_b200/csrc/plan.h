@@ -1,0 +1,32 @@
+// Host-side device execution plan (built once in kkt_dev_create; see plan.cpp).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "kkt_internal.h"
+
+namespace kkt {
+
+struct HostPlan {
+  int32_t n = 0;
+  int64_t nnz_a = 0, in_nnz = 0, nnz_L = 0, nnz_U = 0;
+  int has_lower = 0;
+  // operator (general CSR) + value expansion + SpMV split points
+  std::vector<int64_t> A_rp, A_ci, gen_src, A_split;
+  // factors (CSC, position space) and permutations
+  std::vector<int64_t> Lp, Up, row_perm, col_perm;
+  std::vector<double> Lx0, Ux0, Udiag0;
+  // refactor schedule
+  std::vector<int64_t> so_ptr, ap_ptr;
+  std::vector<int32_t> so_data, upd_ptr, a_src, col_order;
+  std::vector<uint16_t> so_slot, upd_slot, a_slot;
+  int32_t maxpat = 1, refactor_levels = 0;
+  // trisolve CSR (L ascending cols, U descending cols) + CSC->CSR maps
+  std::vector<int32_t> Lrp, Lci, Lmap, Urp, Uci, Umap, L_order, U_order;
+  int32_t L_levels = 0, U_levels = 0;
+};
+
+int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int64_t in_nnz,
+               const int64_t *gen_src, HostPlan &P);
+
+}  // namespace kkt

@@ -1,0 +1,288 @@
+"""Python owners of the device handles (``kkt_device`` / ``kkt_operator``).
+
+PyTorch is used only as the device-memory allocator: buffers are torch tensors whose raw
+pointers go through the C ABI, and all copies are issued on the library's own CUDA stream
+(wrapped as a ``torch.cuda.ExternalStream``) so they order with the kernels.  There is no
+CPU path: constructing a handle without a CUDA device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .sparse import SYMMETRIC_LOWER, CsMatrix, lower_map
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("kktb200: no CUDA device visible; the solver path runs on the GPU "
+                           "only (there is no CPU fallback)")
+    return torch
+
+
+def _vp(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())
+
+
+@dataclass
+class ResidualStats:
+    """Norms of e = r - K x (kkt_dev_residual_norms)."""
+
+    err2: float
+    err_inf: float
+    x2: float
+    x_inf: float
+    r2: float
+    k_inf: float
+
+    def nsr(self) -> float:  # refine.py:62-73
+        den = self.k_inf * self.x_inf
+        return float("inf") if den == 0.0 else self.err_inf / den
+
+    def nrbe(self) -> float:  # refine.py:76-85
+        den = self.k_inf * self.x2 + self.r2
+        return float("inf") if den == 0.0 else self.err2 / den
+
+
+class DeviceSystem:
+    """One factorized pattern resident on one GPU: refactor / solve / spmv / FGMRES."""
+
+    def __init__(self, factors, restart_m: int = 10, device: int = 0):
+        torch = _torch()
+        self.lib = nat.load()
+        self.torch = torch
+        self.n = factors.n
+        G = factors._pattern_ref
+        self.pattern = G
+        lm = lower_map(G)
+        self.lower = lm  # (row_ptr, col_idx, gen_src) or None (structurally unsymmetric)
+        opts = nat.DeviceOpts(device=device, batch=1, restart_m=int(restart_m), trisolve_mode=0,
+                              flags=0)
+        h = C.c_void_p()
+        rp = np.ascontiguousarray(G.row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(G.col_idx, dtype=np.int64)
+        if lm is not None:
+            gs = np.ascontiguousarray(lm[2], dtype=np.int64)
+            nat.check(self.lib.kkt_dev_create(factors._sym.ptr, nat.ptr_i64(rp), nat.ptr_i64(ci),
+                                              int(lm[1].size), nat.ptr_i64(gs), C.byref(opts),
+                                              C.byref(h)), "kkt_dev_create")
+        else:
+            nat.check(self.lib.kkt_dev_create(factors._sym.ptr, nat.ptr_i64(rp), nat.ptr_i64(ci),
+                                              0, None, C.byref(opts), C.byref(h)),
+                      "kkt_dev_create")
+        self.h = h
+        self.device = torch.device("cuda", device)
+        self.stream = torch.cuda.ExternalStream(self.lib.kkt_dev_stream(h), device=self.device)
+        n = self.n
+        f64 = torch.float64
+        with torch.cuda.stream(self.stream):
+            self.b = torch.empty(n, dtype=f64, device=self.device)
+            self.x = torch.empty(n, dtype=f64, device=self.device)
+            self.x0 = torch.empty(n, dtype=f64, device=self.device)
+            self.r = torch.empty(n, dtype=f64, device=self.device)
+        self._op_key = None
+        self.nnz_L = int(factors._Li.size)
+        self.nnz_U = int(factors._Ui.size)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.kkt_dev_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------- host <-> device helpers (on the library stream) ----------------
+    def h2d(self, dst, a: np.ndarray):
+        t = self.torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+        with self.torch.cuda.stream(self.stream):
+            dst.copy_(t)
+
+    def d2h(self, src) -> np.ndarray:
+        with self.torch.cuda.stream(self.stream):
+            out = src.cpu()
+        return out.numpy()
+
+    def sync(self):
+        self.stream.synchronize()
+
+    # ---------------- matrix values ----------------
+    def _layout_of(self, A: CsMatrix):
+        if A.symmetry == SYMMETRIC_LOWER:
+            if self.lower is None:
+                raise ValueError("symmetric-lower values for a structurally unsymmetric pattern")
+            if not (np.array_equal(A.row_ptr, self.lower[0])
+                    and np.array_equal(A.col_idx, self.lower[1])):
+                from .direct_lu import PatternMismatchError
+                raise PatternMismatchError("refactorize: sparsity pattern differs from the "
+                                           "originally factorized matrix")
+            return nat.LAYOUT_SYMMETRIC_LOWER
+        if not A.same_pattern(self.pattern):
+            from .direct_lu import PatternMismatchError
+            raise PatternMismatchError("refactorize: sparsity pattern differs from the "
+                                       "originally factorized matrix")
+        return nat.LAYOUT_GENERAL
+
+    def refactor_matrix(self, A: CsMatrix):
+        from .direct_lu import LuDiagnostics
+        layout = self._layout_of(A)
+        vals = np.ascontiguousarray(A.values, dtype=np.float64)
+        dg = (C.c_double * 4)()
+        nat.check(self.lib.kkt_dev_refactor(self.h, vals.ctypes.data_as(C.c_void_p), layout, 0, dg),
+                  "kkt_dev_refactor")
+        self._op_key = (id(A.values), layout)
+        self._op_ref = A.values
+        return LuDiagnostics(max_abs_pivot=dg[0], min_abs_pivot=dg[1],
+                             zero_pivots_patched=int(dg[2]), growth_estimate=dg[3])
+
+    def refactor_device(self, values_t, layout: int):
+        """Refactorize from device-resident values (no host traffic, no sync)."""
+        nat.check(self.lib.kkt_dev_refactor(self.h, _vp(values_t), layout, 1, None),
+                  "kkt_dev_refactor")
+        self._op_key = None
+
+    def set_operator(self, K: CsMatrix):
+        """Make K the FGMRES / spmv operator (skips the upload when it is already current)."""
+        layout = self._layout_of(K)
+        key = (id(K.values), layout)
+        vals = np.ascontiguousarray(K.values, dtype=np.float64)
+        nat.check(self.lib.kkt_dev_set_operator_values(self.h, vals.ctypes.data_as(C.c_void_p),
+                                                       layout, 0), "set_operator_values")
+        self._op_key = key
+        self._op_ref = K.values
+
+    def download_factors(self):
+        Lx, Ux, Ud = np.empty(self.nnz_L), np.empty(self.nnz_U), np.empty(self.n)
+        nat.check(self.lib.kkt_dev_download_factors(self.h, nat.ptr_f64(Lx), nat.ptr_f64(Ux),
+                                                    nat.ptr_f64(Ud)))
+        return Lx, Ux, Ud
+
+    # ---------------- kernels ----------------
+    def solve_device(self, b_t, x_t):
+        nat.check(self.lib.kkt_dev_solve(self.h, _vp(b_t), _vp(x_t)), "kkt_dev_solve")
+
+    def solve_host(self, b: np.ndarray) -> np.ndarray:
+        self.h2d(self.b, b)
+        self.solve_device(self.b, self.x)
+        return self.d2h(self.x)
+
+    def spmv_device(self, x_t, y_t):
+        nat.check(self.lib.kkt_dev_spmv(self.h, _vp(x_t), _vp(y_t)), "kkt_dev_spmv")
+
+    def residual_stats_device(self, r_t, x_t) -> ResidualStats:
+        out = (C.c_double * 6)()
+        nat.check(self.lib.kkt_dev_residual_norms(self.h, _vp(r_t), _vp(x_t), out))
+        return ResidualStats(*list(out))
+
+    def fgmres_device(self, b_t, x0_t, x_t, m: int, max_outer: int, tol: float,
+                      hist_cap: int = 4096):
+        cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(tol), delta_tol=float(tol))
+        rep = nat.KrylovReport()
+        hist = (C.c_double * hist_cap)()
+        nat.check(self.lib.kkt_dev_fgmres(self.h, _vp(b_t), _vp(x0_t), _vp(x_t), C.byref(cfg),
+                                          C.byref(rep), hist, hist_cap), "kkt_dev_fgmres")
+        nh = min(rep.iterations + 1, hist_cap)
+        return rep, [hist[i] for i in range(nh)]
+
+    def step(self, values: np.ndarray | object, layout: int, r, x_out, on_device: bool,
+             m: int, max_outer: int, delta_tol: float):
+        """refactor -> solve -> refine_fgmres in one C call (kkt_dev_step)."""
+        cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(delta_tol),
+                            delta_tol=float(delta_tol))
+        rep = nat.KrylovReport()
+        if on_device:
+            args = (_vp(values), layout, _vp(r), _vp(x_out), 1)
+        else:
+            args = (values.ctypes.data_as(C.c_void_p), layout, r.ctypes.data_as(C.c_void_p),
+                    x_out.ctypes.data_as(C.c_void_p), 0)
+        nat.check(self.lib.kkt_dev_step(self.h, *args, C.byref(cfg), C.byref(rep), None),
+                  "kkt_dev_step")
+        self._op_key = None
+        return rep
+
+    def launch_count(self) -> int:
+        return int(self.lib.kkt_dev_launch_count(self.h))
+
+
+class DeviceOperator:
+    """A bare matrix on the device (sparsecore.spmv / nsr / nrbe without factors)."""
+
+    def __init__(self, A: CsMatrix, device: int = 0):
+        torch = _torch()
+        self.torch = torch
+        self.lib = nat.load()
+        self.n = A.n_rows
+        if A.n_rows != A.n_cols:
+            raise ValueError("operator matrices must be square")
+        rp = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(A.col_idx, dtype=np.int64)
+        h = C.c_void_p()
+        nat.check(self.lib.kkt_op_create(A.n_rows, nat.ptr_i64(rp), nat.ptr_i64(ci),
+                                         1 if A.symmetry == SYMMETRIC_LOWER else 0, device,
+                                         C.byref(h)), "kkt_op_create")
+        self.h = h
+        self.pattern = (A.row_ptr, A.col_idx, A.symmetry)
+        self.device = torch.device("cuda", device)
+        self.stream = torch.cuda.ExternalStream(self.lib.kkt_op_stream(h), device=self.device)
+        with torch.cuda.stream(self.stream):
+            self.a = torch.empty(self.n, dtype=torch.float64, device=self.device)
+            self.b = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        self._vals_ref = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.kkt_op_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_values(self, values: np.ndarray):
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        nat.check(self.lib.kkt_op_set_values(self.h, v.ctypes.data_as(C.c_void_p), 0))
+        self._vals_ref = values
+
+    def _h2d(self, dst, a):
+        with self.torch.cuda.stream(self.stream):
+            dst.copy_(self.torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)))
+
+    def spmv(self, x: np.ndarray) -> np.ndarray:
+        self._h2d(self.a, x)
+        nat.check(self.lib.kkt_op_spmv(self.h, _vp(self.a), _vp(self.b)))
+        with self.torch.cuda.stream(self.stream):
+            return self.b.cpu().numpy()
+
+    def residual_stats(self, r: np.ndarray, x: np.ndarray) -> ResidualStats:
+        self._h2d(self.a, r)
+        self._h2d(self.b, x)
+        out = (C.c_double * 6)()
+        nat.check(self.lib.kkt_op_residual_norms(self.h, _vp(self.a), _vp(self.b), out))
+        return ResidualStats(*list(out))
+
+
+_OPS: dict = {}
+
+
+def operator_for(A: CsMatrix) -> DeviceOperator:
+    """Device operator cached per pattern object (values refreshed on identity change)."""
+    key = (id(A.row_ptr), id(A.col_idx), A.symmetry)
+    op = _OPS.get(key)
+    if op is None or op.pattern[0] is not A.row_ptr:
+        if len(_OPS) > 16:
+            for k in list(_OPS)[:8]:
+                _OPS.pop(k).close()
+        op = DeviceOperator(A)
+        _OPS[key] = op
+    op.set_values(A.values)
+    return op

@@ -1,0 +1,143 @@
+"""Drop-in for ``kktsolve.refine``: FGMRES iterative refinement on the B200.
+
+``refine_fgmres`` follows refine.py:103-132 step for step — trigger, NSR before, FGMRES
+with the (stale) LU factors as right preconditioner and ``tol = delta_tol``, NSR/NRBE after —
+with every vector operation on the device.  The quality metrics come from one fused device
+pass (``kkt_dev_residual_norms``) instead of separate host spmv calls.
+
+Barrier-tied tolerance (the north star's extension; the reference fixes ``delta_tol``,
+SURVEY.md §5): :class:`BarrierTiedTolerance` maps the interior-point parameter mu to
+``delta(mu) = clamp(theta * mu, delta_min, delta_max)``; :class:`FixedTolerance` is the
+reference behaviour and the parity default.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from .krylov import KrylovConfig
+
+NSR_RATIO = "nsr_ratio"
+TOLERANCE = "tolerance"
+
+
+@dataclass
+class RefinementConfig:
+    """Trigger tolerance + per-method knobs (refine.py:26-45)."""
+
+    delta_tol: float = 1e-9
+    krylov: KrylovConfig = field(default_factory=KrylovConfig)
+    richardson_max_steps: int = 10
+    richardson_stop: str = TOLERANCE
+    nsr_ratio_floor: float = 0.5
+
+    def __post_init__(self):
+        if self.delta_tol <= 0:
+            raise ValueError("delta_tol must be positive")
+        if self.richardson_stop not in (TOLERANCE, NSR_RATIO):
+            raise ValueError(f"unknown richardson_stop {self.richardson_stop!r}")
+
+
+@dataclass
+class RefinementReport:
+    triggered: bool
+    method: str
+    ir_iterations: int
+    triangular_solves_used: int
+    nsr_before: float
+    nsr_after: float
+    rr_final: float
+    nrbe_final: float
+    converged: bool
+    diverged: bool = False
+
+
+@dataclass(frozen=True)
+class FixedTolerance:
+    """The reference policy: one delta for every system."""
+
+    delta: float = 1e-9
+
+    def __call__(self, mu: float | None = None) -> float:
+        return self.delta
+
+
+@dataclass(frozen=True)
+class BarrierTiedTolerance:
+    """delta(mu) = clamp(theta * mu, delta_min, delta_max).
+
+    Loose while the barrier parameter is large (early, well-conditioned systems need no
+    refinement), tight as mu -> 0 where the static-pivot factors degrade.
+    """
+
+    theta: float = 1e-6
+    delta_min: float = 1e-14
+    delta_max: float = 1e-8
+
+    def __post_init__(self):
+        if not (self.theta > 0 and 0 < self.delta_min <= self.delta_max):
+            raise ValueError("need theta > 0 and 0 < delta_min <= delta_max")
+
+    def __call__(self, mu: float | None = None) -> float:
+        if mu is None:
+            return self.delta_max
+        return float(min(max(self.theta * float(mu), self.delta_min), self.delta_max))
+
+
+def config_for_mu(cfg: RefinementConfig, policy, mu: float | None) -> RefinementConfig:
+    """The refinement config for one system of a barrier sequence."""
+    return replace(cfg, delta_tol=policy(mu))
+
+
+def _stats(K, x, r):
+    from .sparse_ops import residual_stats
+    return residual_stats(K, r, x)
+
+
+def nsr(K, x, r) -> float:
+    """||r - Kx||_inf / (||K||_inf ||x||_inf), +inf for a zero denominator (refine.py:62)."""
+    return _stats(K, x, r).nsr()
+
+
+def nrbe(K, x, r) -> float:
+    """||r - Kx||_2 / (||K||_inf ||x||_2 + ||r||_2) (refine.py:76)."""
+    return _stats(K, x, r).nrbe()
+
+
+def needs_refinement(K, x0, r, delta_tol: float) -> bool:
+    """||r - K x0||_2 > delta_tol * ||r||_2 (refine.py:88)."""
+    s = _stats(K, x0, r)
+    return s.err2 > delta_tol * s.r2
+
+
+def refine_fgmres(K, factors, x0, r, cfg: RefinementConfig):
+    """FGMRES refinement of a direct solve, LU factors as right preconditioner (refine.py:103)."""
+    x0 = np.asarray(x0, dtype=np.float64)
+    r = np.asarray(r, dtype=np.float64)
+    dev = factors.device(restart_m=cfg.krylov.m)
+    dev.set_operator(K)
+    dev.h2d(dev.r, r)
+    dev.h2d(dev.x0, x0)
+    s0 = dev.residual_stats_device(dev.r, dev.x0)
+    if not (s0.err2 > cfg.delta_tol * s0.r2):
+        q = s0.nsr()
+        return x0.copy(), RefinementReport(
+            triggered=False, method="none", ir_iterations=0, triangular_solves_used=0,
+            nsr_before=q, nsr_after=q, rr_final=1.0, nrbe_final=s0.nrbe(), converged=True)
+    if cfg.krylov.ortho != "cgs2":
+        raise NotImplementedError("the device Arnoldi step implements CGS2")
+    count0 = factors.triangular_solve_count
+    kcfg = replace(cfg.krylov, tol=cfg.delta_tol)
+    rep, hist = dev.fgmres_device(dev.r, dev.x0, dev.x, kcfg.m, kcfg.max_outer, kcfg.tol)
+    factors.triangular_solve_count += rep.precond_applications
+    s1 = dev.residual_stats_device(dev.r, dev.x)
+    x = dev.d2h(dev.x)
+    rho0 = hist[0]
+    rr_final = (hist[-1] / rho0) if rho0 > 0 else 0.0
+    return x, RefinementReport(
+        triggered=True, method="fgmres", ir_iterations=rep.iterations,
+        triangular_solves_used=factors.triangular_solve_count - count0,
+        nsr_before=s0.nsr(), nsr_after=s1.nsr(), rr_final=rr_final, nrbe_final=s1.nrbe(),
+        converged=bool(rep.converged))

@@ -1,0 +1,194 @@
+"""GPU parity: the sm_100a path vs the reference's recorded outputs (tests/golden/*.npz).
+
+Bars (BASELINE.json north star + SURVEY.md §7 hard part 5):
+* refactorize: factor values BITWISE equal (the spec allows 1e-12 relative; the ordered,
+  non-FMA device replay reproduces direct_lu.py:297-356 exactly), diagnostics exact;
+* lu_solve: BITWISE (ordered row accumulation == the column sweep of direct_lu.py:369-377);
+* spmv: BITWISE (the reference's symmetric-lower bincount order);
+* FGMRES-IR: same trigger decision, iteration counts within +-1, and final relative
+  residual rr <= max(1.5 * rr_ref, 4 eps) per system (dot products are tree-reduced on the
+  device, which the survey measured to cost up to 1.5x rr at the rounding floor).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, lower_matrix
+from paper_2401_13926_b200 import (KrylovConfig, LinearOperator, OperatorOutputError,
+                                   PatternMismatchError, RefinementConfig, factorize, fgmres,
+                                   from_dense, lu_preconditioner, lu_solve, refactorize,
+                                   refine_fgmres, spmv, to_general)
+from paper_2401_13926_b200.sparse import CsMatrix
+
+pytestmark = pytest.mark.gpu
+EPS = np.finfo(float).eps
+SEQS = ["standard_trace", "acopf_tiny", "acopf_small"]
+
+
+def _rr(K, x, r):
+    M = K.to_dense() if K.n_rows <= 3000 else None
+    if M is None:
+        return None
+    return np.linalg.norm(r - M @ x) / np.linalg.norm(r)
+
+
+@pytest.mark.parametrize("case", SEQS)
+def test_refactorize_bitwise(case):
+    g = golden(case)
+    f, _ = factorize(to_general(lower_matrix(g, 0)))
+    M = g["K_values"].shape[0]
+    for i in range(M):
+        K = lower_matrix(g, i)
+        d = refactorize(f, to_general(K))
+        assert np.array_equal([d.max_abs_pivot, d.min_abs_pivot, d.zero_pivots_patched,
+                               d.growth_estimate], g["refactor_diag"][i]), i
+        if f"s{i}_Lx" in g:
+            assert np.array_equal(f._Lx, g[f"s{i}_Lx"]), i
+            assert np.array_equal(f._Ux, g[f"s{i}_Ux"]), i
+            assert np.array_equal(f._Udiag, g[f"s{i}_Udiag"]), i
+        # lu_solve after each refactorization: bitwise
+        x0 = lu_solve(f, g["rhs"][i])
+        assert np.array_equal(x0, g["x0"][i]), i
+    assert f.from_refactorization
+    assert f.triangular_solve_count == M
+
+
+@pytest.mark.parametrize("case", SEQS)
+def test_refactorize_symmetric_lower_input(case):
+    g = golden(case)
+    f, _ = factorize(to_general(lower_matrix(g, 0)))
+    last = g["K_values"].shape[0] - 1
+    refactorize(f, lower_matrix(g, last))  # values expanded on the device
+    assert np.array_equal(f._Lx, g[f"s{last}_Lx"])
+    assert np.array_equal(f._Ux, g[f"s{last}_Ux"])
+
+
+@pytest.mark.parametrize("case", SEQS)
+def test_spmv_bitwise(case):
+    g = golden(case)
+    for i in (0, g["K_values"].shape[0] - 1):
+        K = lower_matrix(g, i)
+        assert np.array_equal(spmv(K, g["x0"][i]), g["spmv_K_x0"][i])
+
+
+def test_random_sparse_solve_and_scaled_refactor():
+    g = golden("random_sparse")
+    for s in range(int(g["count"][0])):
+        rp = g[f"r{s}_row_ptr"]
+        n = rp.size - 1
+        A = CsMatrix(n, n, rp, g[f"r{s}_col_idx"], g[f"r{s}_values"])
+        f, _ = factorize(A)
+        assert np.array_equal(lu_solve(f, g[f"r{s}_b"]), g[f"r{s}_x"]), s
+        assert np.array_equal(spmv(A, g[f"r{s}_b"]), g[f"r{s}_spmv_b"]), s
+        d2 = refactorize(f, A.with_values(2.0 * A.values))
+        assert np.array_equal(f._Lx, g[f"r{s}_Lx2"]), s          # L unchanged bitwise
+        assert np.array_equal(f._Ux, g[f"r{s}_Ux2"]), s          # U exactly doubled
+        assert np.array_equal(f._Udiag, g[f"r{s}_Udiag2"]), s
+        assert np.array_equal(lu_solve(f, g[f"r{s}_b"]), g[f"r{s}_x2"]), s
+        assert np.array_equal([d2.max_abs_pivot, d2.min_abs_pivot, d2.zero_pivots_patched,
+                               d2.growth_estimate], g[f"r{s}_diag2"]), s
+
+
+def test_refactorize_unchanged_values_bitwise():
+    g = golden("random_sparse")
+    rp = g["r1_row_ptr"]
+    n = rp.size - 1
+    A = CsMatrix(n, n, rp, g["r1_col_idx"], g["r1_values"])
+    f, _ = factorize(A)
+    L0, U0, D0 = f._Lx.copy(), f._Ux.copy(), f._Udiag.copy()
+    refactorize(f, A)
+    assert np.array_equal(f._Lx, L0) and np.array_equal(f._Ux, U0)
+    assert np.array_equal(f._Udiag, D0)
+
+
+def test_zero_pivot_patched():
+    g = golden("edge_cases")
+    A = from_dense(np.array([[2.0, 1.0], [1.0, 2.0]]))
+    f, _ = factorize(A)
+    d = refactorize(f, from_dense(np.array([[2.0, 1.0], [1.0, 0.5]])))
+    assert d.zero_pivots_patched == 1 and d.min_abs_pivot > 0
+    assert np.array_equal([d.max_abs_pivot, d.min_abs_pivot, d.zero_pivots_patched,
+                           d.growth_estimate], g["patch_diag"])
+    assert np.array_equal(f._Udiag, g["patch_Udiag"])
+    assert np.array_equal(lu_solve(f, np.array([1.0, -1.0])), g["patch_x"])
+
+
+def test_pattern_mismatch():
+    A = from_dense(np.array([[2.0, 1.0], [1.0, 2.0]]))
+    f, _ = factorize(A)
+    with pytest.raises(PatternMismatchError):
+        refactorize(f, from_dense(np.array([[2.0, 0.0], [1.0, 2.0]])))
+
+
+@pytest.mark.parametrize("case", SEQS)
+@pytest.mark.parametrize("delta", [1e-10, 1e-14])
+def test_refine_fgmres_matches_reference(case, delta):
+    g = golden(case)
+    tag = f"{delta:.0e}"
+    ref = g[f"refine_{tag}_report"]
+    f, _ = factorize(to_general(lower_matrix(g, 0)))
+    cfg = RefinementConfig(delta_tol=delta, krylov=KrylovConfig(m=10))
+    for i in range(g["K_values"].shape[0]):
+        K = lower_matrix(g, i)
+        r = g["rhs"][i]
+        refactorize(f, to_general(K))
+        x0 = lu_solve(f, r)
+        c0 = f.triangular_solve_count
+        x, rep = refine_fgmres(K, f, x0, r, cfg)
+        trig, iters = bool(ref[i, 0]), int(ref[i, 1])
+        assert rep.triggered == trig, (i, rep)
+        assert abs(rep.ir_iterations - iters) <= 1, (i, rep.ir_iterations, iters)
+        assert rep.triangular_solves_used == f.triangular_solve_count - c0
+        if not trig:
+            assert np.array_equal(x, x0)
+            continue
+        assert rep.converged == bool(ref[i, 7])
+        rr_ref = _rr(K, g[f"refine_{tag}_x"][i], r)
+        rr = _rr(K, x, r)
+        if rr is not None:
+            assert rr <= max(1.5 * rr_ref, 4 * EPS), (i, rr, rr_ref)
+
+
+def test_fgmres_generic_entry_and_nan():
+    g = golden("acopf_tiny")
+    K = lower_matrix(g, 19)
+    f, _ = factorize(to_general(lower_matrix(g, 0)))
+    refactorize(f, to_general(K))
+    r = g["rhs"][19]
+    x0 = lu_solve(f, r)
+    res = fgmres(LinearOperator.from_matrix(K), lu_preconditioner(f), r, x0,
+                 KrylovConfig(m=10, tol=1e-12))
+    assert res.converged and res.precond_applications == res.iterations
+    assert res.est_residual_history[-1] <= 1e-12 * res.est_residual_history[0]
+    # perfect preconditioner: one iteration (test_krylov.py:61-69)
+    D = from_dense(np.diag([1.0, 2.0, 3.0, 4.0, 5.0]))
+    fd, _ = factorize(D)
+    b = np.random.default_rng(2).standard_normal(5)
+    res = fgmres(LinearOperator.from_matrix(D), lu_preconditioner(fd), b, np.zeros(5),
+                 KrylovConfig(tol=1e-12))
+    assert res.converged and res.iterations == 1
+    # exact x0: zero iterations (test_krylov.py:53-59)
+    res = fgmres(LinearOperator.from_matrix(D), lu_preconditioner(fd), b, b / np.arange(1, 6),
+                 KrylovConfig(tol=1e-10))
+    assert res.converged and res.iterations <= 1
+    # non-finite operator output -> OperatorOutputError (krylov.py:87-90)
+    bad = D.with_values(np.array([1.0, np.nan, 3.0, 4.0, 5.0]))
+    with pytest.raises(OperatorOutputError):
+        fgmres(LinearOperator.from_matrix(bad), lu_preconditioner(fd), b, np.zeros(5),
+               KrylovConfig())
+
+
+@pytest.mark.parametrize("case", ["standard_trace", "acopf_small"])
+def test_harness_rows_device_mode(case):
+    from paper_2401_13926_b200.harness import run_refactor_ir
+    g = golden(case)
+    M = g["K_values"].shape[0]
+    Ks = [lower_matrix(g, i) for i in range(M)]
+    cfg = RefinementConfig(delta_tol=1e-10, krylov=KrylovConfig(m=10))
+    ref = g["harness_1e-10"]
+    for mode in ("device", "dropin"):
+        rows, f = run_refactor_ir(Ks, list(g["rhs"]), cfg, mode=mode)
+        for i, row in enumerate(rows):
+            assert abs(row.ir_iterations - ref[i, 4]) <= 1, (mode, i)
+            assert row.rr <= max(1.5 * ref[i, 3], 4 * EPS), (mode, i, row.rr, ref[i, 3])
+            assert row.converged
