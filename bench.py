@@ -375,6 +375,7 @@ def main():
                 "analyze_s": analyze_s, "device_create_s": create_s, "generate_s": gen_s,
                 "parallelism": f"replicas/shards x{world}",
                 "step_ms": [round(x, 4) for x in step_ms],
+                "schedule": dev.info(),
             },
             "e2e": {"value": e2e_value, "unit": "ms/system",
                     "h2d_bytes_per_step": 8 * (nnz_lower + N), "d2h_bytes_per_step": 8 * N},

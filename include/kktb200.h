@@ -199,6 +199,11 @@ int kkt_op_spmv(kkt_operator *op, const double *x_dev, double *y_dev);
 int kkt_op_residual_norms(kkt_operator *op, const double *r_dev, const double *x_dev,
                           double *out_host);
 
+/* Schedule of the handle: {n, pL, pU, L grid levels, U grid levels, L tail rows, U head rows,
+ * refactor blocks, refactor warps/block, refactor smem bytes, trisolve grid blocks,
+ * refactor levels, arena bytes, update pairs, 0, 0}. */
+int kkt_dev_info(kkt_device *d, int64_t info[16]);
+
 /* Kernel launches issued by this handle since creation (evidence counter). */
 int64_t kkt_dev_launch_count(kkt_device *d);
 

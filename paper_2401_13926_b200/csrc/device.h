@@ -1,4 +1,5 @@
-// Device handle: every buffer the hot path needs, allocated once (one arena).
+// Device handle + the launch interface between the host orchestration (device.cu) and the
+// kernel translation units (refactor.cu, trisolve.cu, vector.cu).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -6,7 +7,14 @@
 
 namespace kkt {
 
-// Device-side view of the plan + workspaces.  int32 indices everywhere on the device.
+constexpr int RED_BLOCKS = 296;  // fixed => reductions are run-to-run deterministic
+constexpr int RED_THREADS = 256;
+constexpr double HAPPY_BREAKDOWN_RTOL = 1e-14;   // krylov.py:25
+constexpr double PATCH_RELATIVE_FLOOR = 1e-12;   // direct_lu.py:32
+constexpr int REFACTOR_STAGE = 512;              // update pairs staged per warp chunk
+constexpr int CTA_PHASE_THREADS = 1024;
+
+// Device-side view of the plan + workspaces.  int32 indices on the device.
 struct DevPlan {
   int n = 0, sym_lower = 0, has_lower = 0;
   int64_t nnz_a = 0, in_nnz = 0, nnz_L = 0, nnz_U = 0, n_so = 0, n_upd = 0, n_ap = 0;
@@ -15,16 +23,17 @@ struct DevPlan {
   int *A_rp, *A_ci, *A_split, *gen_src;
   double *in_vals, *A_vals;
   // refactor
-  int *so_ptr, *so_data, *upd_ptr, *ap_ptr, *a_src, *col_order, *Lp, *Up, *Lmap, *Umap;
-  uint16_t *so_slot, *upd_slot, *a_slot;
+  int *so_ptr, *ap_ptr, *a_src, *col_order, *Lp, *Up, *Lmap, *Umap, *upd_lidx;
+  int4 *so_meta;
+  uint16_t *upd_slot, *a_slot;
   double *Lx, *Ux, *udiag;
-  int *done;
   // trisolves
-  int *Lrp, *Lci, *Urp, *Uci, *L_order, *U_order, *row_perm, *col_perm;
+  int *Lrp, *Lci, *Urp, *Uci, *row_perm, *col_perm;
+  int *L_grid_order, *L_tail_order, *U_head_order, *U_grid_order;
+  int pL, pU, nLg, nUg;  // split positions and grid-phase row counts
   double *Lv, *Uv;
-  int *tflag;
-  double *y;
-  // scalar block (device): see Scal
+  double *yL, *yU;       // sentinel-reset solution buffers (value == readiness flag)
+  // scalars
   unsigned long long *scal;
   int *ticket;
   double *partials;
@@ -32,13 +41,14 @@ struct DevPlan {
 
 // indices into DevPlan::scal (bit patterns of non-negative doubles unless noted)
 enum {
-  SC_MAXABS_A = 0,    // max |a|
-  SC_INFNORM,         // ||A||_inf  (row sums in entry order)
-  SC_GMAX,            // growth numerator (refactorize)
-  SC_PATCHED,         // integer count
-  SC_MAXPIV,          // max |u_jj|
-  SC_MINPIV,          // min |u_jj|
-  SC_NONFINITE,       // integer flag
+  SC_MAXABS_A = 0,  // max |a|
+  SC_INFNORM,       // ||A||_inf of the general matrix (row sums in entry order)
+  SC_GMAX,          // growth numerator (refactorize)
+  SC_PATCHED,       // integer count
+  SC_MAXPIV,        // max |u_jj|
+  SC_MINPIV,        // min |u_jj|
+  SC_NONFINITE,     // integer flag
+  SC_OPNORM,        // ||K||_inf of the operator as the reference computes it
   SC_COUNT
 };
 
@@ -55,11 +65,29 @@ struct Device {
   int refactor_blocks = 0, refactor_warps = 8;
   size_t refactor_smem = 0;
   int trsv_blocks = 0;
-  int epoch_refactor = 0, epoch_trsv = 0;
   long long launches = 0;
   Krylov *kry = nullptr;
   double *pinned = nullptr;  // small pinned host staging buffer
   int restart_m = 10;
 };
+
+// ---- launchers (each returns cudaGetLastError of its launch) ----
+cudaError_t launch_expand_norms(const DevPlan &d, cudaStream_t s);
+cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem, cudaStream_t s);
+cudaError_t launch_diag_stats(const DevPlan &d, int blocks, cudaStream_t s);
+cudaError_t refactor_configure(int warps, size_t smem, int *blocks_per_sm);
+size_t refactor_smem_bytes(int warps, int maxpat);
+
+cudaError_t launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,
+                        cudaStream_t s, long long *launches);
+cudaError_t trsv_configure(int *grid_blocks_per_sm);
+cudaError_t launch_fill_sentinel(double *p, int64_t n, cudaStream_t s);
+
+cudaError_t launch_spmv(const DevPlan &d, const double *x, double *out, const double *bsub,
+                        double *nrm_partials, cudaStream_t s);
+cudaError_t launch_reduce_partials(const double *partials, int nvec, int nblk, double *out,
+                                   int op_sqrt, cudaStream_t s);
+cudaError_t launch_resid_stats(const DevPlan &d, const double *r, const double *x,
+                               double *partials, double *out5, cudaStream_t s);
 
 }  // namespace kkt

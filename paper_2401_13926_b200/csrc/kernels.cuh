@@ -21,6 +21,39 @@ __device__ __forceinline__ void st_release(int *p, int v) {
 }
 __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
 
+// ---- value-as-flag readiness ---------------------------------------------------------
+// Buffers that other warps wait on are reset to an all-ones NaN bit pattern (memset 0xFF).
+// Arithmetic never produces that pattern (canonical NaNs differ) and producers canonicalize
+// it away (`unsentinel`), so "value != sentinel" means "value published".  An aligned 8-byte
+// store is single-copy atomic, so no separate flag or fence is needed.
+constexpr unsigned long long SENTINEL_BITS = 0xFFFFFFFFFFFFFFFFull;
+
+__device__ __forceinline__ bool is_sentinel(double v) {
+  return (unsigned long long)__double_as_longlong(v) == SENTINEL_BITS;
+}
+__device__ __forceinline__ double unsentinel(double v) {
+  return is_sentinel(v) ? __longlong_as_double(0x7FF8000000000000ll) : v;
+}
+__device__ __forceinline__ double ld_relaxed_f64(const double *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ void st_relaxed_f64(double *p, double v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v))
+               : "memory");
+}
+// Spin (with a short back-off after a few tries) until *p is published.
+__device__ __forceinline__ double wait_value(const double *p) {
+  double v = ld_relaxed_f64(p);
+  for (int it = 0; is_sentinel(v); ++it) {
+    if (it > 4) __nanosleep(40);
+    v = ld_relaxed_f64(p);
+  }
+  return v;
+}
+__device__ __forceinline__ double ld_volatile_shared(const volatile double *p) { return *p; }
+
 __device__ __forceinline__ unsigned long long dbits(double v) {
   return (unsigned long long)__double_as_longlong(v);
 }

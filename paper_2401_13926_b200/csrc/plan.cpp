@@ -9,6 +9,7 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 namespace kkt {
@@ -122,6 +123,15 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     for (int64_t s = 0; s < nl; ++s) pos2slot[S.Li[S.Lp[j] + s]] = -1;
   }
   P.upd_ptr[nso] = (int32_t)u;
+  P.so_meta.assign(4 * nso, 0);
+  P.upd_lidx.resize(pairs);
+  for (int64_t t = 0; t < nso; ++t) {
+    const int64_t k = S.so_data[t];
+    P.so_meta[4 * t + 0] = P.so_slot[t];
+    P.so_meta[4 * t + 1] = (int32_t)(S.Lp[k + 1] - S.Lp[k]);
+    P.so_meta[4 * t + 2] = P.upd_ptr[t];
+    for (int64_t e = 0; e < S.Lp[k + 1] - S.Lp[k]; ++e) P.upd_lidx[P.upd_ptr[t] + e] = (int32_t)(S.Lp[k] + e);
+  }
   P.maxpat = maxpat;
   P.col_order = order_by_level(lev);
   P.refactor_levels = 0;
@@ -168,18 +178,88 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     for (int32_t p = P.Urp[r]; p < P.Urp[r + 1]; ++p) l = std::max(l, levU[P.Uci[p]] + 1);
     levU[r] = l;
   }
-  P.L_order = order_by_level(levL);
-  P.U_order = order_by_level(levU);
   P.L_levels = 0;
   P.U_levels = 0;
   for (int64_t i = 0; i < n; ++i) {
     P.L_levels = std::max(P.L_levels, levL[i] + 1);
     P.U_levels = std::max(P.U_levels, levU[i] + 1);
   }
+  // ---- phase split ----
+  {
+    const int TL = choose_tail(P, false), TU = choose_tail(P, true);
+    P.pL = (int32_t)(n - TL);
+    P.pU = (int32_t)(n - TU);
+    std::vector<int32_t> lg(levL.begin(), levL.begin() + P.pL);
+    std::vector<int32_t> lt(levL.begin() + P.pL, levL.end());
+    P.L_grid_order = order_by_level(lg);
+    P.L_tail_order = order_by_level(lt);
+    for (auto &v : P.L_tail_order) v += P.pL;
+    P.L_grid_levels = 0;
+    for (int32_t l : lg) P.L_grid_levels = std::max(P.L_grid_levels, l + 1);
+    // U: head rows [pU, n) keep their levels; grid rows' levels ignore head dependencies
+    std::vector<int32_t> uh(levU.begin() + P.pU, levU.end());
+    P.U_head_order = order_by_level(uh);
+    for (auto &v : P.U_head_order) v += P.pU;
+    std::vector<int32_t> lu(P.pU, 0);
+    for (int64_t r = P.pU - 1; r >= 0; --r) {
+      int32_t l = 0;
+      for (int32_t q = P.Urp[r]; q < P.Urp[r + 1]; ++q)
+        if (P.Uci[q] < P.pU) l = std::max(l, lu[P.Uci[q]] + 1);
+      lu[r] = l;
+    }
+    P.U_grid_order = order_by_level(lu);
+    P.U_grid_levels = 0;
+    for (int32_t l : lu) P.U_grid_levels = std::max(P.U_grid_levels, l + 1);
+  }
   P.Lx0.assign(S.Lx.begin(), S.Lx.end());
   P.Ux0.assign(S.Ux.begin(), S.Ux.end());
   P.Udiag0.assign(S.Udiag.begin(), S.Udiag.end());
   return KKT_OK;
+}
+
+// Cost model for the single-CTA phase size T (rows at the end of the position order):
+// grid-wide sync-free hops cost ~GRID_HOP_US each (L2 round trips), the CTA phase costs
+// ~CTA_ROW_US per row on its dependency chain plus ~CTA_NNZ_US per entry of throughput.
+int choose_tail(const HostPlan &P, bool upper) {
+  const char *env = std::getenv(upper ? "KKT_HEAD_ROWS" : "KKT_TAIL_ROWS");
+  const int n = P.n;
+  if (env) return std::max(0, std::min(n, std::min(atoi(env), KKT_CTA_PHASE_MAX_ROWS)));
+  const double GRID_HOP_US = 0.45, CTA_LEVEL_US = 0.04, CTA_NNZ_US = 0.0012;
+  const std::vector<int32_t> &rp = upper ? P.Urp : P.Lrp;
+  const std::vector<int32_t> &ci = upper ? P.Uci : P.Lci;
+  double best = 1e30;
+  int bestT = 0;
+  for (int T : {0, 32, 64, 128, 256, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144, 8192, 12288}) {
+    if (T > n || T > KKT_CTA_PHASE_MAX_ROWS) break;
+    const int p = n - T;
+    // levels of the grid part and of the CTA part
+    std::vector<int32_t> lev(n, 0);
+    int32_t gl = 0, tl = 0;
+    if (!upper) {
+      for (int r = 0; r < n; ++r) {
+        int32_t l = 0;
+        for (int32_t q = rp[r]; q < rp[r + 1]; ++q)
+          if ((r < p) == (ci[q] < p)) l = std::max(l, lev[ci[q]] + 1);
+        lev[r] = l;
+        if (r < p) gl = std::max(gl, l + 1); else tl = std::max(tl, l + 1);
+      }
+    } else {
+      for (int r = n - 1; r >= 0; --r) {
+        int32_t l = 0;
+        for (int32_t q = rp[r]; q < rp[r + 1]; ++q)
+          if ((r < p) == (ci[q] < p)) l = std::max(l, lev[ci[q]] + 1);
+        lev[r] = l;
+        if (r < p) gl = std::max(gl, l + 1); else tl = std::max(tl, l + 1);
+      }
+    }
+    const int64_t tnnz = T ? (int64_t)(rp[n] - rp[p]) : 0;
+    const double cost = GRID_HOP_US * gl + CTA_LEVEL_US * tl + CTA_NNZ_US * (double)tnnz;
+    if (cost < best) {
+      best = cost;
+      bestT = T;
+    }
+  }
+  return bestT;
 }
 
 }  // namespace kkt

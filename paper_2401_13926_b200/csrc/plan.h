@@ -5,6 +5,8 @@
 
 #include "kkt_internal.h"
 
+#define KKT_CTA_PHASE_MAX_ROWS 12288  // shared-memory rows of the single-CTA phase
+
 namespace kkt {
 
 struct HostPlan {
@@ -21,10 +23,20 @@ struct HostPlan {
   std::vector<int32_t> so_data, upd_ptr, a_src, col_order;
   std::vector<uint16_t> so_slot, upd_slot, a_slot;
   int32_t maxpat = 1, refactor_levels = 0;
+  // per so-entry metadata {slot of k in pattern(j), |L(:,k)|, first update pair, 0} and,
+  // per update pair, the CSC index of the L(:,k) entry it consumes
+  std::vector<int32_t> so_meta, upd_lidx;
   // trisolve CSR (L ascending cols, U descending cols) + CSC->CSR maps
-  std::vector<int32_t> Lrp, Lci, Lmap, Urp, Uci, Umap, L_order, U_order;
+  std::vector<int32_t> Lrp, Lci, Lmap, Urp, Uci, Umap;
   int32_t L_levels = 0, U_levels = 0;
+  // trisolve phases.  L: rows [0, pL) grid-wide sync-free, rows [pL, n) one CTA (tail);
+  // U: rows [pU, n) one CTA first (head), rows [0, pU) grid-wide.  Row orders by level.
+  int32_t pL = 0, pU = 0, L_grid_levels = 0, U_grid_levels = 0;
+  std::vector<int32_t> L_grid_order, L_tail_order, U_head_order, U_grid_order;
 };
+
+// Tunables of the phase split (env KKT_TAIL_ROWS / KKT_HEAD_ROWS override the model).
+int choose_tail(const HostPlan &P, bool upper);
 
 int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int64_t in_nnz,
                const int64_t *gen_src, HostPlan &P);

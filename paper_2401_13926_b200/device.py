@@ -208,6 +208,14 @@ class DeviceSystem:
         self._op_key = None
         return rep
 
+    def info(self) -> dict:
+        v = (C.c_int64 * 16)()
+        nat.check(self.lib.kkt_dev_info(self.h, v))
+        keys = ["n", "pL", "pU", "L_grid_levels", "U_grid_levels", "L_tail_rows", "U_head_rows",
+                "refactor_blocks", "refactor_warps", "refactor_smem", "trsv_blocks",
+                "refactor_levels", "arena_bytes", "update_pairs"]
+        return {k: int(v[i]) for i, k in enumerate(keys)}
+
     def launch_count(self) -> int:
         return int(self.lib.kkt_dev_launch_count(self.h))
 
