@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -87,6 +88,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.n_upd = (int64_t)h.upd_slot.size();
   d.n_ap = (int64_t)h.a_src.size();
   d.maxpat = h.maxpat;
+  d.poll_ns = std::getenv("KKT_POLL_NS") ? std::atoi(std::getenv("KKT_POLL_NS")) : 0;
   d.pL = h.pL;
   d.pU = h.pU;
   d.nLg = (int)h.L_grid_order.size();
@@ -105,6 +107,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   acc(4 * n); acc(4 * n);                                                  // perms
   acc(4 * h.L_grid_order.size()); acc(4 * h.L_tail_order.size());
   acc(4 * h.U_head_order.size()); acc(4 * h.U_grid_order.size());
+  acc(4 * h.L_crit.size()); acc(4 * h.U_crit.size()); acc(4 * h.Uhead_off.size());
+  acc(4 * d.nnz_L); acc(4 * d.nnz_U);                                      // Li Ui (CSC)
   acc(8 * d.nnz_L); acc(8 * d.nnz_U); acc(8 * n); acc(8 * n);              // Lv Uv yL yU
   acc(8 * 32); acc(64); acc(8 * 8 * RED_BLOCKS);                           // scal ticket partials
   ce = cudaMalloc(&dev->arena, bytes);
@@ -145,6 +149,11 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.L_tail_order = carve<int>(cur, h.L_tail_order.size());
   d.U_head_order = carve<int>(cur, h.U_head_order.size());
   d.U_grid_order = carve<int>(cur, h.U_grid_order.size());
+  d.L_crit = carve<int>(cur, h.L_crit.size());
+  d.U_crit = carve<int>(cur, h.U_crit.size());
+  d.Uhead_off = carve<int>(cur, h.Uhead_off.size());
+  d.Li = carve<int>(cur, d.nnz_L);
+  d.Ui = carve<int>(cur, d.nnz_U);
   d.Lv = carve<double>(cur, d.nnz_L);
   d.Uv = carve<double>(cur, d.nnz_U);
   d.yL = carve<double>(cur, n);
@@ -178,6 +187,11 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   UP(d.L_tail_order, h.L_tail_order);
   UP(d.U_head_order, h.U_head_order);
   UP(d.U_grid_order, h.U_grid_order);
+  UP(d.L_crit, h.L_crit);
+  UP(d.U_crit, h.U_crit);
+  UP(d.Uhead_off, h.Uhead_off);
+  UP(d.Li, h.Li32);
+  UP(d.Ui, h.Ui32);
   // the first factorization's values, so solve() works before any refactor (LuFactors)
   UP(d.Lx, h.Lx0);
   UP(d.Ux, h.Ux0);

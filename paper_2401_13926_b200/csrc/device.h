@@ -19,6 +19,7 @@ struct DevPlan {
   int n = 0, sym_lower = 0, has_lower = 0;
   int64_t nnz_a = 0, in_nnz = 0, nnz_L = 0, nnz_U = 0, n_so = 0, n_upd = 0, n_ap = 0;
   int maxpat = 1;
+  int poll_ns = 0;  // __nanosleep back-off while polling (env KKT_POLL_NS)
   // operator
   int *A_rp, *A_ci, *A_split, *gen_src;
   double *in_vals, *A_vals;
@@ -30,6 +31,7 @@ struct DevPlan {
   // trisolves
   int *Lrp, *Lci, *Urp, *Uci, *row_perm, *col_perm;
   int *L_grid_order, *L_tail_order, *U_head_order, *U_grid_order;
+  int *L_crit, *U_crit, *Uhead_off, *Li, *Ui;
   int pL, pU, nLg, nUg;  // split positions and grid-phase row counts
   double *Lv, *Uv;
   double *yL, *yU;       // sentinel-reset solution buffers (value == readiness flag)

@@ -43,14 +43,42 @@ __device__ __forceinline__ void st_relaxed_f64(double *p, double v) {
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v))
                : "memory");
 }
-// Spin (with a short back-off after a few tries) until *p is published.
-__device__ __forceinline__ double wait_value(const double *p) {
+// Spin (optionally backing off with __nanosleep(sleep_ns) after a few tries) until *p is
+// published.
+__device__ __forceinline__ double wait_value(const double *p, int sleep_ns = 0) {
   double v = ld_relaxed_f64(p);
   for (int it = 0; is_sentinel(v); ++it) {
-    if (it > 4) __nanosleep(40);
+    if (sleep_ns && it > 4) __nanosleep(sleep_ns);
     v = ld_relaxed_f64(p);
   }
   return v;
+}
+// Exponential back-off variant for addresses many warps may wait on at once (hot spots):
+// polling pressure on one L2 slice would otherwise delay the producer's own store.
+__device__ __forceinline__ double wait_value_backoff(const double *p) {
+  double v = ld_relaxed_f64(p);
+  unsigned ns = 32;
+  while (is_sentinel(v)) {
+    __nanosleep(ns);
+    ns = ns < 1024 ? 2 * ns : 1024;
+    v = ld_relaxed_f64(p);
+  }
+  return v;
+}
+
+// ---- cp.async (LDGSTS) helpers for shared-memory prefetch rings ----------------------
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ double ld_volatile_shared(const volatile double *p) { return *p; }
 

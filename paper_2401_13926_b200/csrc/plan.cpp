@@ -210,6 +210,42 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     P.U_grid_order = order_by_level(lu);
     P.U_grid_levels = 0;
     for (int32_t l : lu) P.U_grid_levels = std::max(P.U_grid_levels, l + 1);
+    // critical dependency: highest level, ties -> the most recently finished column
+    P.L_crit.assign(P.L_grid_order.size(), -1);
+    for (size_t i = 0; i < P.L_grid_order.size(); ++i) {
+      const int32_t r = P.L_grid_order[i];
+      int32_t best = -1, bl = -1;
+      for (int32_t q = P.Lrp[r]; q < P.Lrp[r + 1]; ++q) {
+        const int32_t c = P.Lci[q];
+        if (levL[c] > bl || (levL[c] == bl && c > best)) {
+          bl = levL[c];
+          best = c;
+        }
+      }
+      P.L_crit[i] = best;
+    }
+    P.U_crit.assign(P.U_grid_order.size(), -1);
+    for (size_t i = 0; i < P.U_grid_order.size(); ++i) {
+      const int32_t r = P.U_grid_order[i];
+      int32_t best = -1, bl = -1;
+      for (int32_t q = P.Urp[r]; q < P.Urp[r + 1]; ++q) {
+        const int32_t c = P.Uci[q];
+        if (c >= P.pU) continue;  // head columns are final before the grid phase starts
+        if (lu[c] > bl || (lu[c] == bl && c < best)) {
+          bl = lu[c];
+          best = c;
+        }
+      }
+      P.U_crit[i] = best;
+    }
+    P.Uhead_off.assign(n - P.pU, 0);
+    for (int64_t j = P.pU; j < n; ++j) {
+      int64_t q = S.Up[j];
+      while (q < S.Up[j + 1] && S.Ui[q] < P.pU) ++q;
+      P.Uhead_off[j - P.pU] = (int32_t)(q - S.Up[j]);
+    }
+    P.Li32.assign(S.Li.begin(), S.Li.end());
+    P.Ui32.assign(S.Ui.begin(), S.Ui.end());
   }
   P.Lx0.assign(S.Lx.begin(), S.Lx.end());
   P.Ux0.assign(S.Ux.begin(), S.Ux.end());
@@ -217,19 +253,19 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
   return KKT_OK;
 }
 
-// Cost model for the single-CTA phase size T (rows at the end of the position order):
-// grid-wide sync-free hops cost ~GRID_HOP_US each (L2 round trips), the CTA phase costs
-// ~CTA_ROW_US per row on its dependency chain plus ~CTA_NNZ_US per entry of throughput.
+// Cost model for the sweep-phase size T (the last T positions): each grid-phase level costs
+// ~GRID_HOP_US (an L2 round trip on the dependency chain), each sweep column ~SWEEP_COL_US
+// (one CTA barrier + shared RMW) plus ~SWEEP_NNZ_US per block entry of throughput.
 int choose_tail(const HostPlan &P, bool upper) {
   const char *env = std::getenv(upper ? "KKT_HEAD_ROWS" : "KKT_TAIL_ROWS");
   const int n = P.n;
   if (env) return std::max(0, std::min(n, std::min(atoi(env), KKT_CTA_PHASE_MAX_ROWS)));
-  const double GRID_HOP_US = 0.45, CTA_LEVEL_US = 0.04, CTA_NNZ_US = 0.0012;
+  const double GRID_HOP_US = 1.0, SWEEP_COL_US = 0.06, SWEEP_NNZ_US = 0.0003;
   const std::vector<int32_t> &rp = upper ? P.Urp : P.Lrp;
   const std::vector<int32_t> &ci = upper ? P.Uci : P.Lci;
   double best = 1e30;
   int bestT = 0;
-  for (int T : {0, 32, 64, 128, 256, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144, 8192, 12288}) {
+  for (int T : {0, 32, 64, 128, 256, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144}) {
     if (T > n || T > KKT_CTA_PHASE_MAX_ROWS) break;
     const int p = n - T;
     // levels of the grid part and of the CTA part
@@ -253,7 +289,8 @@ int choose_tail(const HostPlan &P, bool upper) {
       }
     }
     const int64_t tnnz = T ? (int64_t)(rp[n] - rp[p]) : 0;
-    const double cost = GRID_HOP_US * gl + CTA_LEVEL_US * tl + CTA_NNZ_US * (double)tnnz;
+    (void)tl;
+    const double cost = GRID_HOP_US * gl + SWEEP_COL_US * T + SWEEP_NNZ_US * (double)tnnz;
     if (cost < best) {
       best = cost;
       bestT = T;

@@ -5,7 +5,7 @@
 
 #include "kkt_internal.h"
 
-#define KKT_CTA_PHASE_MAX_ROWS 12288  // shared-memory rows of the single-CTA phase
+#define KKT_CTA_PHASE_MAX_ROWS 6144  // shared-memory rows of the single-CTA sweep phase
 
 namespace kkt {
 
@@ -33,6 +33,11 @@ struct HostPlan {
   // U: rows [pU, n) one CTA first (head), rows [0, pU) grid-wide.  Row orders by level.
   int32_t pL = 0, pU = 0, L_grid_levels = 0, U_grid_levels = 0;
   std::vector<int32_t> L_grid_order, L_tail_order, U_head_order, U_grid_order;
+  // per grid-order index: the row's critical (highest-level) grid dependency, or -1
+  std::vector<int32_t> L_crit, U_crit;
+  // per head column j >= pU: offset in U(:,j) (CSC, rows ascending) of the first row >= pU
+  std::vector<int32_t> Uhead_off;
+  std::vector<int32_t> Li32, Ui32;  // CSC row indices (int32) for the sweep phase
 };
 
 // Tunables of the phase split (env KKT_TAIL_ROWS / KKT_HEAD_ROWS override the model).

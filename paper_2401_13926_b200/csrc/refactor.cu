@@ -23,24 +23,42 @@ namespace kkt {
 // Operator values: expand caller layout -> general CSR, inf-norms, max|a|.
 // One thread per row; sums in entry order (np.bincount order => bitwise).
 // ----------------------------------------------------------------------------
-__global__ void k_expand_norms(DevPlan d) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= d.n) return;
-  const int b = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
-  double sg = 0.0, s1 = 0.0, s2 = 0.0, mx = 0.0;
-  for (int p = b; p < e; ++p) {
-    const double v = d.in_vals[d.sym_lower ? d.gen_src[p] : p];
-    d.A_vals[p] = v;
-    const double a = fabs(v);
-    sg = __dadd_rn(sg, a);
-    if (p < s) s1 = __dadd_rn(s1, a); else s2 = __dadd_rn(s2, a);
-    mx = fmax(mx, a);
+__global__ void __launch_bounds__(256) k_expand_norms(DevPlan d) {
+  __shared__ double sh[3][8];
+  double mx = 0.0, sg = 0.0, op = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x) {
+    const int b = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
+    double g = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int p = b; p < e; ++p) {
+      const double v = d.in_vals[d.sym_lower ? d.gen_src[p] : p];
+      d.A_vals[p] = v;
+      const double a = fabs(v);
+      g = __dadd_rn(g, a);
+      if (p < s) s1 = __dadd_rn(s1, a); else s2 = __dadd_rn(s2, a);
+      mx = fmax(mx, a);
+    }
+    // refactorize uses inf_norm of the general matrix (direct_lu.py:318); nsr/nrbe use the
+    // operator's: two bincounts for symmetric-lower storage (sparsecore.py:339-342).
+    sg = fmax(sg, g);
+    op = fmax(op, d.sym_lower ? __dadd_rn(s1, s2) : g);
   }
-  // refactorize uses inf_norm of the general matrix (direct_lu.py:318); nsr/nrbe use the
-  // operator's: two bincounts for symmetric-lower storage (sparsecore.py:339-342).
-  atomic_max_nonneg(&d.scal[SC_MAXABS_A], mx);
-  atomic_max_nonneg(&d.scal[SC_INFNORM], sg);
-  atomic_max_nonneg(&d.scal[SC_OPNORM], d.sym_lower ? __dadd_rn(s1, s2) : sg);
+  // maxima are order-independent: warp + block max, then one atomic per block
+  mx = warp_max(mx);
+  sg = warp_max(sg);
+  op = warp_max(op);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][w] = mx;
+    sh[1][w] = sg;
+    sh[2][w] = op;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double m = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) m = fmax(m, sh[threadIdx.x][q]);
+    const int slot = threadIdx.x == 0 ? SC_MAXABS_A : threadIdx.x == 1 ? SC_INFNORM : SC_OPNORM;
+    atomic_max_nonneg(&d.scal[slot], m);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
@@ -119,13 +137,13 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
         if (!big) {
           for (int e = lane; e < cnt; e += 32) {
             double l = st_l[off + e];
-            if (is_sentinel(l)) l = wait_value(&d.Lx[d.upd_lidx[pair0 + off + e]]);
+            if (is_sentinel(l)) l = wait_value_backoff(&d.Lx[d.upd_lidx[pair0 + off + e]]);
             const int s = st_s[off + e];
             x[s] = __dsub_rn(x[s], __dmul_rn(l, xk));
           }
         } else {
           for (int e = lane; e < cnt; e += 32) {
-            const double l = wait_value(&d.Lx[d.upd_lidx[pair0 + e]]);
+            const double l = wait_value_backoff(&d.Lx[d.upd_lidx[pair0 + e]]);
             const int s = d.upd_slot[pair0 + e];
             x[s] = __dsub_rn(x[s], __dmul_rn(l, xk));
           }
@@ -177,7 +195,7 @@ __global__ void k_diag_stats(DevPlan d) {
 
 // ----------------------------------------------------------------------------
 cudaError_t launch_expand_norms(const DevPlan &d, cudaStream_t s) {
-  if (d.n) k_expand_norms<<<(d.n + 255) / 256, 256, 0, s>>>(d);
+  if (d.n) k_expand_norms<<<min((d.n + 255) / 256, 2 * 148), 256, 0, s>>>(d);
   return cudaGetLastError();
 }
 

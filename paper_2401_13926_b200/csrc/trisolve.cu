@@ -2,18 +2,22 @@
 //
 // The reference sweeps columns: forward `y[Li(j)] -= Lx(j)*y[j]` for ascending j, backward
 // `y_j /= u_jj; y[Ui(j)] -= Ux(j)*y_j` for descending j.  Row r therefore receives its
-// updates in ascending column order (L) / descending column order (U); a row-oriented solve
-// that accumulates each CSR row sequentially in that order, with separately rounded products,
-// reproduces every bit.
+// updates in ascending column order (L) / descending column order (U).  Both schedules below
+// preserve that per-row order, with separately rounded products, so every bit matches.
 //
-// Schedule (per sweep, chosen on the host from the level profile, plan.cpp choose_tail):
-//   * grid phase — persistent, sync-free, warp per row, rows round-robin in level order.
-//     Readiness is the value itself: y is reset to a sentinel NaN pattern and a consumer
-//     re-reads y[col] until it is published (one L2 round trip per dependency hop);
-//   * CTA phase — the narrow end of the DAG (the dense separator rows at the end of the
-//     elimination order): one 1024-thread CTA, thread per row, y of the phase rows in shared
-//     memory with the same sentinel protocol (~40 cycles per hop instead of ~1 us).
-//   L = [grid rows < pL] then [CTA rows >= pL];  U = [CTA rows >= pU] then [grid rows < pU].
+// Per sweep the rows split at a position chosen on the host from the level profile
+// (plan.cpp choose_tail):
+//   * grid phase (wide part of the DAG) — persistent, sync-free, warp per row, rows
+//     round-robin in level order.  Readiness is the value itself: y is reset to a sentinel
+//     NaN pattern and consumers re-read y[col] until it is published.  Only ONE lane polls,
+//     on the row's critical (highest-level) dependency, so a just-published value is not
+//     hammered by every row of a dense separator (that L2 hot spot cost ~10 us per hop);
+//   * sweep phase (the dense separator at the end of the elimination order) — one CTA
+//     replays the reference's own column sweep over the block in shared memory: per column
+//     one barrier, each target updated by one thread.  Column data stream in through a
+//     cp.async ring RING-1 columns ahead, so a step costs a barrier + a shared RMW.
+//   L = [grid rows < pL] then [sweep columns pL..n-1];
+//   U = [sweep columns n-1..pU] then [grid rows < pU].
 // Each sweep resets the other sweep's buffer for the next solve, so no memsets are needed.
 #include <cuda_runtime.h>
 
@@ -21,6 +25,10 @@
 #include "kernels.cuh"
 
 namespace kkt {
+
+constexpr int SWEEP_THREADS = 256;
+constexpr int SWEEP_RING = 8;    // columns in flight
+constexpr int SWEEP_SLOT = 512;  // entries per ring slot (longer columns read from global)
 
 // ---- grid phase: warp per row ------------------------------------------------------------
 template <bool IS_U>
@@ -30,6 +38,7 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int *order = IS_U ? d.U_grid_order : d.L_grid_order;
+  const int *crit = IS_U ? d.U_crit : d.L_crit;
   const int nrows = IS_U ? d.nUg : d.nLg;
   const int *rp = IS_U ? d.Urp : d.Lrp;
   const int *ci = IS_U ? d.Uci : d.Lci;
@@ -39,20 +48,18 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
   bool bad = false;
   for (int idx = gwarp; idx < nrows; idx += nwarps) {
     const int r = order[idx];
-    double acc;
-    if (IS_U) {
-      acc = ldcg(&d.yL[r]);  // final L result (previous kernel)
-    } else {
-      acc = b[d.row_perm[r]];
-    }
     const int beg = rp[r], end = rp[r + 1];
-    // prefetch the first chunk's pattern/values (independent of the dependencies)
+    // independent loads first: the initial value and the first chunk's pattern/values
+    double acc = IS_U ? ldcg(&d.yL[r]) : b[d.row_perm[r]];
     int col = 0;
     double v = 0.0;
     if (beg + lane < end) {
       col = ci[beg + lane];
       v = vals[beg + lane];
     }
+    const int cr = crit[idx];
+    if (lane == 0 && cr >= 0) wait_value(&ysrc[cr], d.poll_ns);
+    __syncwarp();
     for (int c0 = beg; c0 < end; c0 += 32) {
       const int cnt = min(32, end - c0);
       double p = 0.0;
@@ -62,7 +69,7 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
         ncol = ci[c0 + 32 + lane];
         nv = vals[c0 + 32 + lane];
       }
-      if (lane < cnt) p = __dmul_rn(v, wait_value(&ysrc[col]));
+      if (lane < cnt) p = __dmul_rn(v, wait_value(&ysrc[col], d.poll_ns));
       for (int i = 0; i < cnt; ++i) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, p, i));
       col = ncol;
       v = nv;
@@ -81,51 +88,109 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
   if (IS_U && bad) atomicOr(&d.scal[SC_NONFINITE], 1ull);
 }
 
-// ---- CTA phase: one block, thread per row, phase rows' y in shared memory ----------------
+// ---- sweep phase: one CTA, the reference's column sweep on the dense separator block --------
 template <bool IS_U>
-__global__ void __launch_bounds__(CTA_PHASE_THREADS) k_trsv_cta(DevPlan d,
-                                                                const double *__restrict__ b,
-                                                                double *__restrict__ xout) {
-  extern __shared__ double ys[];  // rows [p, n) -> slot r - p
+__global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
+                                                              const double *__restrict__ b,
+                                                              double *__restrict__ xout) {
+  extern __shared__ double sm[];
   const int p = IS_U ? d.pU : d.pL;
   const int T = d.n - p;
-  const int *order = IS_U ? d.U_head_order : d.L_tail_order;
-  const int *rp = IS_U ? d.Urp : d.Lrp;
-  const int *ci = IS_U ? d.Uci : d.Lci;
-  const double *vals = IS_U ? d.Uv : d.Lv;
-  double *ysrc = IS_U ? d.yU : d.yL;
-  double *yres = IS_U ? d.yL : d.yU;
-  volatile double *vys = ys;
-  for (int s = threadIdx.x; s < T; s += blockDim.x) ys[s] = __longlong_as_double((long long)SENTINEL_BITS);
-  __syncthreads();
-  bool bad = false;
-  for (int idx = threadIdx.x; idx < T; idx += blockDim.x) {
-    const int r = order[idx];
-    double acc = IS_U ? ldcg(&d.yL[r]) : b[d.row_perm[r]];
-    const int beg = rp[r], end = rp[r + 1];
-    for (int e = beg; e < end; ++e) {
-      const int col = ci[e];
-      const double v = vals[e];
-      double y;
-      if (col >= p) {
-        y = vys[col - p];
-        while (is_sentinel(y)) y = vys[col - p];
-      } else {
-        y = ldcg(&ysrc[col]);  // grid phase of this sweep already complete (L only)
-      }
-      acc = __dsub_rn(acc, __dmul_rn(v, y));
-    }
-    double w = acc;
-    if (IS_U) {
-      w = __ddiv_rn(acc, d.udiag[r]);
-      xout[d.col_perm[r]] = w;
-      if (!isfinite(w)) bad = true;
-    }
-    w = unsentinel(w);
-    yres[r] = __longlong_as_double((long long)SENTINEL_BITS);
-    ysrc[r] = w;
-    vys[r - p] = w;
+  const int tid = threadIdx.x;
+  double *acc = sm;                                           // [T]
+  double *dg = acc + T;                                       // [T] (U: pivots)
+  double *rv = dg + (IS_U ? T : 0);                           // [RING*SLOT] values
+  int *rr = reinterpret_cast<int *>(rv + SWEEP_RING * SWEEP_SLOT);  // [RING*SLOT] rows
+  int *cbeg = rr + SWEEP_RING * SWEEP_SLOT;                   // [T] CSC range of step s
+  int *cend = cbeg + T;                                       // [T]
+  const double *cvals = IS_U ? d.Ux : d.Lx;
+  const int *crows = IS_U ? d.Ui : d.Li;
+  // step s handles column j(s): L ascending from p, U descending from n-1
+  for (int s = tid; s < T; s += blockDim.x) {
+    const int j = IS_U ? d.n - 1 - s : p + s;
+    cbeg[s] = IS_U ? d.Up[j] + d.Uhead_off[j - p] : d.Lp[j];
+    cend[s] = IS_U ? d.Up[j + 1] : d.Lp[j + 1];
+    if (IS_U) dg[j - p] = d.udiag[j];
   }
+  if (IS_U) {
+    // acc = L result of the head rows; reset yL for the next solve
+    for (int r = p + tid; r < d.n; r += blockDim.x) {
+      acc[r - p] = ldcg(&d.yL[r]);
+      d.yL[r] = __longlong_as_double((long long)SENTINEL_BITS);
+    }
+  } else {
+    // acc_r = b_perm[r] - sum_{j < p} L(r,j) y_j, ascending j (rows sorted ascending, so these
+    // are each row's leading entries); warp per row.  Reset yU for the next solve.
+    const int lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+    for (int r = p + w; r < d.n; r += nw) {
+      double a = b[d.row_perm[r]];
+      const int beg = d.Lrp[r], end = d.Lrp[r + 1];
+      bool more = true;
+      for (int c0 = beg; c0 < end && more; c0 += 32) {
+        const int e = c0 + lane;
+        int col = e < end ? d.Lci[e] : d.n;
+        double pr = 0.0;
+        if (col < p) pr = __dmul_rn(d.Lv[e], ldcg(&d.yL[col]));
+        const unsigned outside = __ballot_sync(0xffffffffu, col < p);
+        const int cnt = __popc(outside);  // leading run (columns ascending)
+        for (int i = 0; i < cnt; ++i) a = __dsub_rn(a, __shfl_sync(0xffffffffu, pr, i));
+        more = cnt == 32;
+      }
+      if (lane == 0) {
+        acc[r - p] = a;
+        d.yU[r] = __longlong_as_double((long long)SENTINEL_BITS);
+      }
+    }
+  }
+  __syncthreads();
+  auto issue = [&](int s) {
+    if (s < T) {
+      const int slot = s % SWEEP_RING;
+      const int beg = cbeg[s], cnt = min(cend[s] - beg, SWEEP_SLOT);
+      for (int e = tid; e < cnt; e += blockDim.x) {
+        cp_async8(&rv[slot * SWEEP_SLOT + e], &cvals[beg + e]);
+        cp_async4(&rr[slot * SWEEP_SLOT + e], &crows[beg + e]);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll 1
+  for (int s = 0; s < SWEEP_RING - 1; ++s) issue(s);
+  bool bad = false;
+#pragma unroll 1
+  for (int s = 0; s < T; ++s) {
+    cp_async_wait<SWEEP_RING - 2>();
+    __syncthreads();
+    issue(s + SWEEP_RING - 1);
+    const int j = IS_U ? d.n - 1 - s : p + s;
+    double yj = acc[j - p];
+    if (IS_U) yj = __ddiv_rn(yj, dg[j - p]);
+    if (tid == 0) {
+      const double w = unsentinel(yj);
+      if (IS_U) {
+        d.yU[j] = w;
+        xout[d.col_perm[j]] = yj;
+        if (!isfinite(yj)) bad = true;
+      } else {
+        d.yL[j] = w;
+      }
+    }
+    const int slot = s % SWEEP_RING;
+    const int beg = cbeg[s], cnt = cend[s] - beg;
+    for (int e = tid; e < cnt; e += blockDim.x) {
+      double v;
+      int r;
+      if (e < SWEEP_SLOT) {
+        v = rv[slot * SWEEP_SLOT + e];
+        r = rr[slot * SWEEP_SLOT + e];
+      } else {
+        v = cvals[beg + e];
+        r = crows[beg + e];
+      }
+      acc[r - p] = __dsub_rn(acc[r - p], __dmul_rn(v, yj));
+    }
+  }
+  cp_async_wait<0>();
   if (IS_U && bad) atomicOr(&d.scal[SC_NONFINITE], 1ull);
 }
 
@@ -140,35 +205,38 @@ cudaError_t launch_fill_sentinel(double *p, int64_t n, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+static size_t sweep_smem(int T, bool upper) {
+  return (size_t)T * 8 * (upper ? 2 : 1) + (size_t)SWEEP_RING * SWEEP_SLOT * 12 + (size_t)T * 8;
+}
+
 cudaError_t trsv_configure(int *grid_blocks_per_sm) {
   int a = 0, b = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_trsv_grid<false>, 256, 0);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trsv_grid<true>, 256, 0);
   if (e != cudaSuccess) return e;
   *grid_blocks_per_sm = a < b ? a : b;
-  const int smem = KKT_CTA_PHASE_MAX_ROWS * 8;
-  e = cudaFuncSetAttribute(k_trsv_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  e = cudaFuncSetAttribute(k_trsv_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sweep_smem(KKT_CTA_PHASE_MAX_ROWS, false));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_trsv_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = cudaFuncSetAttribute(k_trsv_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sweep_smem(KKT_CTA_PHASE_MAX_ROWS, true));
   return e;
 }
 
 cudaError_t launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,
                         cudaStream_t s, long long *launches) {
   if (!d.n) return cudaSuccess;
-  const size_t smL = 8 * (size_t)(d.n - d.pL), smU = 8 * (size_t)(d.n - d.pU);
-  // forward: grid rows then the CTA tail
-  if (d.nLg) {
+  const int TL = d.n - d.pL, TU = d.n - d.pU;
+  if (d.nLg) {  // forward: grid rows, then the sweep over the trailing block
     k_trsv_grid<false><<<grid_blocks, 256, 0, s>>>(d, b, x);
     ++*launches;
   }
-  if (d.n > d.pL) {
-    k_trsv_cta<false><<<1, CTA_PHASE_THREADS, smL, s>>>(d, b, x);
+  if (TL) {
+    k_trsv_sweep<false><<<1, SWEEP_THREADS, sweep_smem(TL, false), s>>>(d, b, x);
     ++*launches;
   }
-  // backward: CTA head then the grid rows
-  if (d.n > d.pU) {
-    k_trsv_cta<true><<<1, CTA_PHASE_THREADS, smU, s>>>(d, b, x);
+  if (TU) {  // backward: the sweep over the trailing block, then the grid rows
+    k_trsv_sweep<true><<<1, SWEEP_THREADS, sweep_smem(TU, true), s>>>(d, b, x);
     ++*launches;
   }
   if (d.nUg) {
