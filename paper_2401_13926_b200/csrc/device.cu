@@ -93,6 +93,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.pU = h.pU;
   d.nLg = (int)h.L_grid_order.size();
   d.nUg = (int)h.U_grid_order.size();
+  d.sweep_maxL = h.sweep_maxL;
+  d.sweep_maxU = h.sweep_maxU;
   const size_t n = (size_t)h.n;
   const size_t in_cap = (size_t)std::max(d.in_nnz, d.nnz_a);
   size_t bytes = 0;
@@ -109,6 +111,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   acc(4 * h.U_head_order.size()); acc(4 * h.U_grid_order.size());
   acc(4 * h.L_crit.size()); acc(4 * h.U_crit.size()); acc(4 * h.Uhead_off.size());
   acc(4 * d.nnz_L); acc(4 * d.nnz_U);                                      // Li Ui (CSC)
+  acc(4 * h.Ltail_split.size()); acc(8 * h.Ltail_split.size());            // split, tacc
   acc(8 * d.nnz_L); acc(8 * d.nnz_U); acc(8 * n); acc(8 * n);              // Lv Uv yL yU
   acc(8 * 32); acc(64); acc(8 * 8 * RED_BLOCKS);                           // scal ticket partials
   ce = cudaMalloc(&dev->arena, bytes);
@@ -154,6 +157,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.Uhead_off = carve<int>(cur, h.Uhead_off.size());
   d.Li = carve<int>(cur, d.nnz_L);
   d.Ui = carve<int>(cur, d.nnz_U);
+  d.Ltail_split = carve<int>(cur, h.Ltail_split.size());
+  d.tacc = carve<double>(cur, h.Ltail_split.size());
   d.Lv = carve<double>(cur, d.nnz_L);
   d.Uv = carve<double>(cur, d.nnz_U);
   d.yL = carve<double>(cur, n);
@@ -192,6 +197,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   UP(d.Uhead_off, h.Uhead_off);
   UP(d.Li, h.Li32);
   UP(d.Ui, h.Ui32);
+  UP(d.Ltail_split, h.Ltail_split);
   // the first factorization's values, so solve() works before any refactor (LuFactors)
   UP(d.Lx, h.Lx0);
   UP(d.Ux, h.Ux0);

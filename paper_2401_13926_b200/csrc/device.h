@@ -31,8 +31,10 @@ struct DevPlan {
   // trisolves
   int *Lrp, *Lci, *Urp, *Uci, *row_perm, *col_perm;
   int *L_grid_order, *L_tail_order, *U_head_order, *U_grid_order;
-  int *L_crit, *U_crit, *Uhead_off, *Li, *Ui;
+  int *L_crit, *U_crit, *Uhead_off, *Li, *Ui, *Ltail_split;
+  double *tacc;  // partial sums of the L tail rows over columns < pL (grid phase -> sweep)
   int pL, pU, nLg, nUg;  // split positions and grid-phase row counts
+  int sweep_maxL, sweep_maxU;
   double *Lv, *Uv;
   double *yL, *yU;       // sentinel-reset solution buffers (value == readiness flag)
   // scalars

@@ -57,10 +57,10 @@ __device__ __forceinline__ double wait_value(const double *p, int sleep_ns = 0) 
 // polling pressure on one L2 slice would otherwise delay the producer's own store.
 __device__ __forceinline__ double wait_value_backoff(const double *p) {
   double v = ld_relaxed_f64(p);
-  unsigned ns = 32;
+  unsigned ns = 16;
   while (is_sentinel(v)) {
     __nanosleep(ns);
-    ns = ns < 1024 ? 2 * ns : 1024;
+    ns = ns < 256 ? 2 * ns : 256;
     v = ld_relaxed_f64(p);
   }
   return v;

@@ -189,9 +189,18 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     const int TL = choose_tail(P, false), TU = choose_tail(P, true);
     P.pL = (int32_t)(n - TL);
     P.pU = (int32_t)(n - TU);
+    // L grid phase: the rows < pL, plus, for every tail row, its leading entries (columns
+    // < pL) as a partial row whose result seeds the sweep (level = 1 + max level used).
     std::vector<int32_t> lg(levL.begin(), levL.begin() + P.pL);
+    P.Ltail_split.assign(n - P.pL, 0);
+    for (int64_t r = P.pL; r < n; ++r) {
+      int32_t q = P.Lrp[r], l = 0;
+      while (q < P.Lrp[r + 1] && P.Lci[q] < P.pL) l = std::max(l, levL[P.Lci[q++]] + 1);
+      P.Ltail_split[r - P.pL] = q;
+      lg.push_back(l);
+    }
+    P.L_grid_order = order_by_level(lg);  // indices >= pL are the tail partial rows
     std::vector<int32_t> lt(levL.begin() + P.pL, levL.end());
-    P.L_grid_order = order_by_level(lg);
     P.L_tail_order = order_by_level(lt);
     for (auto &v : P.L_tail_order) v += P.pL;
     P.L_grid_levels = 0;
@@ -215,7 +224,8 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     for (size_t i = 0; i < P.L_grid_order.size(); ++i) {
       const int32_t r = P.L_grid_order[i];
       int32_t best = -1, bl = -1;
-      for (int32_t q = P.Lrp[r]; q < P.Lrp[r + 1]; ++q) {
+      const int32_t qend = r >= P.pL ? P.Ltail_split[r - P.pL] : P.Lrp[r + 1];
+      for (int32_t q = P.Lrp[r]; q < qend; ++q) {
         const int32_t c = P.Lci[q];
         if (levL[c] > bl || (levL[c] == bl && c > best)) {
           bl = levL[c];
@@ -244,6 +254,11 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
       while (q < S.Up[j + 1] && S.Ui[q] < P.pU) ++q;
       P.Uhead_off[j - P.pU] = (int32_t)(q - S.Up[j]);
     }
+    for (int64_t j = P.pL; j < n; ++j)
+      P.sweep_maxL = std::max<int32_t>(P.sweep_maxL, (int32_t)(S.Lp[j + 1] - S.Lp[j]));
+    for (int64_t j = P.pU; j < n; ++j)
+      P.sweep_maxU = std::max<int32_t>(P.sweep_maxU,
+                                       (int32_t)(S.Up[j + 1] - S.Up[j] - P.Uhead_off[j - P.pU]));
     P.Li32.assign(S.Li.begin(), S.Li.end());
     P.Ui32.assign(S.Ui.begin(), S.Ui.end());
   }
@@ -265,7 +280,7 @@ int choose_tail(const HostPlan &P, bool upper) {
   const std::vector<int32_t> &ci = upper ? P.Uci : P.Lci;
   double best = 1e30;
   int bestT = 0;
-  for (int T : {0, 32, 64, 128, 256, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144}) {
+  for (int T : {0, 32, 64, 128, 256, 512, 768, 1024, 1536, 2048, 3072, 4096, 5120}) {
     if (T > n || T > KKT_CTA_PHASE_MAX_ROWS) break;
     const int p = n - T;
     // levels of the grid part and of the CTA part

@@ -5,7 +5,7 @@
 
 #include "kkt_internal.h"
 
-#define KKT_CTA_PHASE_MAX_ROWS 6144  // shared-memory rows of the single-CTA sweep phase
+#define KKT_CTA_PHASE_MAX_ROWS 5120  // shared-memory rows of the single-CTA sweep phase
 
 namespace kkt {
 
@@ -38,6 +38,8 @@ struct HostPlan {
   // per head column j >= pU: offset in U(:,j) (CSC, rows ascending) of the first row >= pU
   std::vector<int32_t> Uhead_off;
   std::vector<int32_t> Li32, Ui32;  // CSC row indices (int32) for the sweep phase
+  std::vector<int32_t> Ltail_split;  // tail row r: CSR index of its first entry >= pL
+  int32_t sweep_maxL = 0, sweep_maxU = 0;  // longest column inside each sweep block
 };
 
 // Tunables of the phase split (env KKT_TAIL_ROWS / KKT_HEAD_ROWS override the model).

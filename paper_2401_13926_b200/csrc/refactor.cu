@@ -135,9 +135,25 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
         const int off = __shfl_sync(0xffffffffu, incl - m.y, i);
         const double xk = x[kslot];
         if (!big) {
+          // L(:,k) not yet published when staged?  One lane waits (with back-off) so a
+          // column many warps depend on is not polled by every lane of every consumer;
+          // the rest then re-read their entries (normally already visible).
+          bool miss = false;
+          for (int e = lane; e < cnt; e += 32) miss |= is_sentinel(st_l[off + e]);
+          const unsigned mm = __ballot_sync(0xffffffffu, miss);
+          if (mm) {
+            if (lane == __ffs(mm) - 1) {
+              for (int e = lane; e < cnt; e += 32)
+                if (is_sentinel(st_l[off + e])) {
+                  wait_value_backoff(&d.Lx[d.upd_lidx[pair0 + off + e]]);
+                  break;
+                }
+            }
+            __syncwarp();
+          }
           for (int e = lane; e < cnt; e += 32) {
             double l = st_l[off + e];
-            if (is_sentinel(l)) l = wait_value_backoff(&d.Lx[d.upd_lidx[pair0 + off + e]]);
+            if (is_sentinel(l)) l = wait_value(&d.Lx[d.upd_lidx[pair0 + off + e]]);
             const int s = st_s[off + e];
             x[s] = __dsub_rn(x[s], __dmul_rn(l, xk));
           }

@@ -27,8 +27,8 @@
 namespace kkt {
 
 constexpr int SWEEP_THREADS = 256;
-constexpr int SWEEP_RING = 8;    // columns in flight
-constexpr int SWEEP_SLOT = 512;  // entries per ring slot (longer columns read from global)
+
+
 
 // ---- grid phase: warp per row ------------------------------------------------------------
 template <bool IS_U>
@@ -48,7 +48,10 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
   bool bad = false;
   for (int idx = gwarp; idx < nrows; idx += nwarps) {
     const int r = order[idx];
-    const int beg = rp[r], end = rp[r + 1];
+    // L: rows >= pL are the sweep block's rows; here only their leading entries (columns
+    // < pL) are summed, into tacc, which seeds the sweep (same per-row order).
+    const bool partial = !IS_U && r >= d.pL;
+    const int beg = rp[r], end = partial ? d.Ltail_split[r - d.pL] : rp[r + 1];
     // independent loads first: the initial value and the first chunk's pattern/values
     double acc = IS_U ? ldcg(&d.yL[r]) : b[d.row_perm[r]];
     int col = 0;
@@ -76,6 +79,10 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
     }
     if (lane == 0) {
       double w = acc;
+      if (partial) {
+        d.tacc[r - d.pL] = acc;
+        continue;
+      }
       if (IS_U) {
         w = __ddiv_rn(acc, d.udiag[r]);
         xout[d.col_perm[r]] = w;
@@ -89,7 +96,7 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
 }
 
 // ---- sweep phase: one CTA, the reference's column sweep on the dense separator block --------
-template <bool IS_U>
+template <bool IS_U, int RING, int SLOT>
 __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
                                                               const double *__restrict__ b,
                                                               double *__restrict__ xout) {
@@ -100,8 +107,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
   double *acc = sm;                                           // [T]
   double *dg = acc + T;                                       // [T] (U: pivots)
   double *rv = dg + (IS_U ? T : 0);                           // [RING*SLOT] values
-  int *rr = reinterpret_cast<int *>(rv + SWEEP_RING * SWEEP_SLOT);  // [RING*SLOT] rows
-  int *cbeg = rr + SWEEP_RING * SWEEP_SLOT;                   // [T] CSC range of step s
+  int *rr = reinterpret_cast<int *>(rv + RING * SLOT);  // [RING*SLOT] rows
+  int *cbeg = rr + RING * SLOT;                   // [T] CSC range of step s
   int *cend = cbeg + T;                                       // [T]
   const double *cvals = IS_U ? d.Ux : d.Lx;
   const int *crows = IS_U ? d.Ui : d.Li;
@@ -119,49 +126,33 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
       d.yL[r] = __longlong_as_double((long long)SENTINEL_BITS);
     }
   } else {
-    // acc_r = b_perm[r] - sum_{j < p} L(r,j) y_j, ascending j (rows sorted ascending, so these
-    // are each row's leading entries); warp per row.  Reset yU for the next solve.
-    const int lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
-    for (int r = p + w; r < d.n; r += nw) {
-      double a = b[d.row_perm[r]];
-      const int beg = d.Lrp[r], end = d.Lrp[r + 1];
-      bool more = true;
-      for (int c0 = beg; c0 < end && more; c0 += 32) {
-        const int e = c0 + lane;
-        int col = e < end ? d.Lci[e] : d.n;
-        double pr = 0.0;
-        if (col < p) pr = __dmul_rn(d.Lv[e], ldcg(&d.yL[col]));
-        const unsigned outside = __ballot_sync(0xffffffffu, col < p);
-        const int cnt = __popc(outside);  // leading run (columns ascending)
-        for (int i = 0; i < cnt; ++i) a = __dsub_rn(a, __shfl_sync(0xffffffffu, pr, i));
-        more = cnt == 32;
-      }
-      if (lane == 0) {
-        acc[r - p] = a;
-        d.yU[r] = __longlong_as_double((long long)SENTINEL_BITS);
-      }
+    // acc_r = b_perm[r] - sum_{j < p} L(r,j) y_j (ascending j) was computed by the grid
+    // kernel as the partial rows; reset yU for the next solve.
+    for (int r = p + tid; r < d.n; r += blockDim.x) {
+      acc[r - p] = ldcg(&d.tacc[r - p]);
+      d.yU[r] = __longlong_as_double((long long)SENTINEL_BITS);
     }
   }
   __syncthreads();
   auto issue = [&](int s) {
     if (s < T) {
-      const int slot = s % SWEEP_RING;
-      const int beg = cbeg[s], cnt = min(cend[s] - beg, SWEEP_SLOT);
+      const int slot = s % RING;
+      const int beg = cbeg[s], cnt = min(cend[s] - beg, SLOT);
       for (int e = tid; e < cnt; e += blockDim.x) {
-        cp_async8(&rv[slot * SWEEP_SLOT + e], &cvals[beg + e]);
-        cp_async4(&rr[slot * SWEEP_SLOT + e], &crows[beg + e]);
+        cp_async8(&rv[slot * SLOT + e], &cvals[beg + e]);
+        cp_async4(&rr[slot * SLOT + e], &crows[beg + e]);
       }
     }
     cp_async_commit();
   };
 #pragma unroll 1
-  for (int s = 0; s < SWEEP_RING - 1; ++s) issue(s);
+  for (int s = 0; s < RING - 1; ++s) issue(s);
   bool bad = false;
 #pragma unroll 1
   for (int s = 0; s < T; ++s) {
-    cp_async_wait<SWEEP_RING - 2>();
+    cp_async_wait<RING - 2>();
     __syncthreads();
-    issue(s + SWEEP_RING - 1);
+    issue(s + RING - 1);
     const int j = IS_U ? d.n - 1 - s : p + s;
     double yj = acc[j - p];
     if (IS_U) yj = __ddiv_rn(yj, dg[j - p]);
@@ -175,14 +166,14 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
         d.yL[j] = w;
       }
     }
-    const int slot = s % SWEEP_RING;
+    const int slot = s % RING;
     const int beg = cbeg[s], cnt = cend[s] - beg;
     for (int e = tid; e < cnt; e += blockDim.x) {
       double v;
       int r;
-      if (e < SWEEP_SLOT) {
-        v = rv[slot * SWEEP_SLOT + e];
-        r = rr[slot * SWEEP_SLOT + e];
+      if (e < SLOT) {
+        v = rv[slot * SLOT + e];
+        r = rr[slot * SLOT + e];
       } else {
         v = cvals[beg + e];
         r = crows[beg + e];
@@ -205,8 +196,34 @@ cudaError_t launch_fill_sentinel(double *p, int64_t n, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ring shapes (RING x SLOT entries, 96 KB each): deep rings for short columns
+constexpr int RING_BYTES = 96 * 1024;
 static size_t sweep_smem(int T, bool upper) {
-  return (size_t)T * 8 * (upper ? 2 : 1) + (size_t)SWEEP_RING * SWEEP_SLOT * 12 + (size_t)T * 8;
+  return (size_t)T * 8 * (upper ? 2 : 1) + (size_t)RING_BYTES + (size_t)T * 8;
+}
+
+template <bool IS_U>
+static cudaError_t configure_sweep() {
+  const int sm = (int)sweep_smem(KKT_CTA_PHASE_MAX_ROWS, IS_U);
+  cudaError_t e = cudaFuncSetAttribute(k_trsv_sweep<IS_U, 32, 256>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_trsv_sweep<IS_U, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_trsv_sweep<IS_U, 8, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  return e;
+}
+
+template <bool IS_U>
+static void launch_sweep(const DevPlan &d, const double *b, double *x, int T, int maxcol,
+                         cudaStream_t s) {
+  const size_t sm = sweep_smem(T, IS_U);
+  if (maxcol <= 256)
+    k_trsv_sweep<IS_U, 32, 256><<<1, SWEEP_THREADS, sm, s>>>(d, b, x);
+  else if (maxcol <= 512)
+    k_trsv_sweep<IS_U, 16, 512><<<1, SWEEP_THREADS, sm, s>>>(d, b, x);
+  else
+    k_trsv_sweep<IS_U, 8, 1024><<<1, SWEEP_THREADS, sm, s>>>(d, b, x);
 }
 
 cudaError_t trsv_configure(int *grid_blocks_per_sm) {
@@ -215,11 +232,8 @@ cudaError_t trsv_configure(int *grid_blocks_per_sm) {
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trsv_grid<true>, 256, 0);
   if (e != cudaSuccess) return e;
   *grid_blocks_per_sm = a < b ? a : b;
-  e = cudaFuncSetAttribute(k_trsv_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sweep_smem(KKT_CTA_PHASE_MAX_ROWS, false));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_trsv_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sweep_smem(KKT_CTA_PHASE_MAX_ROWS, true));
+  e = configure_sweep<false>();
+  if (e == cudaSuccess) e = configure_sweep<true>();
   return e;
 }
 
@@ -232,11 +246,11 @@ cudaError_t launch_trsv(const DevPlan &d, const double *b, double *x, int grid_b
     ++*launches;
   }
   if (TL) {
-    k_trsv_sweep<false><<<1, SWEEP_THREADS, sweep_smem(TL, false), s>>>(d, b, x);
+    launch_sweep<false>(d, b, x, TL, d.sweep_maxL, s);
     ++*launches;
   }
   if (TU) {  // backward: the sweep over the trailing block, then the grid rows
-    k_trsv_sweep<true><<<1, SWEEP_THREADS, sweep_smem(TU, true), s>>>(d, b, x);
+    launch_sweep<true>(d, b, x, TU, d.sweep_maxU, s);
     ++*launches;
   }
   if (d.nUg) {
