@@ -280,7 +280,7 @@ int choose_tail(const HostPlan &P, bool upper) {
   const std::vector<int32_t> &ci = upper ? P.Uci : P.Lci;
   double best = 1e30;
   int bestT = 0;
-  for (int T : {0, 32, 64, 128, 256, 512, 768, 1024, 1536, 2048, 3072, 4096, 5120}) {
+  for (int T : {0, 32, 64, 128, 256, 512, 768, 1024, 1536, 2048, 3072, 4096}) {
     if (T > n || T > KKT_CTA_PHASE_MAX_ROWS) break;
     const int p = n - T;
     // levels of the grid part and of the CTA part

@@ -5,7 +5,7 @@
 
 #include "kkt_internal.h"
 
-#define KKT_CTA_PHASE_MAX_ROWS 5120  // shared-memory rows of the single-CTA sweep phase
+#define KKT_CTA_PHASE_MAX_ROWS 4096  // shared-memory rows of the single-CTA sweep phase
 
 namespace kkt {
 

@@ -26,7 +26,7 @@
 
 namespace kkt {
 
-constexpr int SWEEP_THREADS = 256;
+constexpr int SWEEP_THREADS = 128;  // 4 warps: cheap barrier, <= 2 entries per thread per step
 
 
 
@@ -60,9 +60,16 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
       col = ci[beg + lane];
       v = vals[beg + lane];
     }
+    // every lane issues its first-chunk y load now (older dependencies are normally
+    // published already); lane 0 alone spins on the critical one and broadcasts it
     const int cr = crit[idx];
-    if (lane == 0 && cr >= 0) wait_value(&ysrc[cr], d.poll_ns);
-    __syncwarp();
+    double y0 = 0.0;
+    if (beg + lane < end) y0 = ld_relaxed_f64(&ysrc[col]);
+    double ycr = 0.0;
+    if (lane == 0 && cr >= 0) ycr = wait_value(&ysrc[cr], d.poll_ns);
+    ycr = __shfl_sync(0xffffffffu, ycr, 0);
+    if (cr >= 0 && col == cr) y0 = ycr;
+    bool first = true;
     for (int c0 = beg; c0 < end; c0 += 32) {
       const int cnt = min(32, end - c0);
       double p = 0.0;
@@ -72,7 +79,12 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
         ncol = ci[c0 + 32 + lane];
         nv = vals[c0 + 32 + lane];
       }
-      if (lane < cnt) p = __dmul_rn(v, wait_value(&ysrc[col], d.poll_ns));
+      if (lane < cnt) {
+        double y = first ? y0 : ld_relaxed_f64(&ysrc[col]);
+        if (is_sentinel(y)) y = wait_value(&ysrc[col], d.poll_ns);
+        p = __dmul_rn(v, y);
+      }
+      first = false;
       for (int i = 0; i < cnt; ++i) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, p, i));
       col = ncol;
       v = nv;
@@ -110,6 +122,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
   int *rr = reinterpret_cast<int *>(rv + RING * SLOT);  // [RING*SLOT] rows
   int *cbeg = rr + RING * SLOT;                   // [T] CSC range of step s
   int *cend = cbeg + T;                                       // [T]
+  int *cperm = cend + T;                                      // [T] (U: col_perm)
   const double *cvals = IS_U ? d.Ux : d.Lx;
   const int *crows = IS_U ? d.Ui : d.Li;
   // step s handles column j(s): L ascending from p, U descending from n-1
@@ -117,7 +130,10 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
     const int j = IS_U ? d.n - 1 - s : p + s;
     cbeg[s] = IS_U ? d.Up[j] + d.Uhead_off[j - p] : d.Lp[j];
     cend[s] = IS_U ? d.Up[j + 1] : d.Lp[j + 1];
-    if (IS_U) dg[j - p] = d.udiag[j];
+    if (IS_U) {
+      dg[j - p] = d.udiag[j];
+      cperm[s] = d.col_perm[j];
+    }
   }
   if (IS_U) {
     // acc = L result of the head rows; reset yL for the next solve
@@ -160,7 +176,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
       const double w = unsentinel(yj);
       if (IS_U) {
         d.yU[j] = w;
-        xout[d.col_perm[j]] = yj;
+        xout[cperm[s]] = yj;
         if (!isfinite(yj)) bad = true;
       } else {
         d.yL[j] = w;
@@ -199,7 +215,7 @@ cudaError_t launch_fill_sentinel(double *p, int64_t n, cudaStream_t s) {
 // ring shapes (RING x SLOT entries, 96 KB each): deep rings for short columns
 constexpr int RING_BYTES = 96 * 1024;
 static size_t sweep_smem(int T, bool upper) {
-  return (size_t)T * 8 * (upper ? 2 : 1) + (size_t)RING_BYTES + (size_t)T * 8;
+  return (size_t)T * 8 * (upper ? 2 : 1) + (size_t)RING_BYTES + (size_t)T * 12;
 }
 
 template <bool IS_U>
