@@ -60,16 +60,11 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
       col = ci[beg + lane];
       v = vals[beg + lane];
     }
-    // every lane issues its first-chunk y load now (older dependencies are normally
-    // published already); lane 0 alone spins on the critical one and broadcasts it
+    // lane 0 alone spins on the critical dependency; the other dependencies are then
+    // normally published already, so the lanes' loads below rarely have to wait
     const int cr = crit[idx];
-    double y0 = 0.0;
-    if (beg + lane < end) y0 = ld_relaxed_f64(&ysrc[col]);
-    double ycr = 0.0;
-    if (lane == 0 && cr >= 0) ycr = wait_value(&ysrc[cr], d.poll_ns);
-    ycr = __shfl_sync(0xffffffffu, ycr, 0);
-    if (cr >= 0 && col == cr) y0 = ycr;
-    bool first = true;
+    if (lane == 0 && cr >= 0) wait_value(&ysrc[cr], d.poll_ns);
+    __syncwarp();
     for (int c0 = beg; c0 < end; c0 += 32) {
       const int cnt = min(32, end - c0);
       double p = 0.0;
@@ -79,12 +74,7 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
         ncol = ci[c0 + 32 + lane];
         nv = vals[c0 + 32 + lane];
       }
-      if (lane < cnt) {
-        double y = first ? y0 : ld_relaxed_f64(&ysrc[col]);
-        if (is_sentinel(y)) y = wait_value(&ysrc[col], d.poll_ns);
-        p = __dmul_rn(v, y);
-      }
-      first = false;
+      if (lane < cnt) p = __dmul_rn(v, wait_value(&ysrc[col], d.poll_ns));
       for (int i = 0; i < cnt; ++i) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, p, i));
       col = ncol;
       v = nv;
