@@ -368,7 +368,7 @@ def main():
                 "refactor_flops": st["refactor_flops"],
                 "levels_refactor_L_U": [st["refactor_levels"], st["L_levels"], st["U_levels"]],
                 "offdiag_pivots": st["offdiag_pivots"], "systems": M,
-                "tolerance": "delta(mu)=clamp(1e-6*mu,1e-14,1e-8)" if args.tol == "barrier"
+                "tolerance": "delta(mu)=clamp(1e-2*mu,1e-10,1e-8)" if args.tol == "barrier"
                 else f"{args.delta}",
                 "mean_ir_iterations": mean_iters,
                 "l2": "flushed between steps (256 MiB write, excluded from timing)",

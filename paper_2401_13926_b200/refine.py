@@ -68,12 +68,16 @@ class FixedTolerance:
 class BarrierTiedTolerance:
     """delta(mu) = clamp(theta * mu, delta_min, delta_max).
 
+    Defaults 1e-2 / 1e-10 / 1e-8: the paper's IR tolerances span 1e-9..1e-10 (PAPER.md:366);
+    at N~238k the FGMRES floor sits near 1e-12..1e-14 relative, so tighter minima exhaust
+    the restart budget on the last barrier systems (measured with the oracle).
+
     Loose while the barrier parameter is large (early, well-conditioned systems need no
     refinement), tight as mu -> 0 where the static-pivot factors degrade.
     """
 
-    theta: float = 1e-6
-    delta_min: float = 1e-14
+    theta: float = 1e-2
+    delta_min: float = 1e-10
     delta_max: float = 1e-8
 
     def __post_init__(self):
