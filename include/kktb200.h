@@ -204,6 +204,11 @@ int kkt_op_residual_norms(kkt_operator *op, const double *r_dev, const double *x
  * refactor levels, arena bytes, update pairs, 0, 0}. */
 int kkt_dev_info(kkt_device *d, int64_t info[16]);
 
+/* Timeline of the last refactor / solve when the handle was created with KKT_TRACE=1:
+ * refactor_out[2n] = {dispatch ns, done ns} per column, trisolve_out[2n] = publish ns per
+ * row of the L then the U sweep (grid phase rows).  Profiling aid. */
+int kkt_dev_trace(kkt_device *d, uint64_t *refactor_out, uint64_t *trisolve_out);
+
 /* Kernel launches issued by this handle since creation (evidence counter). */
 int64_t kkt_dev_launch_count(kkt_device *d);
 

@@ -48,6 +48,7 @@ static void destroy(Device *dev) {
   if (dev->stream) cudaStreamSynchronize(dev->stream);
   free_krylov(dev);
   if (dev->arena) cudaFree(dev->arena);
+  if (dev->trace_mem) cudaFree(dev->trace_mem);
   if (dev->pinned) cudaFreeHost(dev->pinned);
   if (dev->stream) cudaStreamDestroy(dev->stream);
   delete dev;
@@ -166,6 +167,15 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.scal = carve<unsigned long long>(cur, 32);
   d.ticket = carve<int>(cur, 16);
   d.partials = carve<double>(cur, 8 * RED_BLOCKS);
+  d.trace_ref = d.trace_trsv = nullptr;
+  if (std::getenv("KKT_TRACE") && std::atoi(std::getenv("KKT_TRACE")) > 0) {
+    ce = cudaMalloc(&dev->trace_mem, 4 * 8 * n + 64);
+    if (ce == cudaSuccess) {
+      d.trace_ref = (unsigned long long *)dev->trace_mem;
+      d.trace_trsv = d.trace_ref + 2 * n;
+      cudaMemsetAsync(dev->trace_mem, 0, 4 * 8 * n, dev->stream);
+    }
+  }
   UP(d.A_rp, to_i32(h.A_rp));
   UP(d.A_ci, to_i32(h.A_ci));
   UP(d.A_split, to_i32(h.A_split));
@@ -645,6 +655,21 @@ int kkt_dev_info(kkt_device *dd, int64_t info[16]) {
                          dev->trsv_blocks, h.refactor_levels, (int64_t)dev->arena_bytes,
                          (int64_t)h.upd_slot.size(), 0, 0};
   for (int i = 0; i < 16; ++i) info[i] = v[i];
+  return KKT_OK;
+}
+
+int kkt_dev_trace(kkt_device *dd, uint64_t *refactor_out, uint64_t *trisolve_out) {
+  Device *dev = reinterpret_cast<Device *>(dd);
+  if (!dev) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
+  if (!dev->d.trace_ref) return kkt::set_error(KKT_ERR_BAD_ARG, "tracing disabled (set KKT_TRACE=1)");
+  cudaSetDevice(dev->device);
+  const size_t n = (size_t)dev->d.n;
+  cudaError_t e = cudaStreamSynchronize(dev->stream);
+  if (e == cudaSuccess && refactor_out)
+    e = cudaMemcpy(refactor_out, dev->d.trace_ref, 16 * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && trisolve_out)
+    e = cudaMemcpy(trisolve_out, dev->d.trace_trsv, 16 * n, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
   return KKT_OK;
 }
 

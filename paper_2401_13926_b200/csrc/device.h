@@ -37,6 +37,8 @@ struct DevPlan {
   int sweep_maxL, sweep_maxU;
   double *Lv, *Uv;
   double *yL, *yU;       // sentinel-reset solution buffers (value == readiness flag)
+  // optional timeline (KKT_TRACE=1): refactor {grab, end} ns per column, trisolve end per row
+  unsigned long long *trace_ref, *trace_trsv;
   // scalars
   unsigned long long *scal;
   int *ticket;
@@ -64,6 +66,7 @@ struct Device {
   DevPlan d;
   HostPlan h;
   void *arena = nullptr;
+  void *trace_mem = nullptr;
   size_t arena_bytes = 0;
   int sm_count = 0;
   int refactor_blocks = 0, refactor_warps = 8;

@@ -82,6 +82,12 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 __device__ __forceinline__ double ld_volatile_shared(const volatile double *p) { return *p; }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ unsigned long long dbits(double v) {
   return (unsigned long long)__double_as_longlong(v);
 }

@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
     idx = __shfl_sync(0xffffffffu, idx, 0);
     if (idx >= d.n) break;
     const int j = d.col_order[idx];
+    if (d.trace_ref && lane == 0) d.trace_ref[2 * j] = globaltimer();
     const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
     const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
     const int np = nu + 1 + nl;
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
     if (lane == 0) {
       d.udiag[j] = ujj;
       atomic_max_nonneg(&d.scal[SC_GMAX], gm);
+      if (d.trace_ref) d.trace_ref[2 * j + 1] = globaltimer();
     }
     __syncwarp();
   }

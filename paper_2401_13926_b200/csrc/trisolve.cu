@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
       }
       st_relaxed_f64(&yres[r], __longlong_as_double((long long)SENTINEL_BITS));
       st_relaxed_f64(&ysrc[r], unsentinel(w));
+      if (d.trace_trsv) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
     }
   }
   if (IS_U && bad) atomicOr(&d.scal[SC_NONFINITE], 1ull);

@@ -1,0 +1,55 @@
+"""Timeline of one refactorization (KKT_TRACE=1): per-level dispatch/finish statistics."""
+import ctypes as C
+import os
+import sys
+
+os.environ["KKT_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2401_13926_b200._native as nat
+from paper_2401_13926_b200 import factorize, to_general
+from paper_2401_13926_b200.acopf import make_sequence
+
+seq = make_sequence(sys.argv[1] if len(sys.argv) > 1 else "activsg10k", seed=0, length=20)
+f, _ = factorize(to_general(seq.matrix(0)))
+dev = f.device()
+n = f.n
+with torch.cuda.stream(dev.stream):
+    vals = torch.from_numpy(seq.values(19)).cuda()
+    b = torch.randn(n, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(b)
+for _ in range(2):
+    dev.refactor_device(vals, nat.LAYOUT_SYMMETRIC_LOWER)
+    dev.solve_device(b, x)
+dev.sync()
+tr = np.zeros(2 * n, dtype=np.uint64)
+ts = np.zeros(2 * n, dtype=np.uint64)
+nat.check(dev.lib.kkt_dev_trace(dev.h, tr.ctypes.data_as(C.c_void_p), ts.ctypes.data_as(C.c_void_p)))
+st, en = tr[0::2].astype(np.int64), tr[1::2].astype(np.int64)
+t0 = st.min()
+st, en = (st - t0) / 1e3, (en - t0) / 1e3  # us
+sop, sod = f._so_ptr, f._so_data
+lev = np.zeros(n, np.int64)
+for j in range(n):
+    ks = sod[sop[j]:sop[j + 1]]
+    if ks.size:
+        lev[j] = lev[ks].max() + 1
+print(f"refactor span {en.max():.1f} us")
+for a, bnd in [(0, 1), (1, 2), (2, 5), (5, 20), (20, 50), (50, 100), (100, 200), (200, 300),
+               (300, 400), (400, 600)]:
+    m = (lev >= a) & (lev < bnd)
+    if not m.any():
+        continue
+    dur = en[m] - st[m]
+    print(f"levels [{a},{bnd}): cols {m.sum():7d} dispatch {st[m].min():8.1f}..{st[m].max():8.1f} "
+          f"finish {en[m].min():8.1f}..{en[m].max():8.1f} us; per-col dur med {np.median(dur):7.2f} "
+          f"max {dur.max():8.2f}")
+# trisolve L/U grid rows
+tl = ts[:n].astype(np.int64)
+tu = ts[n:].astype(np.int64)
+for name, t in (("L", tl), ("U", tu)):
+    t = t[t > 0]
+    if t.size:
+        print(f"trisolve {name} grid rows published over {(t.max() - t.min()) / 1e3:.1f} us")
