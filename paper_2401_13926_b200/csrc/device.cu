@@ -89,6 +89,9 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.n_upd = (int64_t)h.upd_slot.size();
   d.n_ap = (int64_t)h.a_src.size();
   d.maxpat = h.maxpat;
+  d.n_small_levels = h.n_small_levels;
+  for (int l = 0; l <= h.n_small_levels; ++l) d.lev_ptr[l] = h.small_lev_ptr[l];
+  d.ref_start = h.small_lev_ptr[h.n_small_levels];
   d.poll_ns = std::getenv("KKT_POLL_NS") ? std::atoi(std::getenv("KKT_POLL_NS")) : 0;
   d.pL = h.pL;
   d.pU = h.pU;
@@ -271,7 +274,11 @@ static int refactor(Device *dev, const double *vals, int layout, int on_device, 
   if (rc != KKT_OK) return rc;
   const unsigned long long big = 0x7FF0000000000000ull;  // +inf bits for the min
   CUDA_TRY(cudaMemcpyAsync(&d.scal[SC_MINPIV], &big, 8, cudaMemcpyHostToDevice, dev->stream));
-  LAUNCH(launch_refactor(d, dev->refactor_blocks, dev->refactor_warps, dev->refactor_smem, dev->stream));
+  {
+    cudaError_t e = launch_refactor(d, dev->refactor_blocks, dev->refactor_warps, dev->refactor_smem,
+                                    dev->stream, &dev->launches);
+    if (e != cudaSuccess) return set_error(KKT_ERR_CUDA, std::string("refactor: ") + cudaGetErrorString(e));
+  }
   LAUNCH(launch_diag_stats(d, dev->sm_count, dev->stream));
   if (diag_out) {
     CUDA_TRY(cudaMemcpyAsync(dev->pinned, d.scal, 8 * SC_COUNT, cudaMemcpyDeviceToHost, dev->stream));

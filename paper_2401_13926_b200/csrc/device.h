@@ -19,6 +19,9 @@ struct DevPlan {
   int n = 0, sym_lower = 0, has_lower = 0;
   int64_t nnz_a = 0, in_nnz = 0, nnz_L = 0, nnz_U = 0, n_so = 0, n_upd = 0, n_ap = 0;
   int maxpat = 1;
+  int ref_start = 0;       // first col_order index handled by the warp kernel
+  int n_small_levels = 0;  // leading levels run by k_refactor_small
+  int lev_ptr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // col_order offsets of those levels
   int poll_ns = 0;  // __nanosleep back-off while polling (env KKT_POLL_NS)
   // operator
   int *A_rp, *A_ci, *A_split, *gen_src;
@@ -80,7 +83,8 @@ struct Device {
 
 // ---- launchers (each returns cudaGetLastError of its launch) ----
 cudaError_t launch_expand_norms(const DevPlan &d, cudaStream_t s);
-cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem, cudaStream_t s);
+cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem, cudaStream_t s,
+                            long long *launches);
 cudaError_t launch_diag_stats(const DevPlan &d, int blocks, cudaStream_t s);
 cudaError_t refactor_configure(int warps, size_t smem, int *blocks_per_sm);
 size_t refactor_smem_bytes(int warps, int maxpat);

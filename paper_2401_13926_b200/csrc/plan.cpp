@@ -130,12 +130,29 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     P.so_meta[4 * t + 0] = P.so_slot[t];
     P.so_meta[4 * t + 1] = (int32_t)(S.Lp[k + 1] - S.Lp[k]);
     P.so_meta[4 * t + 2] = P.upd_ptr[t];
+    P.so_meta[4 * t + 3] = (int32_t)S.Lp[k];
     for (int64_t e = 0; e < S.Lp[k + 1] - S.Lp[k]; ++e) P.upd_lidx[P.upd_ptr[t] + e] = (int32_t)(S.Lp[k] + e);
   }
   P.maxpat = maxpat;
   P.col_order = order_by_level(lev);
   P.refactor_levels = 0;
   for (int32_t l : lev) P.refactor_levels = std::max(P.refactor_levels, l + 1);
+  {
+    // leading levels that are wide (>= 2048 columns) with small patterns (<= 64 slots):
+    // thread-per-column launches instead of one warp per column
+    std::vector<int64_t> cnt(P.refactor_levels + 1, 0), mp(P.refactor_levels + 1, 0);
+    for (int64_t j = 0; j < n; ++j) {
+      cnt[lev[j]]++;
+      mp[lev[j]] = std::max<int64_t>(mp[lev[j]], S.Up[j + 1] - S.Up[j] + 1 + S.Lp[j + 1] - S.Lp[j]);
+    }
+    P.small_lev_ptr.assign(1, 0);
+    int32_t l = 0;
+    while (l < P.refactor_levels && l < 8 && cnt[l] >= 2048 && mp[l] <= 64) {
+      P.small_lev_ptr.push_back(P.small_lev_ptr.back() + (int32_t)cnt[l]);
+      ++l;
+    }
+    P.n_small_levels = l;
+  }
 
   // ---------------- trisolves: CSR of L (ascending cols) and U (descending cols) -------
   P.Lrp.assign(n + 1, 0);

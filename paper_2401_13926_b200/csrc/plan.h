@@ -23,6 +23,9 @@ struct HostPlan {
   std::vector<int32_t> so_data, upd_ptr, a_src, col_order;
   std::vector<uint16_t> so_slot, upd_slot, a_slot;
   int32_t maxpat = 1, refactor_levels = 0;
+  // leading levels refactorized thread-per-column: offsets into col_order (<= 8 levels)
+  int32_t n_small_levels = 0;
+  std::vector<int32_t> small_lev_ptr;
   // per so-entry metadata {slot of k in pattern(j), |L(:,k)|, first update pair, 0} and,
   // per update pair, the CSC index of the L(:,k) entry it consumes
   std::vector<int32_t> so_meta, upd_lidx;

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
   int *st_s = reinterpret_cast<int *>(st_l + REFACTOR_STAGE);
   while (true) {
     int idx = 0;
-    if (lane == 0) idx = atomicAdd(d.ticket, 1);
+    if (lane == 0) idx = d.ref_start + atomicAdd(d.ticket, 1);
     idx = __shfl_sync(0xffffffffu, idx, 0);
     if (idx >= d.n) break;
     const int j = d.col_order[idx];
@@ -135,32 +135,35 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
         const int cnt = __shfl_sync(0xffffffffu, m.y, i);
         const int off = __shfl_sync(0xffffffffu, incl - m.y, i);
         const double xk = x[kslot];
+        const int lbk = __shfl_sync(0xffffffffu, m.w, i);  // L(:,k) = Lx[lbk, lbk+cnt)
         if (!big) {
           // L(:,k) not yet published when staged?  One lane waits (with back-off) so a
           // column many warps depend on is not polled by every lane of every consumer;
-          // the rest then re-read their entries (normally already visible).
+          // then the whole step is re-staged with one parallel round trip.
           bool miss = false;
           for (int e = lane; e < cnt; e += 32) miss |= is_sentinel(st_l[off + e]);
           const unsigned mm = __ballot_sync(0xffffffffu, miss);
           if (mm) {
-            if (lane == __ffs(mm) - 1) {
-              for (int e = lane; e < cnt; e += 32)
-                if (is_sentinel(st_l[off + e])) {
-                  wait_value_backoff(&d.Lx[d.upd_lidx[pair0 + off + e]]);
-                  break;
-                }
-            }
+            if (lane == __ffs(mm) - 1) wait_value_backoff(&d.Lx[lbk + cnt - 1]);
             __syncwarp();
+            double lv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (lane + 32 * q < cnt) lv[q] = ld_relaxed_f64(&d.Lx[lbk + lane + 32 * q]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (lane + 32 * q < cnt) st_l[off + lane + 32 * q] = lv[q];
+            for (int e = lane + 256; e < cnt; e += 32) st_l[off + e] = ld_relaxed_f64(&d.Lx[lbk + e]);
           }
           for (int e = lane; e < cnt; e += 32) {
             double l = st_l[off + e];
-            if (is_sentinel(l)) l = wait_value(&d.Lx[d.upd_lidx[pair0 + off + e]]);
+            if (is_sentinel(l)) l = wait_value(&d.Lx[lbk + e]);  // rare: store not yet visible
             const int s = st_s[off + e];
             x[s] = __dsub_rn(x[s], __dmul_rn(l, xk));
           }
         } else {
           for (int e = lane; e < cnt; e += 32) {
-            const double l = wait_value_backoff(&d.Lx[d.upd_lidx[pair0 + e]]);
+            const double l = wait_value_backoff(&d.Lx[lbk + e]);
             const int s = d.upd_slot[pair0 + e];
             x[s] = __dsub_rn(x[s], __dmul_rn(l, xk));
           }
@@ -200,6 +203,59 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
   }
 }
 
+// ----------------------------------------------------------------------------
+// Wide leading levels (level 0: no replay steps; level 1: <= a few) hold most columns but
+// almost no work: one thread per column, one launch per level (the kernel boundary is the
+// dependency), workspace in local memory.  Same arithmetic order as k_refactor.
+// ----------------------------------------------------------------------------
+constexpr int SMALL_PAT = 64;
+
+__global__ void __launch_bounds__(256) k_refactor_small(DevPlan d, int begin, int end) {
+  const double eps =
+      __dmul_rn(PATCH_RELATIVE_FLOOR, __longlong_as_double((long long)d.scal[SC_INFNORM]));
+  const int idx = begin + blockIdx.x * blockDim.x + threadIdx.x;
+  double gm = 0.0;
+  if (idx < end) {
+    const int j = d.col_order[idx];
+    const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
+    const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
+    double x[SMALL_PAT];
+#pragma unroll 1
+    for (int s = 0; s < nu + 1 + nl; ++s) x[s] = 0.0;
+    for (int q = d.ap_ptr[j]; q < d.ap_ptr[j + 1]; ++q) x[d.a_slot[q]] = d.A_vals[d.a_src[q]];
+    for (int t = d.so_ptr[j]; t < d.so_ptr[j + 1]; ++t) {
+      const int4 m = d.so_meta[t];
+      const double xk = x[m.x];
+      for (int e = 0; e < m.y; ++e) {
+        const int s = d.upd_slot[m.z + e];
+        x[s] = __dsub_rn(x[s], __dmul_rn(ldcg(&d.Lx[m.w + e]), xk));
+      }
+    }
+    for (int s = 0; s < nu; ++s) {
+      d.Ux[ub + s] = x[s];
+      d.Uv[d.Umap[ub + s]] = x[s];
+      gm = fmax(gm, fabs(x[s]));
+    }
+    double ujj = x[nu];
+    gm = fmax(gm, fabs(ujj));
+    if (fabs(ujj) < eps) {
+      ujj = (ujj >= 0.0) ? eps : -eps;
+      atomicAdd(&d.scal[SC_PATCHED], 1ull);
+    }
+    for (int s = 0; s < nl; ++s) {
+      const double v = x[nu + 1 + s];
+      gm = fmax(gm, fabs(v));
+      const double l = unsentinel(__ddiv_rn(v, ujj));
+      d.Lv[d.Lmap[lb + s]] = l;
+      d.Lx[lb + s] = l;
+    }
+    d.udiag[j] = ujj;
+    if (d.trace_ref) d.trace_ref[2 * j] = d.trace_ref[2 * j + 1] = globaltimer();
+  }
+  gm = warp_max(gm);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(&d.scal[SC_GMAX], gm);
+}
+
 __global__ void k_diag_stats(DevPlan d) {
   double mx = 0.0, mn = INFINITY;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x) {
@@ -228,13 +284,25 @@ cudaError_t refactor_configure(int warps, size_t smem, int *blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_refactor, 32 * warps, smem);
 }
 
-cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem, cudaStream_t s) {
+cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem, cudaStream_t s,
+                            long long *launches) {
   if (!d.n) return cudaSuccess;
   // readiness protocol: L(:,k) entries start as the sentinel
   cudaError_t e = cudaMemsetAsync(d.Lx, 0xFF, 8 * (size_t)d.nnz_L, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.ticket, 0, 4, s);
   if (e != cudaSuccess) return e;
-  k_refactor<<<blocks, 32 * warps, smem, s>>>(d);
+  // wide leading levels: thread per column, level-synchronous
+  for (int l = 0; l < d.n_small_levels; ++l) {
+    const int b = d.lev_ptr[l], en = d.lev_ptr[l + 1];
+    if (en > b) {
+      k_refactor_small<<<(en - b + 255) / 256, 256, 0, s>>>(d, b, en);
+      ++*launches;
+    }
+  }
+  if (d.ref_start < d.n) {
+    k_refactor<<<blocks, 32 * warps, smem, s>>>(d);
+    ++*launches;
+  }
   return cudaGetLastError();
 }
 
