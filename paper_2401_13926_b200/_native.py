@@ -84,6 +84,7 @@ SIGNATURES = [
     ("kkt_op_residual_norms", C.c_int, [vp, vp, vp, f64p]),
     ("kkt_dev_info", C.c_int, [vp, i64p]),
     ("kkt_dev_trace", C.c_int, [vp, vp, vp]),
+    ("kkt_dev_trace_steps", C.c_int, [vp, vp]),
     ("kkt_dev_launch_count", i64, [vp]),
 ]
 

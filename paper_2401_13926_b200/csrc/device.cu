@@ -170,13 +170,15 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.scal = carve<unsigned long long>(cur, 32);
   d.ticket = carve<int>(cur, 16);
   d.partials = carve<double>(cur, 8 * RED_BLOCKS);
-  d.trace_ref = d.trace_trsv = nullptr;
+  d.trace_ref = d.trace_trsv = d.trace_step = nullptr;
   if (std::getenv("KKT_TRACE") && std::atoi(std::getenv("KKT_TRACE")) > 0) {
-    ce = cudaMalloc(&dev->trace_mem, 4 * 8 * n + 64);
+    const size_t tb = 4 * 8 * n + 8 * (size_t)d.n_so;
+    ce = cudaMalloc(&dev->trace_mem, tb + 64);
     if (ce == cudaSuccess) {
       d.trace_ref = (unsigned long long *)dev->trace_mem;
       d.trace_trsv = d.trace_ref + 2 * n;
-      cudaMemsetAsync(dev->trace_mem, 0, 4 * 8 * n, dev->stream);
+      d.trace_step = d.trace_trsv + 2 * n;
+      cudaMemsetAsync(dev->trace_mem, 0, tb, dev->stream);
     }
   }
   UP(d.A_rp, to_i32(h.A_rp));
@@ -662,6 +664,17 @@ int kkt_dev_info(kkt_device *dd, int64_t info[16]) {
                          dev->trsv_blocks, h.refactor_levels, (int64_t)dev->arena_bytes,
                          (int64_t)h.upd_slot.size(), 0, 0};
   for (int i = 0; i < 16; ++i) info[i] = v[i];
+  return KKT_OK;
+}
+
+int kkt_dev_trace_steps(kkt_device *dd, uint64_t *steps_out) {
+  Device *dev = reinterpret_cast<Device *>(dd);
+  if (!dev || !dev->d.trace_step) return kkt::set_error(KKT_ERR_BAD_ARG, "tracing disabled");
+  cudaSetDevice(dev->device);
+  cudaError_t e = cudaStreamSynchronize(dev->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(steps_out, dev->d.trace_step, 8 * (size_t)dev->d.n_so, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
   return KKT_OK;
 }
 

@@ -41,7 +41,7 @@ struct DevPlan {
   double *Lv, *Uv;
   double *yL, *yU;       // sentinel-reset solution buffers (value == readiness flag)
   // optional timeline (KKT_TRACE=1): refactor {grab, end} ns per column, trisolve end per row
-  unsigned long long *trace_ref, *trace_trsv;
+  unsigned long long *trace_ref, *trace_trsv, *trace_step;
   // scalars
   unsigned long long *scal;
   int *ticket;

@@ -147,7 +147,7 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     }
     P.small_lev_ptr.assign(1, 0);
     int32_t l = 0;
-    while (l < P.refactor_levels && l < 8 && cnt[l] >= 2048 && mp[l] <= 64) {
+    while (l < P.refactor_levels && l < 2 && cnt[l] >= 2048 && mp[l] <= 64) {
       P.small_lev_ptr.push_back(P.small_lev_ptr.back() + (int32_t)cnt[l]);
       ++l;
     }

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
           for (int e = lane; e < cnt; e += 32) miss |= is_sentinel(st_l[off + e]);
           const unsigned mm = __ballot_sync(0xffffffffu, miss);
           if (mm) {
-            if (lane == __ffs(mm) - 1) wait_value_backoff(&d.Lx[lbk + cnt - 1]);
+            if (lane == __ffs(mm) - 1) wait_value(&d.Lx[lbk + cnt - 1], d.poll_ns);
             __syncwarp();
             double lv[8];
 #pragma unroll
@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
             const int s = st_s[off + e];
             x[s] = __dsub_rn(x[s], __dmul_rn(l, xk));
           }
+          if (d.trace_step && lane == 0) d.trace_step[t0 + i] = globaltimer() | (mm ? 1ull : 0ull);
         } else {
           for (int e = lane; e < cnt; e += 32) {
             const double l = wait_value_backoff(&d.Lx[lbk + e]);
@@ -172,14 +173,9 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
       }
       t0 += nsteps;
     }
-    // U(:,j) = x[Ui]; u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj            (:327-344)
+    // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj; U(:,j) = x[Ui]               (:327-344)
+    // L(:,j) is what other columns wait for: publish it first, bookkeeping after.
     double gm = 0.0;
-    for (int s = lane; s < nu; s += 32) {
-      const double v = x[s];
-      d.Ux[ub + s] = v;
-      d.Uv[d.Umap[ub + s]] = v;
-      gm = fmax(gm, fabs(v));
-    }
     double ujj = x[nu];
     gm = fmax(gm, fabs(ujj));
     if (fabs(ujj) < eps) {
@@ -189,9 +185,39 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
     for (int s = lane; s < nl; s += 32) {
       const double v = x[nu + 1 + s];
       gm = fmax(gm, fabs(v));
-      const double l = unsentinel(__ddiv_rn(v, ujj));
-      d.Lv[d.Lmap[lb + s]] = l;
-      st_relaxed_f64(&d.Lx[lb + s], l);  // publishes L(:,j): value == readiness
+      st_relaxed_f64(&d.Lx[lb + s], unsentinel(__ddiv_rn(v, ujj)));  // value == readiness
+    }
+    // CSR copies for the solves (scatter through the maps: batch the map loads)
+    for (int s0 = 0; s0 < nl; s0 += 128) {
+      int mp[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int s = s0 + 32 * q + lane;
+        mp[q] = s < nl ? d.Lmap[lb + s] : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int s = s0 + 32 * q + lane;
+        if (s < nl) d.Lv[mp[q]] = unsentinel(__ddiv_rn(x[nu + 1 + s], ujj));
+      }
+    }
+    for (int s0 = 0; s0 < nu; s0 += 128) {
+      int mp[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int s = s0 + 32 * q + lane;
+        mp[q] = s < nu ? d.Umap[ub + s] : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int s = s0 + 32 * q + lane;
+        if (s < nu) {
+          const double v = x[s];
+          d.Ux[ub + s] = v;
+          d.Uv[mp[q]] = v;
+          gm = fmax(gm, fabs(v));
+        }
+      }
     }
     gm = warp_max(gm);
     if (lane == 0) {

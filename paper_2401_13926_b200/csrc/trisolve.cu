@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
     const int beg = rp[r], end = partial ? d.Ltail_split[r - d.pL] : rp[r + 1];
     // independent loads first: the initial value and the first chunk's pattern/values
     double acc = IS_U ? ldcg(&d.yL[r]) : b[d.row_perm[r]];
+    const double piv = IS_U ? d.udiag[r] : 1.0;  // prefetched: off the critical path
     int col = 0;
     double v = 0.0;
     if (beg + lane < end) {
@@ -85,14 +86,14 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
         d.tacc[r - d.pL] = acc;
         continue;
       }
+      if (IS_U) w = __ddiv_rn(acc, piv);
+      st_relaxed_f64(&ysrc[r], unsentinel(w));  // publish first: other rows wait on it
+      if (d.trace_trsv) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
+      st_relaxed_f64(&yres[r], __longlong_as_double((long long)SENTINEL_BITS));
       if (IS_U) {
-        w = __ddiv_rn(acc, d.udiag[r]);
         xout[d.col_perm[r]] = w;
         if (!isfinite(w)) bad = true;
       }
-      st_relaxed_f64(&yres[r], __longlong_as_double((long long)SENTINEL_BITS));
-      st_relaxed_f64(&ysrc[r], unsentinel(w));
-      if (d.trace_trsv) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
     }
   }
   if (IS_U && bad) atomicOr(&d.scal[SC_NONFINITE], 1ull);

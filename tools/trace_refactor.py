@@ -46,6 +46,23 @@ for a, bnd in [(0, 1), (1, 2), (2, 5), (5, 20), (20, 50), (50, 100), (100, 200),
     print(f"levels [{a},{bnd}): cols {m.sum():7d} dispatch {st[m].min():8.1f}..{st[m].max():8.1f} "
           f"finish {en[m].min():8.1f}..{en[m].max():8.1f} us; per-col dur med {np.median(dur):7.2f} "
           f"max {dur.max():8.2f}")
+# hop decomposition on the deep chain: F(k*) -> step k* applied in column j -> F(j)
+steps = np.zeros(sod.size, dtype=np.uint64)
+nat.check(dev.lib.kkt_dev_trace_steps(dev.h, steps.ctypes.data_as(C.c_void_p)))
+late = (steps & np.uint64(1)).astype(bool)
+stt = ((steps & ~np.uint64(1)).astype(np.int64) - t0) / 1e3
+deep = np.flatnonzero(lev >= 300)
+det, fin, prev = [], [], []
+for j in deep:
+    a, b = sop[j], sop[j + 1]
+    if b - a < 2:
+        continue
+    k = sod[b - 1]
+    det.append(stt[b - 1] - en[k])
+    fin.append(en[j] - stt[b - 1])
+    prev.append(stt[b - 1] - stt[b - 2])
+print(f"deep hop: F(k*)->applied median {np.median(det):.2f} us, applied->F(j) median {np.median(fin):.2f} us, "
+      f"gap between last two steps median {np.median(prev):.2f} us; late-step fraction {late[sop[deep[0]]:].mean():.2f}")
 # trisolve L/U grid rows
 tl = ts[:n].astype(np.int64)
 tu = ts[n:].astype(np.int64)
