@@ -70,3 +70,31 @@ for name, t in (("L", tl), ("U", tu)):
     t = t[t > 0]
     if t.size:
         print(f"trisolve {name} grid rows published over {(t.max() - t.min()) / 1e3:.1f} us")
+# trisolve L grid hop: publish(r) - publish(critical dep) for rows in the narrow levels
+info = dev.info()
+pL = info["pL"]
+Lp_, Li_ = f._Lp, f._Li
+rows_of = [[] for _ in range(n)]
+levL = np.zeros(n, np.int64)
+# CSR of L: row r's columns
+order = np.argsort(Li_, kind="stable")
+cols = np.repeat(np.arange(n), np.diff(Lp_))[order]
+rr = Li_[order]
+rptr = np.zeros(n + 1, np.int64)
+np.cumsum(np.bincount(rr, minlength=n), out=rptr[1:])
+for r in range(n):
+    cs = cols[rptr[r]:rptr[r + 1]]
+    if cs.size:
+        levL[r] = levL[cs].max() + 1
+tl = ts[:n].astype(np.int64)
+hops = []
+for r in range(pL):
+    cs = cols[rptr[r]:rptr[r + 1]]
+    if cs.size == 0 or levL[r] < 50:
+        continue
+    c = cs[np.flatnonzero(levL[cs] == levL[cs].max())[-1]]
+    if tl[r] and tl[c]:
+        hops.append((tl[r] - tl[c]) / 1e3)
+if hops:
+    hops = np.array(hops)
+    print(f"L grid hop (levels>=50): median {np.median(hops):.2f} us, p90 {np.percentile(hops, 90):.2f} us, n={hops.size}")
