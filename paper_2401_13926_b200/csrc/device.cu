@@ -66,9 +66,10 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   const HostPlan &h = dev->h;
   dev->device = opts ? opts->device : 0;
   dev->restart_m = (opts && opts->restart_m > 0) ? opts->restart_m : 10;
-  if (opts && opts->batch > 1) {
+  const int nb = (opts && opts->batch > 1) ? opts->batch : 1;
+  if (nb > 64) {
     delete dev;
-    return set_error(KKT_ERR_BAD_ARG, "batch > 1 is not supported by this handle type");
+    return set_error(KKT_ERR_BAD_ARG, "batch must be <= 64");
   }
   cudaError_t ce = cudaSetDevice(dev->device);
   if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&dev->stream, cudaStreamNonBlocking);
@@ -79,6 +80,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   cudaDeviceGetAttribute(&dev->sm_count, cudaDevAttrMultiProcessorCount, dev->device);
   DevPlan &d = dev->d;
   d.n = h.n;
+  d.nb = nb;
+  d.rb = std::max(8, RED_BLOCKS / nb);  // reduction blocks per system
   d.sym_lower = 0;
   d.has_lower = h.has_lower;
   d.nnz_a = h.nnz_a;
@@ -99,25 +102,26 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.nUg = (int)h.U_grid_order.size();
   d.sweep_maxL = h.sweep_maxL;
   d.sweep_maxU = h.sweep_maxU;
-  const size_t n = (size_t)h.n;
+  const size_t n = (size_t)h.n, B = (size_t)nb;
   const size_t in_cap = (size_t)std::max(d.in_nnz, d.nnz_a);
+  d.in_cap = (int64_t)in_cap;
   size_t bytes = 0;
   auto acc = [&](size_t b) { bytes += align_up(b + 1); };
   acc(4 * (n + 1)); acc(4 * d.nnz_a); acc(4 * n); acc(4 * d.nnz_a);  // A_rp ci split gen_src
-  acc(8 * in_cap); acc(8 * d.nnz_a);                                 // in_vals A_vals
+  acc(8 * in_cap * B); acc(8 * d.nnz_a * B);                         // in_vals A_vals
   acc(4 * (n + 1)); acc(4 * (n + 1)); acc(4 * d.n_ap); acc(4 * n);   // so_ptr ap_ptr a_src order
   acc(4 * (n + 1)); acc(4 * (n + 1)); acc(4 * d.nnz_L); acc(4 * d.nnz_U);  // Lp Up Lmap Umap
   acc(4 * d.n_upd); acc(16 * d.n_so); acc(2 * d.n_upd); acc(2 * d.n_ap);   // lidx meta slots
-  acc(8 * d.nnz_L); acc(8 * d.nnz_U); acc(8 * n);                          // Lx Ux udiag
+  acc(8 * d.nnz_L * B); acc(8 * d.nnz_U * B); acc(8 * n * B);              // Lx Ux udiag
   acc(4 * (n + 1)); acc(4 * d.nnz_L); acc(4 * (n + 1)); acc(4 * d.nnz_U);  // Lrp Lci Urp Uci
   acc(4 * n); acc(4 * n);                                                  // perms
   acc(4 * h.L_grid_order.size()); acc(4 * h.L_tail_order.size());
   acc(4 * h.U_head_order.size()); acc(4 * h.U_grid_order.size());
   acc(4 * h.L_crit.size()); acc(4 * h.U_crit.size()); acc(4 * h.Uhead_off.size());
   acc(4 * d.nnz_L); acc(4 * d.nnz_U);                                      // Li Ui (CSC)
-  acc(4 * h.Ltail_split.size()); acc(8 * h.Ltail_split.size());            // split, tacc
-  acc(8 * d.nnz_L); acc(8 * d.nnz_U); acc(8 * n); acc(8 * n);              // Lv Uv yL yU
-  acc(8 * 32); acc(64); acc(8 * 8 * RED_BLOCKS);                           // scal ticket partials
+  acc(4 * h.Ltail_split.size()); acc(8 * h.Ltail_split.size() * B);        // split, tacc
+  acc(8 * d.nnz_L * B); acc(8 * d.nnz_U * B); acc(8 * n * B); acc(8 * n * B);  // Lv Uv yL yU
+  acc(8 * SCAL_STRIDE * B); acc(64); acc(8 * 8 * (size_t)d.rb * B);        // scal ticket partials
   ce = cudaMalloc(&dev->arena, bytes);
   if (ce != cudaSuccess) {
     destroy(dev);
@@ -129,8 +133,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.A_ci = carve<int>(cur, d.nnz_a);
   d.A_split = carve<int>(cur, n);
   d.gen_src = carve<int>(cur, d.nnz_a);
-  d.in_vals = carve<double>(cur, in_cap);
-  d.A_vals = carve<double>(cur, d.nnz_a);
+  d.in_vals = carve<double>(cur, in_cap * B);
+  d.A_vals = carve<double>(cur, d.nnz_a * B);
   d.so_ptr = carve<int>(cur, n + 1);
   d.ap_ptr = carve<int>(cur, n + 1);
   d.a_src = carve<int>(cur, d.n_ap);
@@ -143,9 +147,9 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.so_meta = carve<int4>(cur, d.n_so);
   d.upd_slot = carve<uint16_t>(cur, d.n_upd);
   d.a_slot = carve<uint16_t>(cur, d.n_ap);
-  d.Lx = carve<double>(cur, d.nnz_L);
-  d.Ux = carve<double>(cur, d.nnz_U);
-  d.udiag = carve<double>(cur, n);
+  d.Lx = carve<double>(cur, d.nnz_L * B);
+  d.Ux = carve<double>(cur, d.nnz_U * B);
+  d.udiag = carve<double>(cur, n * B);
   d.Lrp = carve<int>(cur, n + 1);
   d.Lci = carve<int>(cur, d.nnz_L);
   d.Urp = carve<int>(cur, n + 1);
@@ -162,14 +166,14 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.Li = carve<int>(cur, d.nnz_L);
   d.Ui = carve<int>(cur, d.nnz_U);
   d.Ltail_split = carve<int>(cur, h.Ltail_split.size());
-  d.tacc = carve<double>(cur, h.Ltail_split.size());
-  d.Lv = carve<double>(cur, d.nnz_L);
-  d.Uv = carve<double>(cur, d.nnz_U);
-  d.yL = carve<double>(cur, n);
-  d.yU = carve<double>(cur, n);
-  d.scal = carve<unsigned long long>(cur, 32);
+  d.tacc = carve<double>(cur, h.Ltail_split.size() * B);
+  d.Lv = carve<double>(cur, d.nnz_L * B);
+  d.Uv = carve<double>(cur, d.nnz_U * B);
+  d.yL = carve<double>(cur, n * B);
+  d.yU = carve<double>(cur, n * B);
+  d.scal = carve<unsigned long long>(cur, SCAL_STRIDE * B);
   d.ticket = carve<int>(cur, 16);
-  d.partials = carve<double>(cur, 8 * RED_BLOCKS);
+  d.partials = carve<double>(cur, 8 * (size_t)d.rb * B);
   d.trace_ref = d.trace_trsv = d.trace_step = nullptr;
   if (std::getenv("KKT_TRACE") && std::atoi(std::getenv("KKT_TRACE")) > 0) {
     const size_t tb = 4 * 8 * n + 8 * (size_t)d.n_so;
@@ -225,9 +229,16 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
     UP(d.Uv, uv);
     CUDA_TRY(cudaStreamSynchronize(dev->stream));
   }
-  CUDA_TRY(launch_fill_sentinel(d.yL, (int64_t)n, dev->stream));
-  CUDA_TRY(launch_fill_sentinel(d.yU, (int64_t)n, dev->stream));
-  CUDA_TRY(cudaMemsetAsync(d.scal, 0, 8 * 32, dev->stream));
+  for (size_t q = 1; q < B; ++q) {  // every system starts from the first factorization
+    CUDA_TRY(cudaMemcpyAsync(d.Lx + q * d.nnz_L, d.Lx, 8 * d.nnz_L, cudaMemcpyDeviceToDevice, dev->stream));
+    CUDA_TRY(cudaMemcpyAsync(d.Ux + q * d.nnz_U, d.Ux, 8 * d.nnz_U, cudaMemcpyDeviceToDevice, dev->stream));
+    CUDA_TRY(cudaMemcpyAsync(d.Lv + q * d.nnz_L, d.Lv, 8 * d.nnz_L, cudaMemcpyDeviceToDevice, dev->stream));
+    CUDA_TRY(cudaMemcpyAsync(d.Uv + q * d.nnz_U, d.Uv, 8 * d.nnz_U, cudaMemcpyDeviceToDevice, dev->stream));
+    CUDA_TRY(cudaMemcpyAsync(d.udiag + q * n, d.udiag, 8 * n, cudaMemcpyDeviceToDevice, dev->stream));
+  }
+  CUDA_TRY(launch_fill_sentinel(d.yL, (int64_t)(n * B), dev->stream));
+  CUDA_TRY(launch_fill_sentinel(d.yU, (int64_t)(n * B), dev->stream));
+  CUDA_TRY(cudaMemsetAsync(d.scal, 0, 8 * SCAL_STRIDE * B, dev->stream));
   CUDA_TRY(cudaMemsetAsync(d.ticket, 0, 64, dev->stream));
   // launch shapes
   dev->refactor_warps = 8;
@@ -246,7 +257,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   int tb = 0;
   CUDA_TRY(trsv_configure(&tb));
   dev->trsv_blocks = std::max(1, tb) * dev->sm_count;
-  CUDA_TRY(cudaMallocHost(&dev->pinned, 4096));
+  dev->pinned_bytes = 64 * 1024;
+  CUDA_TRY(cudaMallocHost(&dev->pinned, dev->pinned_bytes));
   rc = alloc_krylov(dev, dev->restart_m);
   if (rc != KKT_OK) return rc;
   CUDA_TRY(cudaStreamSynchronize(dev->stream));
@@ -262,10 +274,11 @@ static int set_values(Device *dev, const double *vals, int layout, int on_device
     return set_error(KKT_ERR_BAD_ARG, "unknown value layout");
   d.sym_lower = layout == KKT_LAYOUT_SYMMETRIC_LOWER ? 1 : 0;
   const int64_t cnt = d.sym_lower ? d.in_nnz : d.nnz_a;
-  CUDA_TRY(cudaMemcpyAsync(d.in_vals, vals, 8 * (size_t)cnt,
-                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, dev->stream));
-  CUDA_TRY(cudaMemsetAsync(d.scal, 0, 8 * SC_MINPIV, dev->stream));
-  CUDA_TRY(cudaMemsetAsync(&d.scal[SC_OPNORM], 0, 8, dev->stream));
+  // values_in is [nb][cnt]; the device copy has a per-system pitch of in_cap
+  CUDA_TRY(cudaMemcpy2DAsync(d.in_vals, 8 * (size_t)d.in_cap, vals, 8 * (size_t)cnt, 8 * (size_t)cnt,
+                             (size_t)d.nb, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                             dev->stream));
+  LAUNCH(launch_reset_scal(d, 0, dev->stream));
   LAUNCH(launch_expand_norms(d, dev->stream));
   return KKT_OK;
 }
@@ -274,25 +287,28 @@ static int refactor(Device *dev, const double *vals, int layout, int on_device, 
   DevPlan &d = dev->d;
   int rc = set_values(dev, vals, layout, on_device);
   if (rc != KKT_OK) return rc;
-  const unsigned long long big = 0x7FF0000000000000ull;  // +inf bits for the min
-  CUDA_TRY(cudaMemcpyAsync(&d.scal[SC_MINPIV], &big, 8, cudaMemcpyHostToDevice, dev->stream));
+  LAUNCH(launch_reset_scal(d, 1, dev->stream));  // min |u_jj| starts at +inf
   {
     cudaError_t e = launch_refactor(d, dev->refactor_blocks, dev->refactor_warps, dev->refactor_smem,
                                     dev->stream, &dev->launches);
     if (e != cudaSuccess) return set_error(KKT_ERR_CUDA, std::string("refactor: ") + cudaGetErrorString(e));
   }
   LAUNCH(launch_diag_stats(d, dev->sm_count, dev->stream));
-  if (diag_out) {
-    CUDA_TRY(cudaMemcpyAsync(dev->pinned, d.scal, 8 * SC_COUNT, cudaMemcpyDeviceToHost, dev->stream));
+  if (diag_out) {  // [nb][4] = {max|u|, min|u|, patched, growth}
+    CUDA_TRY(cudaMemcpyAsync(dev->pinned, d.scal, 8 * SCAL_STRIDE * (size_t)d.nb, cudaMemcpyDeviceToHost,
+                             dev->stream));
     CUDA_TRY(cudaStreamSynchronize(dev->stream));
-    unsigned long long s[SC_COUNT];
-    std::memcpy(s, dev->pinned, sizeof s);
-    double v[SC_COUNT];
-    std::memcpy(v, s, sizeof v);
-    diag_out[0] = v[SC_MAXPIV];
-    diag_out[1] = d.n ? v[SC_MINPIV] : 0.0;
-    diag_out[2] = (double)s[SC_PATCHED];
-    diag_out[3] = v[SC_MAXABS_A] > 0 ? v[SC_GMAX] / v[SC_MAXABS_A] : 0.0;
+    for (int q = 0; q < d.nb; ++q) {
+      unsigned long long s[SC_COUNT];
+      std::memcpy(s, dev->pinned + (size_t)q * SCAL_STRIDE, sizeof s);
+      double v[SC_COUNT];
+      std::memcpy(v, s, sizeof v);
+      double *o = diag_out + 4 * q;
+      o[0] = v[SC_MAXPIV];
+      o[1] = d.n ? v[SC_MINPIV] : 0.0;
+      o[2] = (double)s[SC_PATCHED];
+      o[3] = v[SC_MAXABS_A] > 0 ? v[SC_GMAX] / v[SC_MAXABS_A] : 0.0;
+    }
   }
   return KKT_OK;
 }
@@ -308,15 +324,21 @@ int dev_spmv(Device *dev, const double *x, double *y, const double *bsub, double
   return KKT_OK;
 }
 
+// out6 [nb][6] = {||r-Kx||_2, ||r-Kx||_inf, ||x||_2, ||x||_inf, ||r||_2, ||K||_inf}
 int dev_residual_norms(Device *dev, const double *r, const double *x, double *out6) {
   DevPlan &d = dev->d;
-  LAUNCH(launch_resid_stats(d, r, x, d.partials, d.partials + 6 * RED_BLOCKS, dev->stream));
+  const size_t nb = (size_t)d.nb;
+  double *out5 = d.partials + 5 * (size_t)d.rb * nb;  // after the [nb][5][rb] partials
+  LAUNCH(launch_resid_stats(d, r, x, d.partials, out5, dev->stream));
   dev->launches++;
-  CUDA_TRY(cudaMemcpyAsync(dev->pinned, d.partials + 6 * RED_BLOCKS, 5 * 8, cudaMemcpyDeviceToHost,
+  CUDA_TRY(cudaMemcpyAsync(dev->pinned, out5, 8 * 5 * nb, cudaMemcpyDeviceToHost, dev->stream));
+  CUDA_TRY(cudaMemcpyAsync(dev->pinned + 5 * nb, d.scal, 8 * SCAL_STRIDE * nb, cudaMemcpyDeviceToHost,
                            dev->stream));
-  CUDA_TRY(cudaMemcpyAsync(dev->pinned + 5, &d.scal[SC_OPNORM], 8, cudaMemcpyDeviceToHost, dev->stream));
   CUDA_TRY(cudaStreamSynchronize(dev->stream));
-  std::memcpy(out6, dev->pinned, 6 * 8);
+  for (size_t q = 0; q < nb; ++q) {
+    std::memcpy(out6 + 6 * q, dev->pinned + 5 * q, 5 * 8);
+    std::memcpy(out6 + 6 * q + 5, dev->pinned + 5 * nb + q * SCAL_STRIDE + SC_OPNORM, 8);
+  }
   return KKT_OK;
 }
 
@@ -392,6 +414,7 @@ static int op_create(int64_t n, const int64_t *rp, const int64_t *ci, int sym, i
   d.n = (int)n;
   d.nnz_a = ng;
   d.in_nnz = nnz;
+  d.in_cap = std::max(nnz, ng);
   d.sym_lower = sym ? 1 : 0;
   d.has_lower = sym ? 1 : 0;
   size_t bytes = 0;
@@ -482,11 +505,14 @@ int kkt_dev_download_factors(kkt_device *d, double *Lx, double *Ux, double *Udia
   if (!dev) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
   cudaSetDevice(dev->device);
   const kkt::DevPlan &p = dev->d;
+  const size_t nb = (size_t)p.nb;
   cudaStream_t s = dev->stream;
   cudaError_t e = cudaSuccess;
-  if (Lx && p.nnz_L) e = cudaMemcpyAsync(Lx, p.Lx, 8 * (size_t)p.nnz_L, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && Ux && p.nnz_U) e = cudaMemcpyAsync(Ux, p.Ux, 8 * (size_t)p.nnz_U, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && Udiag && p.n) e = cudaMemcpyAsync(Udiag, p.udiag, 8 * (size_t)p.n, cudaMemcpyDeviceToHost, s);
+  if (Lx && p.nnz_L) e = cudaMemcpyAsync(Lx, p.Lx, 8 * (size_t)p.nnz_L * nb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && Ux && p.nnz_U)
+    e = cudaMemcpyAsync(Ux, p.Ux, 8 * (size_t)p.nnz_U * nb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && Udiag && p.n)
+    e = cudaMemcpyAsync(Udiag, p.udiag, 8 * (size_t)p.n * nb, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
   return KKT_OK;
@@ -519,9 +545,12 @@ int kkt_dev_fgmres(kkt_device *d, const double *b_dev, const double *x0_dev, dou
   if (!dev || !b_dev || !x0_dev || !x_dev || !cfg || !rep)
     return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
   cudaSetDevice(dev->device);
-  return kkt::dev_fgmres(dev, b_dev, x0_dev, x_dev, cfg, rep, history_host, hist_cap);
+  return kkt::dev_fgmres(dev, b_dev, x0_dev, x_dev, cfg, rep, history_host, hist_cap, nullptr);
 }
 
+// refine_fgmres for every system of the handle (refine.py:103-132): per-system trigger
+// ||r - K x0||_2 > delta ||r||_2; untriggered systems return x0; the triggered ones run
+// FGMRES(tol = delta) together.
 int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_dev, double *x_dev,
                           const kkt_krylov_cfg *cfg, kkt_krylov_report *rep) {
   Device *dev = reinterpret_cast<Device *>(d);
@@ -529,22 +558,33 @@ int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_d
     return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
   if (!(cfg->delta_tol > 0)) return kkt::set_error(KKT_ERR_BAD_ARG, "delta_tol must be positive");
   cudaSetDevice(dev->device);
-  double st[6];
-  int rc = kkt::dev_residual_norms(dev, r_dev, x0_dev, st);
+  const int nb = dev->d.nb;
+  std::vector<double> st(6 * (size_t)nb);
+  int rc = kkt::dev_residual_norms(dev, r_dev, x0_dev, st.data());
   if (rc) return rc;
-  std::memset(rep, 0, sizeof *rep);
-  // needs_refinement: ||r - K x0||_2 > delta * ||r||_2   (refine.py:88-92)
-  if (!(st[0] > cfg->delta_tol * st[4])) {
-    cudaError_t e = cudaMemcpyAsync(x_dev, x0_dev, 8 * (size_t)dev->d.n, cudaMemcpyDeviceToDevice, dev->stream);
+  std::vector<int> trig(nb, 0);
+  int any = 0;
+  for (int q = 0; q < nb; ++q) {
+    trig[q] = st[6 * q] > cfg->delta_tol * st[6 * q + 4] ? 1 : 0;
+    any |= trig[q];
+  }
+  if (!any) {
+    for (int q = 0; q < nb; ++q) {
+      std::memset(&rep[q], 0, sizeof rep[q]);
+      rep[q].converged = 1;
+    }
+    cudaError_t e = cudaMemcpyAsync(x_dev, x0_dev, 8 * (size_t)dev->d.n * nb, cudaMemcpyDeviceToDevice,
+                                    dev->stream);
     if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
-    rep->triggered = 0;
-    rep->converged = 1;
     return KKT_OK;
   }
   kkt_krylov_cfg c = *cfg;
   c.tol = cfg->delta_tol;
-  rc = kkt::dev_fgmres(dev, r_dev, x0_dev, x_dev, &c, rep, nullptr, 0);
-  rep->triggered = 1;
+  rc = kkt::dev_fgmres(dev, r_dev, x0_dev, x_dev, &c, rep, nullptr, 0, trig.data());
+  for (int q = 0; q < nb; ++q) {
+    rep[q].triggered = trig[q];
+    if (!trig[q]) rep[q].converged = 1;
+  }
   return rc;
 }
 
@@ -558,10 +598,10 @@ int kkt_dev_step(kkt_device *d, const double *values_in, int layout, const doubl
   int rc = kkt::refactor(dev, values_in, layout, io_on_device, diag_out);
   if (rc) return rc;
   kkt::Krylov &K = *dev->kry;
-  const size_t nb = 8 * (size_t)dev->d.n;
+  const size_t bytes = 8 * (size_t)dev->d.n * dev->d.nb;
   const double *r_dev = r_in;
   if (!io_on_device) {
-    cudaError_t e = cudaMemcpyAsync(K.sr, r_in, nb, cudaMemcpyHostToDevice, dev->stream);
+    cudaError_t e = cudaMemcpyAsync(K.sr, r_in, bytes, cudaMemcpyHostToDevice, dev->stream);
     if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
     r_dev = K.sr;
   }
@@ -569,7 +609,7 @@ int kkt_dev_step(kkt_device *d, const double *values_in, int layout, const doubl
   if (rc) return rc;
   rc = kkt_dev_refine_fgmres(d, r_dev, K.sx0, K.sx, cfg, rep);  // (harness.py:240)
   if (rc) return rc;
-  cudaError_t e = cudaMemcpyAsync(x_out, K.sx, nb,
+  cudaError_t e = cudaMemcpyAsync(x_out, K.sx, bytes,
                                   io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                   dev->stream);
   if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
@@ -615,6 +655,7 @@ static kkt::Device op_view(kkt::Operator *op) {
   v.stream = op->stream;
   v.d = op->d;
   v.pinned = op->pinned;
+  v.pinned_bytes = 4096;
   return v;
 }
 

@@ -1,5 +1,10 @@
-// Device handle + the launch interface between the host orchestration (device.cu) and the
-// kernel translation units (refactor.cu, trisolve.cu, vector.cu).
+// Device handle + the launch interface between the host orchestration (device.cu, krylov.cu)
+// and the kernel translation units (refactor.cu, trisolve.cu, vector.cu).
+//
+// A handle holds nb >= 1 same-pattern systems.  Every per-system array is system-major:
+// system b's copy starts at b * (per-system size).  Kernels decompose their work into
+// (task, system) pairs dispatched in dependency (level) order, so the dependency chains of
+// all systems advance together in one launch (the batched path).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -7,48 +12,50 @@
 
 namespace kkt {
 
-constexpr int RED_BLOCKS = 296;  // fixed => reductions are run-to-run deterministic
+constexpr int RED_BLOCKS = 296;  // reduction blocks for one system (fixed => deterministic)
 constexpr int RED_THREADS = 256;
 constexpr double HAPPY_BREAKDOWN_RTOL = 1e-14;   // krylov.py:25
 constexpr double PATCH_RELATIVE_FLOOR = 1e-12;   // direct_lu.py:32
 constexpr int REFACTOR_STAGE = 512;              // update pairs staged per warp chunk
-constexpr int CTA_PHASE_THREADS = 1024;
+constexpr int SCAL_STRIDE = 16;                  // per-system scalar block
 
 // Device-side view of the plan + workspaces.  int32 indices on the device.
 struct DevPlan {
   int n = 0, sym_lower = 0, has_lower = 0;
-  int64_t nnz_a = 0, in_nnz = 0, nnz_L = 0, nnz_U = 0, n_so = 0, n_upd = 0, n_ap = 0;
+  int nb = 1;   // systems held
+  int rb = RED_BLOCKS;  // reduction blocks per system
+  int64_t nnz_a = 0, in_nnz = 0, in_cap = 0, nnz_L = 0, nnz_U = 0, n_so = 0, n_upd = 0, n_ap = 0;
   int maxpat = 1;
   int ref_start = 0;       // first col_order index handled by the warp kernel
   int n_small_levels = 0;  // leading levels run by k_refactor_small
   int lev_ptr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // col_order offsets of those levels
   int poll_ns = 0;  // __nanosleep back-off while polling (env KKT_POLL_NS)
-  // operator
+  // operator (pattern shared; values per system)
   int *A_rp, *A_ci, *A_split, *gen_src;
-  double *in_vals, *A_vals;
-  // refactor
+  double *in_vals, *A_vals;                 // [nb][in_cap], [nb][nnz_a]
+  // refactor (schedule shared)
   int *so_ptr, *ap_ptr, *a_src, *col_order, *Lp, *Up, *Lmap, *Umap, *upd_lidx;
   int4 *so_meta;
   uint16_t *upd_slot, *a_slot;
-  double *Lx, *Ux, *udiag;
-  // trisolves
+  double *Lx, *Ux, *udiag;                  // [nb][nnz_L], [nb][nnz_U], [nb][n]
+  // trisolves (pattern/schedule shared)
   int *Lrp, *Lci, *Urp, *Uci, *row_perm, *col_perm;
   int *L_grid_order, *L_tail_order, *U_head_order, *U_grid_order;
   int *L_crit, *U_crit, *Uhead_off, *Li, *Ui, *Ltail_split;
-  double *tacc;  // partial sums of the L tail rows over columns < pL (grid phase -> sweep)
-  int pL, pU, nLg, nUg;  // split positions and grid-phase row counts
+  double *tacc;                             // [nb][n - pL] tail partial sums (grid -> sweep)
+  int pL, pU, nLg, nUg;                     // split positions and grid-phase row counts
   int sweep_maxL, sweep_maxU;
-  double *Lv, *Uv;
-  double *yL, *yU;       // sentinel-reset solution buffers (value == readiness flag)
-  // optional timeline (KKT_TRACE=1): refactor {grab, end} ns per column, trisolve end per row
+  double *Lv, *Uv;                          // [nb][nnz_L], [nb][nnz_U] (CSR order)
+  double *yL, *yU;                          // [nb][n] sentinel-reset (value == readiness)
+  // optional timeline (KKT_TRACE=1), system 0 only
   unsigned long long *trace_ref, *trace_trsv, *trace_step;
   // scalars
-  unsigned long long *scal;
+  unsigned long long *scal;                 // [nb][SCAL_STRIDE]
   int *ticket;
-  double *partials;
+  double *partials;                         // [nb][8][rb]
 };
 
-// indices into DevPlan::scal (bit patterns of non-negative doubles unless noted)
+// indices into a system's scalar block (bit patterns of non-negative doubles unless noted)
 enum {
   SC_MAXABS_A = 0,  // max |a|
   SC_INFNORM,       // ||A||_inf of the general matrix (row sums in entry order)
@@ -61,7 +68,7 @@ enum {
   SC_COUNT
 };
 
-struct Krylov;  // FGMRES workspace (device.cu)
+struct Krylov;  // FGMRES workspace (krylov.cu)
 
 struct Device {
   int device = 0;
@@ -77,12 +84,14 @@ struct Device {
   int trsv_blocks = 0;
   long long launches = 0;
   Krylov *kry = nullptr;
-  double *pinned = nullptr;  // small pinned host staging buffer
+  double *pinned = nullptr;  // pinned host staging (status words)
+  size_t pinned_bytes = 0;
   int restart_m = 10;
 };
 
 // ---- launchers (each returns cudaGetLastError of its launch) ----
 cudaError_t launch_expand_norms(const DevPlan &d, cudaStream_t s);
+cudaError_t launch_reset_scal(const DevPlan &d, int mode, cudaStream_t s);
 cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem, cudaStream_t s,
                             long long *launches);
 cudaError_t launch_diag_stats(const DevPlan &d, int blocks, cudaStream_t s);
@@ -94,10 +103,11 @@ cudaError_t launch_trsv(const DevPlan &d, const double *b, double *x, int grid_b
 cudaError_t trsv_configure(int *grid_blocks_per_sm);
 cudaError_t launch_fill_sentinel(double *p, int64_t n, cudaStream_t s);
 
+// vectors are [nb][n]; partials are [nb][nvec][rb]; out is [nb][nvec]
 cudaError_t launch_spmv(const DevPlan &d, const double *x, double *out, const double *bsub,
                         double *nrm_partials, cudaStream_t s);
-cudaError_t launch_reduce_partials(const double *partials, int nvec, int nblk, double *out,
-                                   int op_sqrt, cudaStream_t s);
+cudaError_t launch_reduce_partials(const DevPlan &d, const double *partials, int nvec, double *out,
+                                   int ostride, int op_sqrt, cudaStream_t s);
 cudaError_t launch_resid_stats(const DevPlan &d, const double *r, const double *x,
                                double *partials, double *out5, cudaStream_t s);
 

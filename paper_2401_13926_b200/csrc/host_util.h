@@ -40,27 +40,32 @@ struct KState {
   int j, stop, converged, pad;
 };
 
-// FGMRES(m) workspace, allocated once per handle (krylov.cu).
+// FGMRES(m) workspace for nb systems, allocated once per handle (krylov.cu).
 struct Krylov {
   int m = 0, n = 0;
-  double *V = nullptr;  // (m+1) x n basis
-  double *Z = nullptr;  // m x n preconditioned basis (flexible)
-  double *w = nullptr, *w1 = nullptr, *r = nullptr, *x = nullptr;
-  double *sr = nullptr, *sx0 = nullptr, *sx = nullptr;  // kkt_dev_step staging
+  double *V = nullptr;  // [m+1][nb][n] basis
+  double *Z = nullptr;  // [m][nb][n] preconditioned basis (flexible)
+  double *w = nullptr, *w1 = nullptr, *r = nullptr, *x = nullptr;  // [nb][n]
+  double *sr = nullptr, *sx0 = nullptr, *sx = nullptr;             // kkt_dev_step staging
   double *h1 = nullptr, *h2 = nullptr, *H = nullptr, *cs = nullptr, *sn = nullptr, *g = nullptr,
-         *yv = nullptr, *nrm = nullptr, *beta = nullptr;
+         *yv = nullptr, *nrm = nullptr, *beta = nullptr;            // per-system small state
   KState *st = nullptr;
-  double *partials = nullptr;  // (m+2) * RED_BLOCKS
+  double *partials = nullptr;  // [nb][m+2][rb]
+  double *status = nullptr;    // [nb][4] {est|beta, stop, hj1, nonfinite}
+  int *mask = nullptr, *jused = nullptr;
   void *mem = nullptr;
 };
 
-// host-side building blocks (device.cu / krylov.cu)
+// host-side building blocks (device.cu / krylov.cu); vectors are [nb][n]
 int dev_solve(Device *dev, const double *b, double *x);
 int dev_spmv(Device *dev, const double *x, double *y, const double *bsub, double *nrm_partials);
 int dev_residual_norms(Device *dev, const double *r, const double *x, double *out6);
 int alloc_krylov(Device *dev, int m);
 void free_krylov(Device *dev);
+// rep / hist are per system (rep[nb], hist[nb][hist_cap]); active (may be NULL) selects the
+// systems to run, the others keep x = x0 untouched semantics to the caller.
 int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
-               const kkt_krylov_cfg *cfg, kkt_krylov_report *rep, double *hist, int hist_cap);
+               const kkt_krylov_cfg *cfg, kkt_krylov_report *rep, double *hist, int hist_cap,
+               const int *active);
 
 }  // namespace kkt

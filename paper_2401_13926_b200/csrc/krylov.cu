@@ -1,127 +1,182 @@
 // Restarted right-preconditioned FGMRES(m) with CGS2 (krylov.fgmres / cgs2_step,
-// krylov.py:93-208) on the device.  Per iteration: z = M v (triangular solves),
-// w = K z (SpMV), CGS2 as two (multi-dot, fused multi-axpy) passes — the second pass also
-// produces ||w||^2 — then the Hessenberg/Givens update in a one-thread kernel that publishes
-// the residual estimate and the stop flag.  The host reads one 32-byte status per iteration
-// (the reference's per-iteration convergence test); no vector ever leaves HBM.
+// krylov.py:93-208) on the device, for nb same-pattern systems at once.
+//
+// Per iteration: z = M v (triangular solves, all systems in one launch), w = K z (SpMV),
+// CGS2 as two (multi-dot, fused multi-axpy) passes — the second also produces ||w||^2 —
+// then the Hessenberg/Givens update in a one-warp-per-system kernel that publishes the
+// residual estimate and the stop flag.  Systems advance in lockstep cycles; each keeps the
+// reference's own semantics (stop inside a cycle on est <= tol*beta0 or happy breakdown,
+// solution + true residual at the cycle end, restart budget) through a per-system mask.
+// The host reads one small status block per iteration; no vector ever leaves HBM.
+// Layouts: V [m+1][nb][n], Z [m][nb][n] (the j-th basis of all systems is contiguous, which
+// is the [nb][n] layout the solve and SpMV consume); per-system small state [nb][...].
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <vector>
 
 #include "host_util.h"
 #include "kernels.cuh"
 
 namespace kkt {
 
-// h[q] = V_q . w for q < nvec as block partials (vectors in groups of 8, w re-read from L2).
-__global__ void __launch_bounds__(RED_THREADS) k_dots(const double *__restrict__ V, int nvec, int n,
-                                                      const double *__restrict__ w,
+// h[q] = V_q . w (q < nvec) as block partials [nb][nvec][rb]; skipped for masked systems.
+__global__ void __launch_bounds__(RED_THREADS) k_dots(const double *__restrict__ V, int nb, int nvec,
+                                                      int n, const double *__restrict__ w,
+                                                      const int *__restrict__ mask,
                                                       double *__restrict__ partials) {
   __shared__ double sh[32];
+  const int sys = blockIdx.y;
+  if (!mask[sys]) return;
+  const double *ws = w + (size_t)sys * n;
   for (int g0 = 0; g0 < nvec; g0 += 8) {
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const int gn = min(8, nvec - g0);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-      const double wi = w[i];
+      const double wi = ws[i];
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        if (q < gn) acc[q] += V[(size_t)(g0 + q) * n + i] * wi;
+        if (q < gn) acc[q] += V[((size_t)(g0 + q) * nb + sys) * n + i] * wi;
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       if (q < gn) {
         const double t = block_sum<RED_THREADS>(acc[q], sh);
-        if (threadIdx.x == 0) partials[(size_t)(g0 + q) * RED_BLOCKS + blockIdx.x] = t;
+        if (threadIdx.x == 0) partials[((size_t)sys * nvec + g0 + q) * gridDim.x + blockIdx.x] = t;
       }
     }
   }
 }
 
-// w_out = w_in - sum_q V_q h[q]; mode 1 also emits ||w_out||^2 block partials.
-__global__ void __launch_bounds__(RED_THREADS) k_cgs(const double *__restrict__ V, int nvec, int n,
-                                                     const double *__restrict__ w_in,
-                                                     const double *__restrict__ h,
+// w_out = w_in - sum_q V_q h[q]; mode 1 also emits ||w_out||^2 block partials [nb][rb].
+__global__ void __launch_bounds__(RED_THREADS) k_cgs(const double *__restrict__ V, int nb, int nvec,
+                                                     int n, const double *__restrict__ w_in,
+                                                     const double *__restrict__ h, int hstride,
                                                      double *__restrict__ w_out, int mode,
+                                                     const int *__restrict__ mask,
                                                      double *__restrict__ partials) {
   __shared__ double sh[32];
   __shared__ double hs[64];
-  for (int q = threadIdx.x; q < nvec; q += blockDim.x) hs[q] = h[q];
+  const int sys = blockIdx.y;
+  if (!mask[sys]) return;
+  for (int q = threadIdx.x; q < nvec; q += blockDim.x) hs[q] = h[(size_t)sys * hstride + q];
   __syncthreads();
+  const double *wi_ = w_in + (size_t)sys * n;
+  double *wo_ = w_out + (size_t)sys * n;
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double t = 0.0;
-    for (int q = 0; q < nvec; ++q) t += V[(size_t)q * n + i] * hs[q];
-    const double o = w_in[i] - t;
-    w_out[i] = o;
+    for (int q = 0; q < nvec; ++q) t += V[((size_t)q * nb + sys) * n + i] * hs[q];
+    const double o = wi_[i] - t;
+    wo_[i] = o;
     acc += o * o;
   }
   if (mode == 1) {
     const double t = block_sum<RED_THREADS>(acc, sh);
-    if (threadIdx.x == 0) partials[blockIdx.x] = t;
+    if (threadIdx.x == 0) partials[(size_t)sys * gridDim.x + blockIdx.x] = t;
   }
 }
 
-// Hessenberg column j, previous rotations, new rotation, residual estimate (:166-186).
+// Per system: Hessenberg column j, previous rotations, new rotation, estimate (:166-186).
+// status[sys] = {est, stop, hj1, nonfinite}.
 __global__ void k_givens(KState *st, int j, int m, const double *__restrict__ h1,
                          const double *__restrict__ h2, const double *__restrict__ nrm2,
-                         double *H, double *cs, double *sn, double *g, double *status) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int i = 0; i <= j; ++i) H[i * m + j] = h1[i] + h2[i];  // H is (m+1) x m row-major
-  const double hj1 = sqrt(nrm2[0]);
-  H[(j + 1) * m + j] = hj1;
-  for (int i = 0; i < j; ++i) {
-    const double a = H[i * m + j], b = H[(i + 1) * m + j];
-    const double t = __dadd_rn(__dmul_rn(cs[i], a), __dmul_rn(sn[i], b));
-    H[(i + 1) * m + j] = __dadd_rn(__dmul_rn(-sn[i], a), __dmul_rn(cs[i], b));
-    H[i * m + j] = t;
-  }
-  const double denom = hypot(H[j * m + j], H[(j + 1) * m + j]);
-  cs[j] = __ddiv_rn(H[j * m + j], denom);
-  sn[j] = __ddiv_rn(H[(j + 1) * m + j], denom);
-  H[j * m + j] = denom;
-  H[(j + 1) * m + j] = 0.0;
-  g[j + 1] = __dmul_rn(-sn[j], g[j]);
-  g[j] = __dmul_rn(cs[j], g[j]);
-  const double est = fabs(g[j + 1]);
-  st->est = est;
-  st->hj1 = hj1;
-  st->j = j;
-  const int stop = (est <= st->target || hj1 <= st->floor) ? 1 : 0;
-  st->stop = stop;
-  status[0] = est;
-  status[1] = stop;
-  status[2] = hj1;
-}
-
-__global__ void k_scale(const double *__restrict__ in, double *__restrict__ out, int n,
-                        const double *__restrict__ den) {
-  const double dv = den[0];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    out[i] = __ddiv_rn(in[i], dv);
-}
-
-__global__ void k_cycle_init(double *g, int m, const double *beta, double *H) {
-  for (int i = threadIdx.x; i <= m; i += blockDim.x) g[i] = (i == 0) ? beta[0] : 0.0;
-  for (int i = threadIdx.x; i < (m + 1) * m; i += blockDim.x) H[i] = 0.0;
-}
-
-// y = R^{-1} g on the leading k x k block (krylov.py:211-216).
-__global__ void k_solve_upper(const double *H, int m, const double *g, int k, double *y) {
+                         double *H, double *cs, double *sn, double *g, double *status,
+                         const int *__restrict__ mask, const unsigned long long *scal) {
+  const int sys = blockIdx.x;
   if (threadIdx.x != 0) return;
+  double *stat = status + 4 * sys;
+  stat[3] = scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE] ? 1.0 : 0.0;
+  if (!mask[sys]) return;
+  const int m1 = m + 1;
+  double *Hs = H + (size_t)sys * m1 * m;
+  double *css = cs + (size_t)sys * m1, *sns = sn + (size_t)sys * m1, *gs = g + (size_t)sys * m1;
+  KState *S = st + sys;
+  for (int i = 0; i <= j; ++i) Hs[i * m + j] = h1[(size_t)sys * m1 + i] + h2[(size_t)sys * m1 + i];
+  const double hj1 = sqrt(nrm2[sys]);
+  Hs[(j + 1) * m + j] = hj1;
+  for (int i = 0; i < j; ++i) {
+    const double a = Hs[i * m + j], b = Hs[(i + 1) * m + j];
+    const double t = __dadd_rn(__dmul_rn(css[i], a), __dmul_rn(sns[i], b));
+    Hs[(i + 1) * m + j] = __dadd_rn(__dmul_rn(-sns[i], a), __dmul_rn(css[i], b));
+    Hs[i * m + j] = t;
+  }
+  const double denom = hypot(Hs[j * m + j], Hs[(j + 1) * m + j]);
+  css[j] = __ddiv_rn(Hs[j * m + j], denom);
+  sns[j] = __ddiv_rn(Hs[(j + 1) * m + j], denom);
+  Hs[j * m + j] = denom;
+  Hs[(j + 1) * m + j] = 0.0;
+  gs[j + 1] = __dmul_rn(-sns[j], gs[j]);
+  gs[j] = __dmul_rn(css[j], gs[j]);
+  const double est = fabs(gs[j + 1]);
+  S->est = est;
+  S->hj1 = hj1;
+  S->j = j;
+  const int stop = (est <= S->target || hj1 <= S->floor) ? 1 : 0;
+  S->stop = stop;
+  stat[0] = est;
+  stat[1] = stop;
+  stat[2] = hj1;
+}
+
+// status[sys] = {beta[sys] (if given), -, -, nonfinite flag}
+__global__ void k_status(double *status, const unsigned long long *scal, const double *beta, int nb) {
+  for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+    if (beta) status[4 * q] = beta[q];
+    status[4 * q + 3] = scal[(size_t)q * SCAL_STRIDE + SC_NONFINITE] ? 1.0 : 0.0;
+  }
+}
+
+// out_sys = in_sys / den[sys * dstride] for systems in the mask
+__global__ void k_scale(const double *__restrict__ in, double *__restrict__ out, int n,
+                        const double *__restrict__ den, int dstride, const int *__restrict__ mask) {
+  const int sys = blockIdx.y;
+  if (!mask[sys]) return;
+  const double dv = den[(size_t)sys * dstride];
+  const double *is = in + (size_t)sys * n;
+  double *os = out + (size_t)sys * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    os[i] = __ddiv_rn(is[i], dv);
+}
+
+__global__ void k_cycle_init(double *g, double *H, int m, const double *beta, const int *mask,
+                             unsigned long long *scal) {
+  const int sys = blockIdx.x;
+  if (!mask[sys]) return;
+  double *gs = g + (size_t)sys * (m + 1);
+  double *Hs = H + (size_t)sys * (m + 1) * m;
+  for (int i = threadIdx.x; i <= m; i += blockDim.x) gs[i] = (i == 0) ? beta[sys] : 0.0;
+  for (int i = threadIdx.x; i < (m + 1) * m; i += blockDim.x) Hs[i] = 0.0;
+  if (threadIdx.x == 0) scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE] = 0ull;
+}
+
+// y = R^{-1} g on the leading k x k block, k = jused[sys] (krylov.py:211-216).
+__global__ void k_solve_upper(const double *H, int m, const double *g, const int *jused, double *y) {
+  const int sys = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  const int k = jused[sys];
+  const double *Hs = H + (size_t)sys * (m + 1) * m;
+  const double *gs = g + (size_t)sys * (m + 1);
+  double *ys = y + (size_t)sys * (m + 1);
   for (int i = k - 1; i >= 0; --i) {
     double dot = 0.0;
-    for (int q = i + 1; q < k; ++q) dot = __dadd_rn(dot, __dmul_rn(H[i * m + q], y[q]));
-    y[i] = __ddiv_rn(__dsub_rn(g[i], dot), H[i * m + i]);
+    for (int q = i + 1; q < k; ++q) dot = __dadd_rn(dot, __dmul_rn(Hs[i * m + q], ys[q]));
+    ys[i] = __ddiv_rn(__dsub_rn(gs[i], dot), Hs[i * m + i]);
   }
 }
 
-// x = x + (sum_q Z_q y_q)   (krylov.py:190: the matvec first, then the add)
-__global__ void k_update_x(double *__restrict__ x, const double *__restrict__ Z, int n,
-                           const double *__restrict__ y, int k) {
+// x = x + (sum_q Z_q y_q) for k = jused[sys] (krylov.py:190: the matvec first, then the add)
+__global__ void k_update_x(double *__restrict__ x, const double *__restrict__ Z, int nb, int n,
+                           const double *__restrict__ y, int ystride, const int *__restrict__ jused) {
+  const int sys = blockIdx.y;
+  const int k = jused[sys];
+  if (!k) return;
+  double *xs = x + (size_t)sys * n;
+  const double *ys = y + (size_t)sys * ystride;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double t = 0.0;
-    for (int q = 0; q < k; ++q) t = __dadd_rn(t, __dmul_rn(Z[(size_t)q * n + i], y[q]));
-    x[i] = __dadd_rn(x[i], t);
+    for (int q = 0; q < k; ++q) t = __dadd_rn(t, __dmul_rn(Z[((size_t)q * nb + sys) * n + i], ys[q]));
+    xs[i] = __dadd_rn(xs[i], t);
   }
 }
 
@@ -137,56 +192,64 @@ int alloc_krylov(Device *dev, int m) {
   Krylov *K = new Krylov();
   K->m = m;
   K->n = dev->d.n;
-  const size_t n = (size_t)dev->d.n;
-  size_t bytes = align_up(8 * (m + 1) * n + 1) + align_up(8 * m * n + 1) + 7 * align_up(8 * n + 1);
-  bytes += 6 * align_up(8 * (m + 1) + 1) + align_up(8 * (m + 1) * m + 1) + 2 * align_up(64 + 1);
-  bytes += align_up(sizeof(KState) + 1) + align_up(8 * (m + 2) * RED_BLOCKS + 1);
+  const size_t n = (size_t)dev->d.n, nb = (size_t)dev->d.nb, rb = (size_t)dev->d.rb;
+  size_t bytes = align_up(8 * (m + 1) * nb * n + 1) + align_up(8 * m * nb * n + 1) +
+                 7 * align_up(8 * nb * n + 1);
+  bytes += 6 * align_up(8 * nb * (m + 1) + 1) + align_up(8 * nb * (m + 1) * m + 1);
+  bytes += 2 * align_up(8 * nb + 64) + align_up(sizeof(KState) * nb + 1);
+  bytes += align_up(8 * (m + 2) * rb * nb + 1) + align_up(8 * 4 * nb + 1) + 2 * align_up(4 * nb + 1);
   if (cudaMalloc(&K->mem, bytes) != cudaSuccess) {
     delete K;
     return set_error(KKT_ERR_OOM, "cudaMalloc of the FGMRES workspace failed");
   }
+  cudaMemsetAsync(K->mem, 0, bytes, dev->stream);
   char *cur = (char *)K->mem;
-  K->V = carve<double>(cur, (m + 1) * n);
-  K->Z = carve<double>(cur, (size_t)m * n);
-  K->w = carve<double>(cur, n);
-  K->w1 = carve<double>(cur, n);
-  K->r = carve<double>(cur, n);
-  K->x = carve<double>(cur, n);
-  K->sr = carve<double>(cur, n);
-  K->sx0 = carve<double>(cur, n);
-  K->sx = carve<double>(cur, n);
-  K->h1 = carve<double>(cur, m + 1);
-  K->h2 = carve<double>(cur, m + 1);
-  K->cs = carve<double>(cur, m + 1);
-  K->sn = carve<double>(cur, m + 1);
-  K->g = carve<double>(cur, m + 1);
-  K->yv = carve<double>(cur, m + 1);
-  K->H = carve<double>(cur, (size_t)(m + 1) * m);
-  K->nrm = carve<double>(cur, 8);
-  K->beta = carve<double>(cur, 8);
-  K->st = carve<KState>(cur, 1);
-  K->partials = carve<double>(cur, (size_t)(m + 2) * RED_BLOCKS);
+  K->V = carve<double>(cur, (m + 1) * nb * n);
+  K->Z = carve<double>(cur, (size_t)m * nb * n);
+  K->w = carve<double>(cur, nb * n);
+  K->w1 = carve<double>(cur, nb * n);
+  K->r = carve<double>(cur, nb * n);
+  K->x = carve<double>(cur, nb * n);
+  K->sr = carve<double>(cur, nb * n);
+  K->sx0 = carve<double>(cur, nb * n);
+  K->sx = carve<double>(cur, nb * n);
+  K->h1 = carve<double>(cur, nb * (m + 1));
+  K->h2 = carve<double>(cur, nb * (m + 1));
+  K->cs = carve<double>(cur, nb * (m + 1));
+  K->sn = carve<double>(cur, nb * (m + 1));
+  K->g = carve<double>(cur, nb * (m + 1));
+  K->yv = carve<double>(cur, nb * (m + 1));
+  K->H = carve<double>(cur, nb * (m + 1) * m);
+  K->nrm = carve<double>(cur, nb + 8);
+  K->beta = carve<double>(cur, nb + 8);
+  K->st = carve<KState>(cur, nb);
+  K->partials = carve<double>(cur, (m + 2) * rb * nb);
+  K->status = carve<double>(cur, 4 * nb);
+  K->mask = carve<int>(cur, nb);
+  K->jused = carve<int>(cur, nb);
   free_krylov(dev);
   dev->kry = K;
   return KKT_OK;
 }
 
-// Read `count` doubles (device) + the non-finite flag into pinned memory; one sync.
-static int read_status(Device *dev, const double *src, int count, bool *nonfinite) {
-  if (count) CUDA_TRY(cudaMemcpyAsync(dev->pinned, src, 8 * count, cudaMemcpyDeviceToHost, dev->stream));
-  CUDA_TRY(cudaMemcpyAsync(dev->pinned + 8, &dev->d.scal[SC_NONFINITE], 8, cudaMemcpyDeviceToHost,
-                           dev->stream));
+// Copy `count` doubles from the device into pinned memory; one stream sync.
+static int read_block(Device *dev, const double *src, size_t count) {
+  if (8 * count > dev->pinned_bytes) return set_error(KKT_ERR_BAD_ARG, "status block too large");
+  CUDA_TRY(cudaMemcpyAsync(dev->pinned, src, 8 * count, cudaMemcpyDeviceToHost, dev->stream));
   CUDA_TRY(cudaStreamSynchronize(dev->stream));
-  unsigned long long f;
-  std::memcpy(&f, dev->pinned + 8, 8);
-  *nonfinite = f != 0;
+  return KKT_OK;
+}
+
+static int upload_mask(Device *dev, const std::vector<int> &mask, int *dst) {
+  CUDA_TRY(cudaMemcpyAsync(dst, mask.data(), 4 * mask.size(), cudaMemcpyHostToDevice, dev->stream));
   return KKT_OK;
 }
 
 int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
-               const kkt_krylov_cfg *cfg, kkt_krylov_report *rep, double *hist, int hist_cap) {
+               const kkt_krylov_cfg *cfg, kkt_krylov_report *rep, double *hist, int hist_cap,
+               const int *active_in) {
   DevPlan &d = dev->d;
-  const int n = d.n;
+  const int n = d.n, nb = d.nb;
   if (cfg->m < 1) return set_error(KKT_ERR_BAD_ARG, "restart length m must be >= 1");
   if (!(cfg->tol > 0)) return set_error(KKT_ERR_BAD_ARG, "tol must be positive");
   if (cfg->m > 62) return set_error(KKT_ERR_BAD_ARG, "restart length m must be <= 62");
@@ -195,116 +258,150 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
     if (rc != KKT_OK) return rc;
   }
   Krylov &K = *dev->kry;
-  const int m = cfg->m;
+  const int m = cfg->m, M = K.m;  // M: workspace stride (>= m)
   cudaStream_t s = dev->stream;
-  std::memset(rep, 0, sizeof *rep);
-  int hn = 0;
-  auto push_hist = [&](double v) {
-    if (hist && hn < hist_cap) hist[hn] = v;
-    hn++;
+  const size_t nbn = (size_t)nb * n;
+  std::vector<int> hn(nb, 0), active(nb, 1), running(nb, 0), jused(nb, 0);
+  std::vector<double> beta(nb, 0.0), target(nb, 0.0), est(nb, 0.0);
+  std::vector<int> iters(nb, 0), converged(nb, 0), restarts(nb, 0);
+  for (int q = 0; q < nb; ++q) {
+    std::memset(&rep[q], 0, sizeof rep[q]);
+    if (active_in) active[q] = active_in[q] ? 1 : 0;
+  }
+  auto push_hist = [&](int q, double v) {
+    if (hist && hn[q] < hist_cap) hist[(size_t)q * hist_cap + hn[q]] = v;
+    hn[q]++;
   };
-  bool nonfinite = false;
-  CUDA_TRY(cudaMemsetAsync(&d.scal[SC_NONFINITE], 0, 8, s));
-  CUDA_TRY(cudaMemcpyAsync(K.x, x0, 8 * (size_t)n, cudaMemcpyDeviceToDevice, s));
-  // r = b - K x; beta0 = ||r||                                           (:133-134)
+  auto fail_nonfinite = [&](int q) {
+    rep[q].nonfinite = 1;
+    return set_error(KKT_ERR_NONFINITE, "operator or preconditioner produced a non-finite entry");
+  };
+  for (int q = 0; q < nb; ++q) CUDA_TRY(cudaMemsetAsync(&d.scal[(size_t)q * SCAL_STRIDE + SC_NONFINITE], 0, 8, s));
+  CUDA_TRY(cudaMemcpyAsync(K.x, x0, 8 * nbn, cudaMemcpyDeviceToDevice, s));
+  // r = b - K x; beta0 = ||r||                                             (:133-134)
   int rc = dev_spmv(dev, K.x, K.r, b, K.partials);
   if (rc) return rc;
-  LAUNCH(launch_reduce_partials(K.partials, 1, RED_BLOCKS, K.beta, 1, s));
-  if ((rc = read_status(dev, K.beta, 1, &nonfinite))) return rc;
-  if (nonfinite) {
-    rep->nonfinite = 1;
-    return set_error(KKT_ERR_NONFINITE, "operator produced a non-finite entry");
+  LAUNCH(launch_reduce_partials(d, K.partials, 1, K.beta, 1, 1, s));
+  LAUNCH((k_status<<<1, 64, 0, s>>>(K.status, d.scal, K.beta, nb), cudaGetLastError()));
+  if ((rc = read_block(dev, K.status, 4 * nb))) return rc;
+  for (int q = 0; q < nb; ++q) {
+    beta[q] = dev->pinned[4 * q];
+    if (active[q] && dev->pinned[4 * q + 3] != 0.0) return fail_nonfinite(q);
   }
-  const double beta0 = dev->pinned[0];
-  push_hist(beta0);
-  rep->beta0 = beta0;
-  if (beta0 == 0.0) {  // (:140-141)
-    CUDA_TRY(cudaMemcpyAsync(xout, K.x, 8 * (size_t)n, cudaMemcpyDeviceToDevice, s));
-    rep->converged = 1;
-    rep->est_final = beta0;
-    return KKT_OK;
-  }
-  KState st{};
-  st.beta0 = beta0;
-  st.target = cfg->tol * beta0;
-  st.floor = HAPPY_BREAKDOWN_RTOL * beta0;
-  CUDA_TRY(cudaMemcpyAsync(K.st, &st, sizeof st, cudaMemcpyHostToDevice, s));
-  double beta = beta0, est = beta0;
-  int converged = 0, iters = 0, restarts = 0;
-  const int G = RED_BLOCKS, T = RED_THREADS;
-  double *status = K.partials + (size_t)(m + 1) * RED_BLOCKS;
-  for (int outer = 0; outer < cfg->max_outer; ++outer) {
-    if (beta <= st.target) {  // (:148-150)
-      converged = 1;
-      break;
+  std::vector<KState> st(nb);
+  for (int q = 0; q < nb; ++q) {
+    rep[q].beta0 = beta[q];
+    est[q] = beta[q];
+    if (!active[q]) continue;
+    push_hist(q, beta[q]);
+    if (beta[q] == 0.0) {  // (:140-141)
+      converged[q] = 1;
+      active[q] = 0;
     }
-    k_scale<<<G, T, 0, s>>>(K.r, K.V, n, K.beta);  // V0 = r / beta (a division, :151)
-    LAUNCH(cudaGetLastError());
-    k_cycle_init<<<1, 128, 0, s>>>(K.g, m, K.beta, K.H);
-    LAUNCH(cudaGetLastError());
-    int j_used = 0;
-    bool stop = false;
+    st[q] = KState{};
+    st[q].beta0 = beta[q];
+    st[q].target = target[q] = cfg->tol * beta[q];
+    st[q].floor = HAPPY_BREAKDOWN_RTOL * beta[q];
+  }
+  CUDA_TRY(cudaMemcpyAsync(K.st, st.data(), sizeof(KState) * nb, cudaMemcpyHostToDevice, s));
+  const int G = d.rb, T = RED_THREADS;
+  for (int outer = 0; outer < cfg->max_outer; ++outer) {
+    int any = 0;
+    for (int q = 0; q < nb; ++q) {
+      running[q] = 0;
+      jused[q] = 0;
+      if (!active[q]) continue;
+      if (beta[q] <= target[q]) {  // (:148-150)
+        converged[q] = 1;
+        active[q] = 0;
+        continue;
+      }
+      running[q] = 1;
+      any = 1;
+    }
+    if (!any) break;
+    if ((rc = upload_mask(dev, running, K.mask))) return rc;
+    LAUNCH((k_scale<<<dim3(G, nb), T, 0, s>>>(K.r, K.V, n, K.beta, 1, K.mask), cudaGetLastError()));
+    LAUNCH((k_cycle_init<<<nb, 128, 0, s>>>(K.g, K.H, M, K.beta, K.mask, d.scal), cudaGetLastError()));
+    std::vector<int> cycle(running);
     for (int j = 0; j < m; ++j) {
-      double *Vj = K.V + (size_t)j * n;
-      double *Zj = K.Z + (size_t)j * n;
+      bool anyrun = false;
+      for (int q = 0; q < nb; ++q) anyrun |= running[q] != 0;
+      if (!anyrun) break;
+      double *Vj = K.V + (size_t)j * nbn;
+      double *Zj = K.Z + (size_t)j * nbn;
       if ((rc = dev_solve(dev, Vj, Zj))) return rc;                    // z = M(V_j)   :161
       if ((rc = dev_spmv(dev, Zj, K.w, nullptr, nullptr))) return rc;  // w = K z      :163
       const int nv = j + 1;
       // cgs2_step (:93-105): h1 = V^T w; w1 = w - V h1; h2 = V^T w1; w2 = w1 - V h2
-      k_dots<<<G, T, 0, s>>>(K.V, nv, n, K.w, K.partials);
-      LAUNCH(cudaGetLastError());
-      LAUNCH(launch_reduce_partials(K.partials, nv, RED_BLOCKS, K.h1, 0, s));
-      k_cgs<<<G, T, 0, s>>>(K.V, nv, n, K.w, K.h1, K.w1, 0, nullptr);
-      LAUNCH(cudaGetLastError());
-      k_dots<<<G, T, 0, s>>>(K.V, nv, n, K.w1, K.partials);
-      LAUNCH(cudaGetLastError());
-      LAUNCH(launch_reduce_partials(K.partials, nv, RED_BLOCKS, K.h2, 0, s));
-      k_cgs<<<G, T, 0, s>>>(K.V, nv, n, K.w1, K.h2, K.w, 1, K.partials);
-      LAUNCH(cudaGetLastError());
-      LAUNCH(launch_reduce_partials(K.partials, 1, RED_BLOCKS, K.nrm, 0, s));
-      k_givens<<<1, 32, 0, s>>>(K.st, j, m, K.h1, K.h2, K.nrm, K.H, K.cs, K.sn, K.g, status);
-      LAUNCH(cudaGetLastError());
-      if ((rc = read_status(dev, status, 3, &nonfinite))) return rc;
-      if (nonfinite) {
-        rep->nonfinite = 1;
-        rep->iterations = iters;
-        return set_error(KKT_ERR_NONFINITE, "preconditioner or operator produced a non-finite entry");
+      LAUNCH((k_dots<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w, K.mask, K.partials), cudaGetLastError()));
+      LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h1, M + 1, 0, s));
+      LAUNCH((k_cgs<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w, K.h1, M + 1, K.w1, 0, K.mask, nullptr),
+              cudaGetLastError()));
+      LAUNCH((k_dots<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w1, K.mask, K.partials), cudaGetLastError()));
+      LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h2, M + 1, 0, s));
+      LAUNCH((k_cgs<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w1, K.h2, M + 1, K.w, 1, K.mask, K.partials),
+              cudaGetLastError()));
+      LAUNCH(launch_reduce_partials(d, K.partials, 1, K.nrm, 1, 0, s));
+      LAUNCH((k_givens<<<nb, 32, 0, s>>>(K.st, j, M, K.h1, K.h2, K.nrm, K.H, K.cs, K.sn, K.g, K.status,
+                                         K.mask, d.scal),
+              cudaGetLastError()));
+      if ((rc = read_block(dev, K.status, 4 * nb))) return rc;
+      bool changed = false;
+      for (int q = 0; q < nb; ++q) {
+        if (!running[q]) continue;
+        const double *stq = dev->pinned + 4 * q;
+        if (stq[3] != 0.0) {
+          rep[q].iterations = iters[q];
+          return fail_nonfinite(q);
+        }
+        est[q] = stq[0];
+        push_hist(q, est[q]);
+        iters[q]++;
+        jused[q] = j + 1;
+        if (stq[1] != 0.0) {  // est <= target or happy breakdown (:184-186)
+          running[q] = 0;
+          changed = true;
+        }
       }
-      est = dev->pinned[0];
-      stop = dev->pinned[1] != 0.0;
-      push_hist(est);
-      iters++;
-      j_used = j + 1;
-      if (stop) break;  // est <= target or happy breakdown (:184-186)
-      k_scale<<<G, T, 0, s>>>(K.w, K.V + (size_t)(j + 1) * n, n, status + 2);  // V_{j+1} = w/hj1
-      LAUNCH(cudaGetLastError());
+      if (j + 1 < m) {
+        if (changed && (rc = upload_mask(dev, running, K.mask))) return rc;
+        // V_{j+1} = w / hj1 for the systems still running
+        LAUNCH((k_scale<<<dim3(G, nb), T, 0, s>>>(K.w, K.V + (size_t)(j + 1) * nbn, n, K.status + 2, 4,
+                                                  K.mask),
+                cudaGetLastError()));
+      }
     }
-    // y = R^{-1} g; x += Z y; r = b - K x; beta = ||r||                    (:189-192)
-    k_solve_upper<<<1, 32, 0, s>>>(K.H, m, K.g, j_used, K.yv);
-    LAUNCH(cudaGetLastError());
-    k_update_x<<<G, T, 0, s>>>(K.x, K.Z, n, K.yv, j_used);
-    LAUNCH(cudaGetLastError());
+    // y = R^{-1} g; x += Z y; r = b - K x; beta = ||r||                      (:189-192)
+    CUDA_TRY(cudaMemcpyAsync(K.jused, jused.data(), 4 * nb, cudaMemcpyHostToDevice, s));
+    LAUNCH((k_solve_upper<<<nb, 32, 0, s>>>(K.H, M, K.g, K.jused, K.yv), cudaGetLastError()));
+    LAUNCH((k_update_x<<<dim3(G, nb), T, 0, s>>>(K.x, K.Z, nb, n, K.yv, M + 1, K.jused), cudaGetLastError()));
     if ((rc = dev_spmv(dev, K.x, K.r, b, K.partials))) return rc;
-    LAUNCH(launch_reduce_partials(K.partials, 1, RED_BLOCKS, K.beta, 1, s));
-    if ((rc = read_status(dev, K.beta, 1, &nonfinite))) return rc;
-    if (nonfinite) {
-      rep->nonfinite = 1;
-      return set_error(KKT_ERR_NONFINITE, "operator produced a non-finite entry");
-    }
-    beta = dev->pinned[0];
-    restarts++;
-    if (stop || beta <= st.target) {  // (:194-198)
-      converged = 1;
-      break;
+    LAUNCH(launch_reduce_partials(d, K.partials, 1, K.beta, 1, 1, s));
+    if ((rc = upload_mask(dev, cycle, K.mask))) return rc;
+    LAUNCH((k_status<<<1, 64, 0, s>>>(K.status, d.scal, K.beta, nb), cudaGetLastError()));
+    if ((rc = read_block(dev, K.status, 4 * nb))) return rc;
+    for (int q = 0; q < nb; ++q) {
+      if (!cycle[q]) continue;
+      beta[q] = dev->pinned[4 * q];
+      if (dev->pinned[4 * q + 3] != 0.0) return fail_nonfinite(q);
+      restarts[q]++;
+      // (:194-198): a stop inside the cycle converges it; otherwise the true residual must
+      if (!running[q] || beta[q] <= target[q]) {
+        converged[q] = 1;
+        active[q] = 0;
+      }
     }
   }
-  CUDA_TRY(cudaMemcpyAsync(xout, K.x, 8 * (size_t)n, cudaMemcpyDeviceToDevice, s));
-  rep->iterations = iters;
-  rep->precond_applications = iters;
-  rep->converged = converged;
-  rep->restarts = restarts;
-  rep->est_final = est;
-  rep->true_final = beta;
+  CUDA_TRY(cudaMemcpyAsync(xout, K.x, 8 * nbn, cudaMemcpyDeviceToDevice, s));
+  for (int q = 0; q < nb; ++q) {
+    rep[q].iterations = iters[q];
+    rep[q].precond_applications = iters[q];
+    rep[q].converged = converged[q];
+    rep[q].restarts = restarts[q];
+    rep[q].est_final = est[q];
+    rep[q].true_final = beta[q];
+  }
   return KKT_OK;
 }
 

@@ -1,17 +1,20 @@
 // Numeric refactorization on the frozen schedule (direct_lu.refactorize, direct_lu.py:297-356).
 //
-// Persistent warp-per-column kernel, sync-free.  Columns are dispatched in DAG-level order
-// through an atomic ticket.  Column j's workspace x (its pattern: U rows, diagonal, L rows
-// — sorted positions) lives in shared memory.  The warp replays so(j) in the reference's
-// topological order; each update pair carries its precomputed workspace slot.
+// Persistent warp-per-task kernel, sync-free.  A task is (column, system); tasks are
+// dispatched through an atomic ticket in DAG-level order (column-major, system-minor), so
+// the chains of all nb systems advance together.  A task's workspace x (the column pattern:
+// U rows, diagonal, L rows — sorted positions) lives in shared memory.  The warp replays
+// so(j) in the reference's topological order; each update pair carries its precomputed
+// workspace slot.
 //
 // Readiness without flags: every L entry is reset to a sentinel NaN bit pattern before the
-// launch, and a consumer simply re-reads an entry of L(:,k) until it is no longer the
-// sentinel — the producer's store of the value is the signal (no fences, one L2 round trip
-// per dependency hop).  Update pairs are staged in shared memory a chunk at a time so the
-// L2 latency overlaps across up to REFACTOR_STAGE pairs; the sequential replay then runs
-// from shared memory.  Products and differences are rounded separately (no FMA) and every
-// workspace entry receives its updates in the reference order => bitwise equal factors.
+// launch, and a consumer re-reads an entry of L(:,k) until it is no longer the sentinel —
+// the producer's store of the value is the signal (no fences, one L2 round trip per hop).
+// Producers publish L(:,j) before any other bookkeeping.  Update pairs are staged in shared
+// memory a chunk at a time so L2 latency overlaps across up to REFACTOR_STAGE pairs; the
+// sequential replay then runs from shared memory.  Products and differences are rounded
+// separately (no FMA) and every workspace entry receives its updates in the reference
+// order => bitwise equal factors.
 #include <cuda_runtime.h>
 
 #include "device.h"
@@ -20,18 +23,21 @@
 namespace kkt {
 
 // ----------------------------------------------------------------------------
-// Operator values: expand caller layout -> general CSR, inf-norms, max|a|.
-// One thread per row; sums in entry order (np.bincount order => bitwise).
+// Operator values: expand caller layout -> general CSR, inf-norms, max|a| (blockIdx.y =
+// system).  One thread per row; sums in entry order (np.bincount order => bitwise).
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_expand_norms(DevPlan d) {
   __shared__ double sh[3][8];
+  const int b = blockIdx.y;
+  const double *in = d.in_vals + (size_t)b * d.in_cap;
+  double *av = d.A_vals + (size_t)b * d.nnz_a;
   double mx = 0.0, sg = 0.0, op = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x) {
-    const int b = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
+    const int rb = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
     double g = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int p = b; p < e; ++p) {
-      const double v = d.in_vals[d.sym_lower ? d.gen_src[p] : p];
-      d.A_vals[p] = v;
+    for (int p = rb; p < e; ++p) {
+      const double v = in[d.sym_lower ? d.gen_src[p] : p];
+      av[p] = v;
       const double a = fabs(v);
       g = __dadd_rn(g, a);
       if (p < s) s1 = __dadd_rn(s1, a); else s2 = __dadd_rn(s2, a);
@@ -57,14 +63,17 @@ __global__ void __launch_bounds__(256) k_expand_norms(DevPlan d) {
     double m = 0.0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) m = fmax(m, sh[threadIdx.x][q]);
     const int slot = threadIdx.x == 0 ? SC_MAXABS_A : threadIdx.x == 1 ? SC_INFNORM : SC_OPNORM;
-    atomic_max_nonneg(&d.scal[slot], m);
+    atomic_max_nonneg(&d.scal[(size_t)b * SCAL_STRIDE + slot], m);
   }
 }
 
+__device__ __forceinline__ double patch_floor(const DevPlan &d, int b) {
+  // eps_patch = 1e-12 * inf_norm(Ag)                                         (:318)
+  return __dmul_rn(PATCH_RELATIVE_FLOOR,
+                   __longlong_as_double((long long)d.scal[(size_t)b * SCAL_STRIDE + SC_INFNORM]));
+}
+
 __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
-  // eps_patch = 1e-12 * inf_norm(Ag)                                       (:318)
-  const double eps =
-      __dmul_rn(PATCH_RELATIVE_FLOOR, __longlong_as_double((long long)d.scal[SC_INFNORM]));
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -72,23 +81,31 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
   double *x = smem + (size_t)wib * wstride;
   double *st_l = x + d.maxpat;
   int *st_s = reinterpret_cast<int *>(st_l + REFACTOR_STAGE);
+  const int ntask = (d.n - d.ref_start) * d.nb;
   while (true) {
-    int idx = 0;
-    if (lane == 0) idx = d.ref_start + atomicAdd(d.ticket, 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
-    if (idx >= d.n) break;
-    const int j = d.col_order[idx];
-    if (d.trace_ref && lane == 0) d.trace_ref[2 * j] = globaltimer();
+    int task = 0;
+    if (lane == 0) task = atomicAdd(d.ticket, 1);
+    task = __shfl_sync(0xffffffffu, task, 0);
+    if (task >= ntask) break;
+    const int sys = task % d.nb;
+    const int j = d.col_order[d.ref_start + task / d.nb];
+    double *Lx = d.Lx + (size_t)sys * d.nnz_L;
+    double *Ux = d.Ux + (size_t)sys * d.nnz_U;
+    double *Lv = d.Lv + (size_t)sys * d.nnz_L;
+    double *Uv = d.Uv + (size_t)sys * d.nnz_U;
+    const double *av = d.A_vals + (size_t)sys * d.nnz_a;
+    const bool trace = d.trace_ref && sys == 0;
+    if (trace && lane == 0) d.trace_ref[2 * j] = globaltimer();
+    const double eps = patch_floor(d, sys);
     const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
     const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
     const int np = nu + 1 + nl;
     for (int s = lane; s < np; s += 32) x[s] = 0.0;
     __syncwarp();
-    // x[a_tgt] = avals[a_src]                                               (:323)
-    for (int q = d.ap_ptr[j] + lane; q < d.ap_ptr[j + 1]; q += 32)
-      x[d.a_slot[q]] = d.A_vals[d.a_src[q]];
+    // x[a_tgt] = avals[a_src]                                                 (:323)
+    for (int q = d.ap_ptr[j] + lane; q < d.ap_ptr[j + 1]; q += 32) x[d.a_slot[q]] = av[d.a_src[q]];
     __syncwarp();
-    // for k in so(j) (topological): x[Li(k)] -= Lx(k) * x[k]                (:324-326)
+    // for k in so(j) (topological): x[Li(k)] -= Lx(k) * x[k]                  (:324-326)
     const int t_end = d.so_ptr[j + 1];
     int t0 = d.so_ptr[j];
     while (t0 < t_end) {
@@ -116,7 +133,7 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
         for (int q = 0; q < 4; ++q) {
           const int p = p0 + q * 32 + lane;
           if (p < npairs) {
-            lv[q] = ld_relaxed_f64(&d.Lx[d.upd_lidx[pair0 + p]]);
+            lv[q] = ld_relaxed_f64(&Lx[d.upd_lidx[pair0 + p]]);
             sv[q] = d.upd_slot[pair0 + p];
           }
         }
@@ -137,34 +154,35 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
         const double xk = x[kslot];
         const int lbk = __shfl_sync(0xffffffffu, m.w, i);  // L(:,k) = Lx[lbk, lbk+cnt)
         if (!big) {
-          // L(:,k) not yet published when staged?  One lane waits (with back-off) so a
-          // column many warps depend on is not polled by every lane of every consumer;
-          // then the whole step is re-staged with one parallel round trip.
+          // L(:,k) not yet published when staged?  One lane waits so a column many warps
+          // depend on is not polled by every lane of every consumer; then the whole step
+          // is re-staged with one parallel round trip.
           bool miss = false;
           for (int e = lane; e < cnt; e += 32) miss |= is_sentinel(st_l[off + e]);
           const unsigned mm = __ballot_sync(0xffffffffu, miss);
           if (mm) {
-            if (lane == __ffs(mm) - 1) wait_value(&d.Lx[lbk + cnt - 1], d.poll_ns);
+            if (lane == __ffs(mm) - 1) wait_value(&Lx[lbk + cnt - 1], d.poll_ns);
             __syncwarp();
             double lv[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              if (lane + 32 * q < cnt) lv[q] = ld_relaxed_f64(&d.Lx[lbk + lane + 32 * q]);
+              if (lane + 32 * q < cnt) lv[q] = ld_relaxed_f64(&Lx[lbk + lane + 32 * q]);
 #pragma unroll
             for (int q = 0; q < 8; ++q)
               if (lane + 32 * q < cnt) st_l[off + lane + 32 * q] = lv[q];
-            for (int e = lane + 256; e < cnt; e += 32) st_l[off + e] = ld_relaxed_f64(&d.Lx[lbk + e]);
+            for (int e = lane + 256; e < cnt; e += 32) st_l[off + e] = ld_relaxed_f64(&Lx[lbk + e]);
           }
           for (int e = lane; e < cnt; e += 32) {
             double l = st_l[off + e];
-            if (is_sentinel(l)) l = wait_value(&d.Lx[lbk + e]);  // rare: store not yet visible
+            if (is_sentinel(l)) l = wait_value(&Lx[lbk + e]);  // rare: store not yet visible
             const int s = st_s[off + e];
             x[s] = __dsub_rn(x[s], __dmul_rn(l, xk));
           }
-          if (d.trace_step && lane == 0) d.trace_step[t0 + i] = globaltimer() | (mm ? 1ull : 0ull);
+          if (d.trace_step && sys == 0 && lane == 0)
+            d.trace_step[t0 + i] = globaltimer() | (mm ? 1ull : 0ull);
         } else {
           for (int e = lane; e < cnt; e += 32) {
-            const double l = wait_value_backoff(&d.Lx[lbk + e]);
+            const double l = wait_value_backoff(&Lx[lbk + e]);
             const int s = d.upd_slot[pair0 + e];
             x[s] = __dsub_rn(x[s], __dmul_rn(l, xk));
           }
@@ -173,19 +191,19 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
       }
       t0 += nsteps;
     }
-    // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj; U(:,j) = x[Ui]               (:327-344)
-    // L(:,j) is what other columns wait for: publish it first, bookkeeping after.
+    // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj; U(:,j) = x[Ui]                 (:327-344)
+    // L(:,j) is what other tasks wait for: publish it first, bookkeeping after.
     double gm = 0.0;
     double ujj = x[nu];
     gm = fmax(gm, fabs(ujj));
     if (fabs(ujj) < eps) {
       ujj = (ujj >= 0.0) ? eps : -eps;
-      if (lane == 0) atomicAdd(&d.scal[SC_PATCHED], 1ull);
+      if (lane == 0) atomicAdd(&d.scal[(size_t)sys * SCAL_STRIDE + SC_PATCHED], 1ull);
     }
     for (int s = lane; s < nl; s += 32) {
       const double v = x[nu + 1 + s];
       gm = fmax(gm, fabs(v));
-      st_relaxed_f64(&d.Lx[lb + s], unsentinel(__ddiv_rn(v, ujj)));  // value == readiness
+      st_relaxed_f64(&Lx[lb + s], unsentinel(__ddiv_rn(v, ujj)));  // value == readiness
     }
     // CSR copies for the solves (scatter through the maps: batch the map loads)
     for (int s0 = 0; s0 < nl; s0 += 128) {
@@ -198,7 +216,7 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int s = s0 + 32 * q + lane;
-        if (s < nl) d.Lv[mp[q]] = unsentinel(__ddiv_rn(x[nu + 1 + s], ujj));
+        if (s < nl) Lv[mp[q]] = unsentinel(__ddiv_rn(x[nu + 1 + s], ujj));
       }
     }
     for (int s0 = 0; s0 < nu; s0 += 128) {
@@ -213,17 +231,17 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
         const int s = s0 + 32 * q + lane;
         if (s < nu) {
           const double v = x[s];
-          d.Ux[ub + s] = v;
-          d.Uv[mp[q]] = v;
+          Ux[ub + s] = v;
+          Uv[mp[q]] = v;
           gm = fmax(gm, fabs(v));
         }
       }
     }
     gm = warp_max(gm);
     if (lane == 0) {
-      d.udiag[j] = ujj;
-      atomic_max_nonneg(&d.scal[SC_GMAX], gm);
-      if (d.trace_ref) d.trace_ref[2 * j + 1] = globaltimer();
+      d.udiag[(size_t)sys * d.n + j] = ujj;
+      atomic_max_nonneg(&d.scal[(size_t)sys * SCAL_STRIDE + SC_GMAX], gm);
+      if (trace) d.trace_ref[2 * j + 1] = globaltimer();
     }
     __syncwarp();
   }
@@ -231,71 +249,112 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
 
 // ----------------------------------------------------------------------------
 // Wide leading levels (level 0: no replay steps; level 1: <= a few) hold most columns but
-// almost no work: one thread per column, one launch per level (the kernel boundary is the
-// dependency), workspace in local memory.  Same arithmetic order as k_refactor.
+// almost no work: one thread per (column, system), one launch per level (the kernel
+// boundary is the dependency), workspace in local memory.  Same arithmetic as k_refactor.
 // ----------------------------------------------------------------------------
 constexpr int SMALL_PAT = 64;
 
+constexpr int MAX_BATCH = 64;
+
 __global__ void __launch_bounds__(256) k_refactor_small(DevPlan d, int begin, int end) {
-  const double eps =
-      __dmul_rn(PATCH_RELATIVE_FLOOR, __longlong_as_double((long long)d.scal[SC_INFNORM]));
-  const int idx = begin + blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ unsigned long long bmax[MAX_BATCH];
+  for (int q = threadIdx.x; q < d.nb; q += blockDim.x) bmax[q] = 0ull;
+  __syncthreads();
+  const int count = end - begin;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int sys = tid / count;  // system-major: a warp mostly serves one system
+  const int idx = begin + tid % count;
   double gm = 0.0;
-  if (idx < end) {
+  if (sys < d.nb) {
     const int j = d.col_order[idx];
+    double *Lx = d.Lx + (size_t)sys * d.nnz_L;
+    const double *av = d.A_vals + (size_t)sys * d.nnz_a;
+    const double eps = patch_floor(d, sys);
     const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
     const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
     double x[SMALL_PAT];
 #pragma unroll 1
     for (int s = 0; s < nu + 1 + nl; ++s) x[s] = 0.0;
-    for (int q = d.ap_ptr[j]; q < d.ap_ptr[j + 1]; ++q) x[d.a_slot[q]] = d.A_vals[d.a_src[q]];
+    for (int q = d.ap_ptr[j]; q < d.ap_ptr[j + 1]; ++q) x[d.a_slot[q]] = av[d.a_src[q]];
     for (int t = d.so_ptr[j]; t < d.so_ptr[j + 1]; ++t) {
       const int4 m = d.so_meta[t];
       const double xk = x[m.x];
       for (int e = 0; e < m.y; ++e) {
         const int s = d.upd_slot[m.z + e];
-        x[s] = __dsub_rn(x[s], __dmul_rn(ldcg(&d.Lx[m.w + e]), xk));
+        x[s] = __dsub_rn(x[s], __dmul_rn(ldcg(&Lx[m.w + e]), xk));
       }
     }
+    double *Ux = d.Ux + (size_t)sys * d.nnz_U;
+    double *Uv = d.Uv + (size_t)sys * d.nnz_U;
+    double *Lv = d.Lv + (size_t)sys * d.nnz_L;
     for (int s = 0; s < nu; ++s) {
-      d.Ux[ub + s] = x[s];
-      d.Uv[d.Umap[ub + s]] = x[s];
+      Ux[ub + s] = x[s];
+      Uv[d.Umap[ub + s]] = x[s];
       gm = fmax(gm, fabs(x[s]));
     }
     double ujj = x[nu];
     gm = fmax(gm, fabs(ujj));
     if (fabs(ujj) < eps) {
       ujj = (ujj >= 0.0) ? eps : -eps;
-      atomicAdd(&d.scal[SC_PATCHED], 1ull);
+      atomicAdd(&d.scal[(size_t)sys * SCAL_STRIDE + SC_PATCHED], 1ull);
     }
     for (int s = 0; s < nl; ++s) {
       const double v = x[nu + 1 + s];
       gm = fmax(gm, fabs(v));
       const double l = unsentinel(__ddiv_rn(v, ujj));
-      d.Lv[d.Lmap[lb + s]] = l;
-      d.Lx[lb + s] = l;
+      Lv[d.Lmap[lb + s]] = l;
+      Lx[lb + s] = l;
     }
-    d.udiag[j] = ujj;
-    if (d.trace_ref) d.trace_ref[2 * j] = d.trace_ref[2 * j + 1] = globaltimer();
+    d.udiag[(size_t)sys * d.n + j] = ujj;
+    if (d.trace_ref && sys == 0) d.trace_ref[2 * j] = d.trace_ref[2 * j + 1] = globaltimer();
+    if (gm > 0.0) atomicMax(&bmax[sys], dbits(gm));
   }
-  gm = warp_max(gm);
-  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(&d.scal[SC_GMAX], gm);
+  __syncthreads();
+  for (int q = threadIdx.x; q < d.nb; q += blockDim.x)
+    if (bmax[q]) atomicMax(&d.scal[(size_t)q * SCAL_STRIDE + SC_GMAX], bmax[q]);
 }
 
 __global__ void k_diag_stats(DevPlan d) {
+  const int b = blockIdx.y;
+  const double *ud = d.udiag + (size_t)b * d.n;
   double mx = 0.0, mn = INFINITY;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x) {
-    const double a = fabs(d.udiag[i]);
+    const double a = fabs(ud[i]);
     mx = fmax(mx, a);
     mn = fmin(mn, a);
   }
-  atomic_max_nonneg(&d.scal[SC_MAXPIV], mx);
-  if (mn < INFINITY) atomic_min_nonneg(&d.scal[SC_MINPIV], mn);
+  mx = warp_max(mx);
+  mn = -warp_max(-mn);
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(&d.scal[(size_t)b * SCAL_STRIDE + SC_MAXPIV], mx);
+    if (mn < INFINITY) atomic_min_nonneg(&d.scal[(size_t)b * SCAL_STRIDE + SC_MINPIV], mn);
+  }
+}
+
+// mode 0: zero the value statistics of every system; mode 1: min |u_jj| := +inf
+__global__ void k_reset_scal(unsigned long long *scal, int nb, int mode) {
+  for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+    unsigned long long *s = scal + (size_t)q * SCAL_STRIDE;
+    if (mode == 0) {
+      for (int k = 0; k < SC_MINPIV; ++k) s[k] = 0ull;
+      s[SC_OPNORM] = 0ull;
+    } else {
+      s[SC_MINPIV] = 0x7FF0000000000000ull;
+    }
+  }
+}
+
+cudaError_t launch_reset_scal(const DevPlan &d, int mode, cudaStream_t s) {
+  k_reset_scal<<<1, 64, 0, s>>>(d.scal, d.nb, mode);
+  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------------------
 cudaError_t launch_expand_norms(const DevPlan &d, cudaStream_t s) {
-  if (d.n) k_expand_norms<<<min((d.n + 255) / 256, 2 * 148), 256, 0, s>>>(d);
+  if (d.n) {
+    const int bx = min((d.n + 255) / 256, max(1, 2 * 148 / d.nb));
+    k_expand_norms<<<dim3(bx, d.nb), 256, 0, s>>>(d);
+  }
   return cudaGetLastError();
 }
 
@@ -314,14 +373,15 @@ cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem
                             long long *launches) {
   if (!d.n) return cudaSuccess;
   // readiness protocol: L(:,k) entries start as the sentinel
-  cudaError_t e = cudaMemsetAsync(d.Lx, 0xFF, 8 * (size_t)d.nnz_L, s);
+  cudaError_t e = cudaMemsetAsync(d.Lx, 0xFF, 8 * (size_t)d.nnz_L * d.nb, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.ticket, 0, 4, s);
   if (e != cudaSuccess) return e;
-  // wide leading levels: thread per column, level-synchronous
+  // wide leading levels: thread per (column, system), level-synchronous
   for (int l = 0; l < d.n_small_levels; ++l) {
     const int b = d.lev_ptr[l], en = d.lev_ptr[l + 1];
     if (en > b) {
-      k_refactor_small<<<(en - b + 255) / 256, 256, 0, s>>>(d, b, en);
+      const long long thr = (long long)(en - b) * d.nb;
+      k_refactor_small<<<(unsigned)((thr + 255) / 256), 256, 0, s>>>(d, b, en);
       ++*launches;
     }
   }
@@ -333,7 +393,7 @@ cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem
 }
 
 cudaError_t launch_diag_stats(const DevPlan &d, int blocks, cudaStream_t s) {
-  if (d.n) k_diag_stats<<<blocks, 256, 0, s>>>(d);
+  if (d.n) k_diag_stats<<<dim3(max(1, blocks / d.nb), d.nb), 256, 0, s>>>(d);
   return cudaGetLastError();
 }
 

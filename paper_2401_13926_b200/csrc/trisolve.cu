@@ -42,19 +42,23 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
   const int nrows = IS_U ? d.nUg : d.nLg;
   const int *rp = IS_U ? d.Urp : d.Lrp;
   const int *ci = IS_U ? d.Uci : d.Lci;
-  const double *vals = IS_U ? d.Uv : d.Lv;
-  double *ysrc = IS_U ? d.yU : d.yL;  // dependencies (published by this sweep)
-  double *yres = IS_U ? d.yL : d.yU;  // the other sweep's buffer: reset for the next solve
-  bool bad = false;
-  for (int idx = gwarp; idx < nrows; idx += nwarps) {
+  const int64_t nnz = IS_U ? d.nnz_U : d.nnz_L;
+  const int ntask = nrows * d.nb;
+  // task = (level-ordered row index, system): row-major so all systems' copies of a row
+  // are adjacent and every dependency of a task has a smaller task index
+  for (int task = gwarp; task < ntask; task += nwarps) {
+    const int idx = task / d.nb, sys = task % d.nb;
     const int r = order[idx];
+    const double *vals = (IS_U ? d.Uv : d.Lv) + (size_t)sys * nnz;
+    double *ysrc = (IS_U ? d.yU : d.yL) + (size_t)sys * d.n;  // published by this sweep
+    double *yres = (IS_U ? d.yL : d.yU) + (size_t)sys * d.n;  // reset for the next solve
     // L: rows >= pL are the sweep block's rows; here only their leading entries (columns
     // < pL) are summed, into tacc, which seeds the sweep (same per-row order).
     const bool partial = !IS_U && r >= d.pL;
     const int beg = rp[r], end = partial ? d.Ltail_split[r - d.pL] : rp[r + 1];
     // independent loads first: the initial value and the first chunk's pattern/values
-    double acc = IS_U ? ldcg(&d.yL[r]) : b[d.row_perm[r]];
-    const double piv = IS_U ? d.udiag[r] : 1.0;  // prefetched: off the critical path
+    double acc = IS_U ? ldcg(&d.yL[(size_t)sys * d.n + r]) : b[(size_t)sys * d.n + d.row_perm[r]];
+    const double piv = IS_U ? d.udiag[(size_t)sys * d.n + r] : 1.0;  // off the critical path
     int col = 0;
     double v = 0.0;
     if (beg + lane < end) {
@@ -83,20 +87,19 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
     if (lane == 0) {
       double w = acc;
       if (partial) {
-        d.tacc[r - d.pL] = acc;
+        d.tacc[(size_t)sys * (d.n - d.pL) + r - d.pL] = acc;
         continue;
       }
       if (IS_U) w = __ddiv_rn(acc, piv);
       st_relaxed_f64(&ysrc[r], unsentinel(w));  // publish first: other rows wait on it
-      if (d.trace_trsv) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
+      if (d.trace_trsv && sys == 0) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
       st_relaxed_f64(&yres[r], __longlong_as_double((long long)SENTINEL_BITS));
       if (IS_U) {
-        xout[d.col_perm[r]] = w;
-        if (!isfinite(w)) bad = true;
+        xout[(size_t)sys * d.n + d.col_perm[r]] = w;
+        if (!isfinite(w)) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
       }
     }
   }
-  if (IS_U && bad) atomicOr(&d.scal[SC_NONFINITE], 1ull);
 }
 
 // ---- sweep phase: one CTA, the reference's column sweep on the dense separator block --------
@@ -105,6 +108,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
                                                               const double *__restrict__ b,
                                                               double *__restrict__ xout) {
   extern __shared__ double sm[];
+  const int sys = blockIdx.x;  // one CTA per system: the nb sweeps run side by side
   const int p = IS_U ? d.pU : d.pL;
   const int T = d.n - p;
   const int tid = threadIdx.x;
@@ -115,30 +119,34 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
   int *cbeg = rr + RING * SLOT;                   // [T] CSC range of step s
   int *cend = cbeg + T;                                       // [T]
   int *cperm = cend + T;                                      // [T] (U: col_perm)
-  const double *cvals = IS_U ? d.Ux : d.Lx;
+  const double *cvals = (IS_U ? d.Ux : d.Lx) + (size_t)sys * (IS_U ? d.nnz_U : d.nnz_L);
   const int *crows = IS_U ? d.Ui : d.Li;
+  double *yL = d.yL + (size_t)sys * d.n;
+  double *yU = d.yU + (size_t)sys * d.n;
+  xout += (size_t)sys * d.n;
   // step s handles column j(s): L ascending from p, U descending from n-1
   for (int s = tid; s < T; s += blockDim.x) {
     const int j = IS_U ? d.n - 1 - s : p + s;
     cbeg[s] = IS_U ? d.Up[j] + d.Uhead_off[j - p] : d.Lp[j];
     cend[s] = IS_U ? d.Up[j + 1] : d.Lp[j + 1];
     if (IS_U) {
-      dg[j - p] = d.udiag[j];
+      dg[j - p] = d.udiag[(size_t)sys * d.n + j];
       cperm[s] = d.col_perm[j];
     }
   }
   if (IS_U) {
     // acc = L result of the head rows; reset yL for the next solve
     for (int r = p + tid; r < d.n; r += blockDim.x) {
-      acc[r - p] = ldcg(&d.yL[r]);
-      d.yL[r] = __longlong_as_double((long long)SENTINEL_BITS);
+      acc[r - p] = ldcg(&yL[r]);
+      yL[r] = __longlong_as_double((long long)SENTINEL_BITS);
     }
   } else {
     // acc_r = b_perm[r] - sum_{j < p} L(r,j) y_j (ascending j) was computed by the grid
     // kernel as the partial rows; reset yU for the next solve.
+    const double *ta = d.tacc + (size_t)sys * T;
     for (int r = p + tid; r < d.n; r += blockDim.x) {
-      acc[r - p] = ldcg(&d.tacc[r - p]);
-      d.yU[r] = __longlong_as_double((long long)SENTINEL_BITS);
+      acc[r - p] = ldcg(&ta[r - p]);
+      yU[r] = __longlong_as_double((long long)SENTINEL_BITS);
     }
   }
   __syncthreads();
@@ -167,11 +175,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
     if (tid == 0) {
       const double w = unsentinel(yj);
       if (IS_U) {
-        d.yU[j] = w;
+        yU[j] = w;
         xout[cperm[s]] = yj;
         if (!isfinite(yj)) bad = true;
       } else {
-        d.yL[j] = w;
+        yL[j] = w;
       }
     }
     const int slot = s % RING;
@@ -190,7 +198,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
     }
   }
   cp_async_wait<0>();
-  if (IS_U && bad) atomicOr(&d.scal[SC_NONFINITE], 1ull);
+  if (IS_U && bad) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
 }
 
 __global__ void k_fill_sentinel(double *p, int64_t n) {
@@ -227,11 +235,11 @@ static void launch_sweep(const DevPlan &d, const double *b, double *x, int T, in
                          cudaStream_t s) {
   const size_t sm = sweep_smem(T, IS_U);
   if (maxcol <= 256)
-    k_trsv_sweep<IS_U, 32, 256><<<1, SWEEP_THREADS, sm, s>>>(d, b, x);
+    k_trsv_sweep<IS_U, 32, 256><<<d.nb, SWEEP_THREADS, sm, s>>>(d, b, x);
   else if (maxcol <= 512)
-    k_trsv_sweep<IS_U, 16, 512><<<1, SWEEP_THREADS, sm, s>>>(d, b, x);
+    k_trsv_sweep<IS_U, 16, 512><<<d.nb, SWEEP_THREADS, sm, s>>>(d, b, x);
   else
-    k_trsv_sweep<IS_U, 8, 1024><<<1, SWEEP_THREADS, sm, s>>>(d, b, x);
+    k_trsv_sweep<IS_U, 8, 1024><<<d.nb, SWEEP_THREADS, sm, s>>>(d, b, x);
 }
 
 cudaError_t trsv_configure(int *grid_blocks_per_sm) {

@@ -50,19 +50,24 @@ class ResidualStats:
 
 
 class DeviceSystem:
-    """One factorized pattern resident on one GPU: refactor / solve / spmv / FGMRES."""
+    """A factorized pattern resident on one GPU: refactor / solve / spmv / FGMRES.
 
-    def __init__(self, factors, restart_m: int = 10, device: int = 0):
+    ``batch`` > 1 holds that many same-pattern systems (values, factors, vectors are
+    system-major ``[batch][...]``); every call then processes all of them in one pass.
+    """
+
+    def __init__(self, factors, restart_m: int = 10, device: int = 0, batch: int = 1):
         torch = _torch()
         self.lib = nat.load()
         self.torch = torch
         self.n = factors.n
+        self.nb = int(batch)
         G = factors._pattern_ref
         self.pattern = G
         lm = lower_map(G)
         self.lower = lm  # (row_ptr, col_idx, gen_src) or None (structurally unsymmetric)
-        opts = nat.DeviceOpts(device=device, batch=1, restart_m=int(restart_m), trisolve_mode=0,
-                              flags=0)
+        opts = nat.DeviceOpts(device=device, batch=self.nb, restart_m=int(restart_m),
+                              trisolve_mode=0, flags=0)
         h = C.c_void_p()
         rp = np.ascontiguousarray(G.row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(G.col_idx, dtype=np.int64)
@@ -78,13 +83,13 @@ class DeviceSystem:
         self.h = h
         self.device = torch.device("cuda", device)
         self.stream = torch.cuda.ExternalStream(self.lib.kkt_dev_stream(h), device=self.device)
-        n = self.n
+        shape = (self.n,) if self.nb == 1 else (self.nb, self.n)
         f64 = torch.float64
         with torch.cuda.stream(self.stream):
-            self.b = torch.empty(n, dtype=f64, device=self.device)
-            self.x = torch.empty(n, dtype=f64, device=self.device)
-            self.x0 = torch.empty(n, dtype=f64, device=self.device)
-            self.r = torch.empty(n, dtype=f64, device=self.device)
+            self.b = torch.empty(shape, dtype=f64, device=self.device)
+            self.x = torch.empty(shape, dtype=f64, device=self.device)
+            self.x0 = torch.empty(shape, dtype=f64, device=self.device)
+            self.r = torch.empty(shape, dtype=f64, device=self.device)
         self._op_key = None
         self.nnz_L = int(factors._Li.size)
         self.nnz_U = int(factors._Ui.size)
@@ -184,29 +189,55 @@ class DeviceSystem:
 
     def fgmres_device(self, b_t, x0_t, x_t, m: int, max_outer: int, tol: float,
                       hist_cap: int = 4096):
+        """FGMRES on every system; returns (report, history) or lists of them (batch)."""
         cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(tol), delta_tol=float(tol))
-        rep = nat.KrylovReport()
-        hist = (C.c_double * hist_cap)()
+        reps = (nat.KrylovReport * self.nb)()
+        hist = (C.c_double * (hist_cap * self.nb))()
         nat.check(self.lib.kkt_dev_fgmres(self.h, _vp(b_t), _vp(x0_t), _vp(x_t), C.byref(cfg),
-                                          C.byref(rep), hist, hist_cap), "kkt_dev_fgmres")
-        nh = min(rep.iterations + 1, hist_cap)
-        return rep, [hist[i] for i in range(nh)]
+                                          reps, hist, hist_cap), "kkt_dev_fgmres")
+        out = []
+        for q in range(self.nb):
+            nh = min(reps[q].iterations + 1, hist_cap)
+            out.append((reps[q], [hist[q * hist_cap + i] for i in range(nh)]))
+        return out[0] if self.nb == 1 else out
 
     def step(self, values: np.ndarray | object, layout: int, r, x_out, on_device: bool,
-             m: int, max_outer: int, delta_tol: float):
-        """refactor -> solve -> refine_fgmres in one C call (kkt_dev_step)."""
+             m: int, max_outer: int, delta_tol: float, diag: bool = False):
+        """refactor -> solve -> refine_fgmres in one C call (kkt_dev_step) for every system.
+
+        Returns the KrylovReport (single system) or the list of reports (batch); with
+        ``diag`` also the per-system LuDiagnostics array ``[nb][4]``.
+        """
         cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(delta_tol),
                             delta_tol=float(delta_tol))
-        rep = nat.KrylovReport()
+        reps = (nat.KrylovReport * self.nb)()
+        dg = (C.c_double * (4 * self.nb))() if diag else None
         if on_device:
             args = (_vp(values), layout, _vp(r), _vp(x_out), 1)
         else:
             args = (values.ctypes.data_as(C.c_void_p), layout, r.ctypes.data_as(C.c_void_p),
                     x_out.ctypes.data_as(C.c_void_p), 0)
-        nat.check(self.lib.kkt_dev_step(self.h, *args, C.byref(cfg), C.byref(rep), None),
-                  "kkt_dev_step")
+        nat.check(self.lib.kkt_dev_step(self.h, *args, C.byref(cfg), reps, dg), "kkt_dev_step")
         self._op_key = None
+        rep = reps[0] if self.nb == 1 else list(reps)
+        if diag:
+            return rep, np.array(list(dg)).reshape(self.nb, 4)
         return rep
+
+    def refactor_batch(self, values_t, layout: int) -> np.ndarray:
+        """Refactorize all systems from device values [nb][nnz]; returns diagnostics [nb][4]."""
+        dg = (C.c_double * (4 * self.nb))()
+        nat.check(self.lib.kkt_dev_refactor(self.h, _vp(values_t), layout, 1, dg), "kkt_dev_refactor")
+        self._op_key = None
+        return np.array(list(dg)).reshape(self.nb, 4)
+
+    def download_factors_batch(self):
+        Lx = np.empty(self.nnz_L * self.nb)
+        Ux = np.empty(self.nnz_U * self.nb)
+        Ud = np.empty(self.n * self.nb)
+        nat.check(self.lib.kkt_dev_download_factors(self.h, nat.ptr_f64(Lx), nat.ptr_f64(Ux),
+                                                    nat.ptr_f64(Ud)))
+        return (Lx.reshape(self.nb, -1), Ux.reshape(self.nb, -1), Ud.reshape(self.nb, -1))
 
     def info(self) -> dict:
         v = (C.c_int64 * 16)()
