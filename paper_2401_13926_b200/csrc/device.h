@@ -53,7 +53,14 @@ struct DevPlan {
   unsigned long long *scal;                 // [nb][SCAL_STRIDE]
   int *ticket;
   double *partials;                         // [nb][8][rb]
+  // systems to process (nullptr = all).  A system may skip a whole solve: after a complete
+  // solve yL is all-sentinel and yU published, which is exactly the state a solve expects.
+  const int *sys_mask = nullptr;
 };
+
+__device__ __forceinline__ bool sys_active(const DevPlan &d, int sys) {
+  return d.sys_mask == nullptr || d.sys_mask[sys] != 0;
+}
 
 // indices into a system's scalar block (bit patterns of non-negative doubles unless noted)
 enum {

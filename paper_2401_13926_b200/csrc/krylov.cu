@@ -259,6 +259,10 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
   }
   Krylov &K = *dev->kry;
   const int m = cfg->m, M = K.m;  // M: workspace stride (>= m)
+  struct MaskGuard {  // the solves/SpMVs below only touch the running systems
+    DevPlan &d;
+    ~MaskGuard() { d.sys_mask = nullptr; }
+  } guard{d};
   cudaStream_t s = dev->stream;
   const size_t nbn = (size_t)nb * n;
   std::vector<int> hn(nb, 0), active(nb, 1), running(nb, 0), jused(nb, 0);
@@ -330,8 +334,10 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
       if (!anyrun) break;
       double *Vj = K.V + (size_t)j * nbn;
       double *Zj = K.Z + (size_t)j * nbn;
+      d.sys_mask = K.mask;
       if ((rc = dev_solve(dev, Vj, Zj))) return rc;                    // z = M(V_j)   :161
       if ((rc = dev_spmv(dev, Zj, K.w, nullptr, nullptr))) return rc;  // w = K z      :163
+      d.sys_mask = nullptr;
       const int nv = j + 1;
       // cgs2_step (:93-105): h1 = V^T w; w1 = w - V h1; h2 = V^T w1; w2 = w1 - V h2
       LAUNCH((k_dots<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w, K.mask, K.partials), cudaGetLastError()));
@@ -376,9 +382,11 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
     CUDA_TRY(cudaMemcpyAsync(K.jused, jused.data(), 4 * nb, cudaMemcpyHostToDevice, s));
     LAUNCH((k_solve_upper<<<nb, 32, 0, s>>>(K.H, M, K.g, K.jused, K.yv), cudaGetLastError()));
     LAUNCH((k_update_x<<<dim3(G, nb), T, 0, s>>>(K.x, K.Z, nb, n, K.yv, M + 1, K.jused), cudaGetLastError()));
-    if ((rc = dev_spmv(dev, K.x, K.r, b, K.partials))) return rc;
-    LAUNCH(launch_reduce_partials(d, K.partials, 1, K.beta, 1, 1, s));
     if ((rc = upload_mask(dev, cycle, K.mask))) return rc;
+    d.sys_mask = K.mask;
+    if ((rc = dev_spmv(dev, K.x, K.r, b, K.partials))) return rc;
+    d.sys_mask = nullptr;
+    LAUNCH(launch_reduce_partials(d, K.partials, 1, K.beta, 1, 1, s));
     LAUNCH((k_status<<<1, 64, 0, s>>>(K.status, d.scal, K.beta, nb), cudaGetLastError()));
     if ((rc = read_block(dev, K.status, 4 * nb))) return rc;
     for (int q = 0; q < nb; ++q) {

@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
   // are adjacent and every dependency of a task has a smaller task index
   for (int task = gwarp; task < ntask; task += nwarps) {
     const int idx = task / d.nb, sys = task % d.nb;
+    if (!sys_active(d, sys)) continue;
     const int r = order[idx];
     const double *vals = (IS_U ? d.Uv : d.Lv) + (size_t)sys * nnz;
     double *ysrc = (IS_U ? d.yU : d.yL) + (size_t)sys * d.n;  // published by this sweep
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_trsv_sweep(DevPlan d,
                                                               double *__restrict__ xout) {
   extern __shared__ double sm[];
   const int sys = blockIdx.x;  // one CTA per system: the nb sweeps run side by side
+  if (!sys_active(d, sys)) return;
   const int p = IS_U ? d.pU : d.pL;
   const int T = d.n - p;
   const int tid = threadIdx.x;

@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_spmv(DevPlan d, const double *_
                                                       double *__restrict__ nrm_out) {
   __shared__ double sh[32];
   const int sys = blockIdx.y;
+  if (!sys_active(d, sys)) return;
   const size_t off = (size_t)sys * d.n;
   const double *av = d.A_vals + (size_t)sys * d.nnz_a;
   x += off;
