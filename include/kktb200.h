@@ -148,6 +148,8 @@ typedef struct {
   int max_outer;          /* restart cycles                  (krylov.py:62) */
   double tol;             /* relative tolerance              (krylov.py:63) */
   double delta_tol;       /* refinement trigger (refine only; refine.py:35) */
+  const double *delta_sys; /* optional per-system delta_tol (and tol) [batch], or NULL:
+                              each system of a batch may carry its own barrier parameter */
 } kkt_krylov_cfg;
 
 typedef struct {

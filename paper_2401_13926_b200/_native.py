@@ -39,7 +39,7 @@ class DeviceOpts(C.Structure):
 
 class KrylovCfg(C.Structure):
     _fields_ = [("m", C.c_int), ("max_outer", C.c_int), ("tol", C.c_double),
-                ("delta_tol", C.c_double)]
+                ("delta_tol", C.c_double), ("delta_sys", C.POINTER(C.c_double))]
 
 
 class KrylovReport(C.Structure):

@@ -565,7 +565,9 @@ int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_d
   std::vector<int> trig(nb, 0);
   int any = 0;
   for (int q = 0; q < nb; ++q) {
-    trig[q] = st[6 * q] > cfg->delta_tol * st[6 * q + 4] ? 1 : 0;
+    const double dq = cfg->delta_sys ? cfg->delta_sys[q] : cfg->delta_tol;
+    if (!(dq > 0)) return kkt::set_error(KKT_ERR_BAD_ARG, "delta_tol must be positive");
+    trig[q] = st[6 * q] > dq * st[6 * q + 4] ? 1 : 0;
     any |= trig[q];
   }
   if (!any) {

@@ -304,7 +304,8 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
     }
     st[q] = KState{};
     st[q].beta0 = beta[q];
-    st[q].target = target[q] = cfg->tol * beta[q];
+    const double tol_q = cfg->delta_sys ? cfg->delta_sys[q] : cfg->tol;
+    st[q].target = target[q] = tol_q * beta[q];
     st[q].floor = HAPPY_BREAKDOWN_RTOL * beta[q];
   }
   CUDA_TRY(cudaMemcpyAsync(K.st, st.data(), sizeof(KState) * nb, cudaMemcpyHostToDevice, s));

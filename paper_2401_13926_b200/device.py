@@ -202,14 +202,19 @@ class DeviceSystem:
         return out[0] if self.nb == 1 else out
 
     def step(self, values: np.ndarray | object, layout: int, r, x_out, on_device: bool,
-             m: int, max_outer: int, delta_tol: float, diag: bool = False):
+             m: int, max_outer: int, delta_tol, diag: bool = False):
         """refactor -> solve -> refine_fgmres in one C call (kkt_dev_step) for every system.
 
-        Returns the KrylovReport (single system) or the list of reports (batch); with
-        ``diag`` also the per-system LuDiagnostics array ``[nb][4]``.
+        ``delta_tol`` is a float or a per-system sequence.  Returns the KrylovReport (single
+        system) or the list of reports (batch); with ``diag`` also the per-system
+        LuDiagnostics array ``[nb][4]``.
         """
+        dsys = None
+        if np.ndim(delta_tol):
+            dsys = (C.c_double * self.nb)(*[float(v) for v in delta_tol])
+            delta_tol = float(np.max(delta_tol))
         cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(delta_tol),
-                            delta_tol=float(delta_tol))
+                            delta_tol=float(delta_tol), delta_sys=dsys)
         reps = (nat.KrylovReport * self.nb)()
         dg = (C.c_double * (4 * self.nb))() if diag else None
         if on_device:
