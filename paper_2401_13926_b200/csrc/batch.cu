@@ -1,0 +1,838 @@
+// Batched hot path (nb > 1 same-pattern systems, BASELINE configs[4]).
+//
+// Layout: every per-system array is INTERLEAVED, element (i, sys) at i * nbp + sys with nbp
+// = nb rounded up to a multiple of 32 (padding systems replicate system 0 and are never
+// reported).  The sparsity pattern and every schedule array are shared, so when a warp's
+// lanes are 32 systems of the same row / column the control flow is identical across lanes
+// (no divergence) and each value access is one coalesced 256-byte transaction; index loads
+// are amortised over the systems.  This is what turns the latency-bound single-system DAG
+// kernels into bandwidth-bound batched kernels.
+//
+// Every kernel keeps the reference's per-system operation order (direct_lu.py:297-379,
+// sparsecore.py:284-305), so each system's factors and solves are bitwise identical to the
+// single-system path and to the reference:
+//   k_b_refactor  — persistent, sync-free; a task is (column, chunk of S systems); the warp's
+//                   lanes are E = 32/S entries x S systems.  S is chosen per column on the
+//                   host: wide S (coalescing) for short columns, wide E (critical path) for
+//                   the heavy separator columns.  Readiness = value != sentinel, per system.
+//   k_b_trsv_grid — persistent, sync-free, warp per (row, 32 systems).
+//   (the dense trailing block of each sweep: sweep.cu, 4 systems per CTA)
+//   k_b_spmv / k_b_resid_stats / FGMRES vector kernels — 2-D blocks (32 systems x 8 rows),
+//                   fixed grids and fixed-order reductions (run-to-run deterministic).
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "device.h"
+#include "kernels.cuh"
+
+namespace kkt {
+
+constexpr int BY = 8;            // rows (warps) per block of the 2-D row kernels
+constexpr int SMALL_PAT_B = 64;
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ double sentinel_value() {
+  return __longlong_as_double((long long)SENTINEL_BITS);
+}
+
+// Fixed-order reduction over threadIdx.y (blockDim = 32 x BY) of a per-lane value; the
+// result is valid in threadIdx.y == 0.  All threads of the block must call it.
+template <bool IS_MAX>
+__device__ __forceinline__ double reduce_y(double v, double (*sh)[32]) {
+  sh[threadIdx.y][threadIdx.x] = v;
+  __syncthreads();
+  double r = v;
+  if (threadIdx.y == 0) {
+    r = sh[0][threadIdx.x];
+    for (int q = 1; q < BY; ++q) r = IS_MAX ? fmax(r, sh[q][threadIdx.x]) : r + sh[q][threadIdx.x];
+  }
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double patch_floor_b(const DevPlan &d, int sys) {
+  return __dmul_rn(PATCH_RELATIVE_FLOOR,
+                   __longlong_as_double((long long)d.scal[(size_t)sys * SCAL_STRIDE + SC_INFNORM]));
+}
+
+// ----------------------------------------------------------------------------
+// Values: caller layout [nb][in_cap] (general or symmetric-lower) -> A_vals [nnz_a][nbp],
+// plus per-system max|a|, ||A||_inf (general) and the operator norm (entry-order sums).
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_b_expand_norms(DevPlan d) {
+  __shared__ double sh[BY][32];
+  const int lane = threadIdx.x, sys = blockIdx.y * 32 + lane;
+  const double *in = d.in_vals + (size_t)(sys < d.nb ? sys : 0) * d.in_cap;
+  double mx = 0.0, sg = 0.0, op = 0.0;
+  for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
+    const int rb = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
+    double g = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int p = rb; p < e; ++p) {
+      const double v = in[d.sym_lower ? d.gen_src[p] : p];
+      d.A_vals[IL(d, p, sys)] = v;
+      const double a = fabs(v);
+      g = __dadd_rn(g, a);
+      if (p < s) s1 = __dadd_rn(s1, a); else s2 = __dadd_rn(s2, a);
+      mx = fmax(mx, a);
+    }
+    sg = fmax(sg, g);
+    op = fmax(op, d.sym_lower ? __dadd_rn(s1, s2) : g);
+  }
+  mx = reduce_y<true>(mx, sh);
+  sg = reduce_y<true>(sg, sh);
+  op = reduce_y<true>(op, sh);
+  if (threadIdx.y == 0) {
+    unsigned long long *sc = d.scal + (size_t)sys * SCAL_STRIDE;
+    atomic_max_nonneg(&sc[SC_MAXABS_A], mx);
+    atomic_max_nonneg(&sc[SC_INFNORM], sg);
+    atomic_max_nonneg(&sc[SC_OPNORM], op);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Refactor, wide leading levels: thread per (column, system), level-synchronous launches.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_b_refactor_small(DevPlan d, int begin, int end) {
+  __shared__ double sh[BY][32];
+  const int lane = threadIdx.x, sys = blockIdx.y * 32 + lane;
+  const double eps = patch_floor_b(d, sys);
+  double gm = 0.0;
+  for (int idx = begin + blockIdx.x * BY + threadIdx.y; idx < end; idx += gridDim.x * BY) {
+    const int j = d.col_order[idx];
+    const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
+    const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
+    double x[SMALL_PAT_B];
+#pragma unroll 1
+    for (int s = 0; s < nu + 1 + nl; ++s) x[s] = 0.0;
+    for (int q = d.ap_ptr[j]; q < d.ap_ptr[j + 1]; ++q) x[d.a_slot[q]] = d.A_vals[IL(d, d.a_src[q], sys)];
+    for (int t = d.so_ptr[j]; t < d.so_ptr[j + 1]; ++t) {
+      const int4 m = d.so_meta[t];
+      const double xk = x[m.x];
+      for (int e = 0; e < m.y; ++e) {
+        const int s = d.upd_slot[m.z + e];
+        x[s] = __dsub_rn(x[s], __dmul_rn(ldcg(&d.Lx[IL(d, m.w + e, sys)]), xk));
+      }
+    }
+    for (int s = 0; s < nu; ++s) {
+      d.Ux[IL(d, ub + s, sys)] = x[s];
+      d.Uv[IL(d, d.Umap[ub + s], sys)] = x[s];
+      gm = fmax(gm, fabs(x[s]));
+    }
+    double ujj = x[nu];
+    gm = fmax(gm, fabs(ujj));
+    if (fabs(ujj) < eps) {
+      ujj = (ujj >= 0.0) ? eps : -eps;
+      atomicAdd(&d.scal[(size_t)sys * SCAL_STRIDE + SC_PATCHED], 1ull);
+    }
+    for (int s = 0; s < nl; ++s) {
+      const double v = x[nu + 1 + s];
+      gm = fmax(gm, fabs(v));
+      const double l = unsentinel(__ddiv_rn(v, ujj));
+      d.Lv[IL(d, d.Lmap[lb + s], sys)] = l;
+      d.Lx[IL(d, lb + s, sys)] = l;
+    }
+    d.udiag[IL(d, j, sys)] = ujj;
+  }
+  gm = reduce_y<true>(gm, sh);
+  if (threadIdx.y == 0) atomic_max_nonneg(&d.scal[(size_t)sys * SCAL_STRIDE + SC_GMAX], gm);
+}
+
+// ----------------------------------------------------------------------------
+// Refactor, the rest of the DAG: persistent warps, tasks in DAG-level order via a ticket.
+// Lane = (entry e < E, system s < S), E * S = 32.  Workspace x[np][S] and the staged update
+// pairs live in shared memory.
+// ----------------------------------------------------------------------------
+size_t b_refactor_smem(int xbudget, int stage) {
+  return (size_t)B_WARPS * (xbudget + 3 * stage) * sizeof(double);
+}
+
+// optional per-warp cycle accounting (d.prof): [0] dispatch+meta [1] A scatter [2] staging
+// issue [3] waiting for staged data [4] replay [5] finalize [6] tasks [7] staged values
+#define PROF_MARK(k)                                            \
+  if (prof) {                                                   \
+    const long long _t = clock64();                             \
+    if (lane == 0) prof[k] += (unsigned long long)(_t - tmark); \
+    tmark = _t;                                                 \
+  }
+
+// One chunk of replay steps whose update pairs fit a stage buffer.
+struct Chunk {
+  int t0, nsteps, npairs;
+  bool big;   // a single step larger than the stage: replayed straight from global memory
+  int4 m;     // this lane's step metadata {slot of k, |L(:,k)|, first pair, first L index}
+  int incl;   // inclusive prefix of the pair counts
+};
+
+__device__ __forceinline__ Chunk chunk_meta(const DevPlan &d, int t0, int t_end, int stp, int lane) {
+  Chunk c;
+  c.t0 = t0;
+  const int t = t0 + lane;
+  c.m = make_int4(0, 0, 0, 0);
+  if (t < t_end) c.m = d.so_meta[t];
+  c.incl = c.m.y;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(FULL, c.incl, o);
+    if (lane >= o) c.incl += v;
+  }
+  c.nsteps = __popc(__ballot_sync(FULL, t < t_end && c.incl <= stp));
+  c.big = c.nsteps == 0;
+  if (c.big) c.nsteps = 1;
+  c.npairs = c.big ? 0 : __shfl_sync(FULL, c.incl, c.nsteps - 1);
+  return c;
+}
+
+// cp.async the chunk's L values (per step: |L(:,k)| x S values, contiguous per entry) and
+// the workspace slots of its pairs into one stage buffer; one commit group per chunk.
+__device__ __forceinline__ void chunk_issue(const DevPlan &d, const Chunk &c, double *stv, int *sts,
+                                            int lgS, int sys0, int lane) {
+  const int S = 1 << lgS;
+  for (int i = 0; i < c.nsteps && !c.big; ++i) {
+    const int cnt = __shfl_sync(FULL, c.m.y, i);
+    const int off = __shfl_sync(FULL, c.incl - c.m.y, i);
+    const int lbk = __shfl_sync(FULL, c.m.w, i);
+    for (int f = lane; f < (cnt << lgS); f += 32)
+      cp_async8(&stv[(off << lgS) + f], &d.Lx[IL(d, lbk + (f >> lgS), sys0 + (f & (S - 1)))]);
+  }
+  const int pair0 = __shfl_sync(FULL, c.m.z, 0);
+  for (int p = lane; p < c.npairs; p += 32) cp_async4(&sts[p], &d.upd_slot32[pair0 + p]);
+  cp_async_commit();
+}
+
+struct TaskInfo {
+  int j, lgS, sys0, ub, nu, lb, nl, t0, t_end, a0, a1;
+};
+
+__device__ __forceinline__ TaskInfo load_task(const DevPlan &d, int task) {
+  TaskInfo t;
+  t.j = -1;
+  if (task >= d.n_btask) return t;
+  const int2 tk = d.btask[task];
+  t.j = tk.x;
+  t.lgS = tk.y & 0xff;
+  t.sys0 = tk.y >> 8;
+  t.ub = d.Up[t.j];
+  t.nu = d.Up[t.j + 1] - t.ub;
+  t.lb = d.Lp[t.j];
+  t.nl = d.Lp[t.j + 1] - t.lb;
+  t.t0 = d.so_ptr[t.j];
+  t.t_end = d.so_ptr[t.j + 1];
+  t.a0 = d.ap_ptr[t.j];
+  t.a1 = d.ap_ptr[t.j + 1];
+  return t;
+}
+
+__global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int XB = d.b_xbudget, STG = d.b_stage;
+  double *x = smem + (size_t)(threadIdx.x >> 5) * (XB + 3 * STG);
+  double *stv0 = x + XB;                                   // [2][STG] staged L values
+  int *sts0 = reinterpret_cast<int *>(stv0 + 2 * STG);     // [2][STG] staged slots
+  unsigned long long *prof =
+      d.prof ? d.prof + 8 * (size_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) : nullptr;
+  long long tmark = prof ? clock64() : 0;
+  // The next task's descriptor is fetched while the current one runs (the dispatch chain
+  // ticket -> task -> column pointers is four dependent global round trips).
+  int ticket = 0;
+  if (lane == 0) ticket = atomicAdd(d.ticket, 1);
+  TaskInfo nt = load_task(d, __shfl_sync(FULL, ticket, 0));
+  while (nt.j >= 0) {
+    const TaskInfo ti = nt;
+    if (lane == 0) ticket = atomicAdd(d.ticket, 1);
+    const int j = ti.j, lgS = ti.lgS, sys0 = ti.sys0;
+    const int S = 1 << lgS, E = 32 >> lgS;
+    const int s = lane & (S - 1), e = lane >> lgS;
+    const int sys = sys0 + s;
+    const int ub = ti.ub, nu = ti.nu, lb = ti.lb, nl = ti.nl;
+    const int np = nu + 1 + nl;
+    const int stp = STG >> lgS;  // pairs per stage buffer
+    const int t_end = ti.t_end;
+    // first chunk in flight before the A scatter
+    Chunk cur = chunk_meta(d, ti.t0, t_end, stp, lane);
+    int buf = 0;
+    chunk_issue(d, cur, stv0, sts0, lgS, sys0, lane);
+    PROF_MARK(0);
+    if (prof && lane == 0) prof[6]++;
+    for (int f = lane; f < np * S; f += 32) x[f] = 0.0;
+    __syncwarp();
+    // x[a_tgt] = avals[a_src]                                                 (:323)
+    for (int q = ti.a0 + e; q < ti.a1; q += E)
+      x[d.a_slot[q] * S + s] = d.A_vals[IL(d, d.a_src[q], sys)];
+    __syncwarp();
+    nt = load_task(d, __shfl_sync(FULL, ticket, 0));  // consumed next iteration
+    PROF_MARK(1);
+    // for k in so(j) (topological): x[Li(k)] -= Lx(k) * x[k]                  (:324-326)
+    while (cur.t0 < t_end) {
+      // the next chunk's loads overlap this chunk's replay (double-buffered stage)
+      const int tn = cur.t0 + cur.nsteps;
+      Chunk nxt;
+      nxt.t0 = tn;
+      if (tn < t_end) {
+        nxt = chunk_meta(d, tn, t_end, stp, lane);
+        chunk_issue(d, nxt, stv0 + (buf ^ 1) * STG, sts0 + (buf ^ 1) * STG, lgS, sys0, lane);
+        if (prof && lane == 0) prof[7] += (unsigned long long)nxt.npairs << lgS;
+        PROF_MARK(2);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      PROF_MARK(3);
+      const double *stv = stv0 + buf * STG;
+      const int *sts = sts0 + buf * STG;
+      const int pair0 = __shfl_sync(FULL, cur.m.z, 0);
+      for (int i = 0; i < cur.nsteps; ++i) {
+        const int kslot = __shfl_sync(FULL, cur.m.x, i);
+        const int cnt = __shfl_sync(FULL, cur.m.y, i);
+        const int off = __shfl_sync(FULL, cur.incl - cur.m.y, i);
+        const int lbk = __shfl_sync(FULL, cur.m.w, i);  // L(:,k) = Lx[lbk, lbk+cnt)
+        const double xk = x[kslot * S + s];
+        if (!cur.big) {
+          // the targets of one step are distinct slots: 4 RMWs per lane in flight
+          for (int idx0 = e; idx0 < cnt; idx0 += 4 * E) {
+            double lv[4], xv[4];
+            int sl[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int idx = idx0 + q * E;
+              if (idx < cnt) {
+                lv[q] = stv[((off + idx) << lgS) + s];
+                sl[q] = sts[off + idx] * S + s;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (idx0 + q * E < cnt) xv[q] = x[sl[q]];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int idx = idx0 + q * E;
+              if (idx < cnt) {
+                double l = lv[q];  // staged before L(:,k) was published?  wait for it
+                if (is_sentinel(l)) l = wait_value_bo(&d.Lx[IL(d, lbk + idx, sys)], d.poll_ns);
+                x[sl[q]] = __dsub_rn(xv[q], __dmul_rn(l, xk));
+              }
+            }
+          }
+        } else {
+          for (int idx = e; idx < cnt; idx += E) {
+            const double l = wait_value_bo(&d.Lx[IL(d, lbk + idx, sys)], d.poll_ns);
+            const int sl = d.upd_slot32[pair0 + idx] * S + s;
+            x[sl] = __dsub_rn(x[sl], __dmul_rn(l, xk));
+          }
+        }
+        __syncwarp();
+      }
+      PROF_MARK(4);
+      cur = nxt;
+      buf ^= 1;
+    }
+    cp_async_wait<0>();
+    // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj (published first); U(:,j) = x[Ui]  (:327-344)
+    double ujj = x[nu * S + s];
+    double gm = fabs(ujj);
+    const double eps = patch_floor_b(d, sys);
+    const bool patched = fabs(ujj) < eps;
+    if (patched) ujj = (ujj >= 0.0) ? eps : -eps;
+    for (int idx = e; idx < nl; idx += E) {
+      const double v = x[(nu + 1 + idx) * S + s];
+      gm = fmax(gm, fabs(v));
+      st_relaxed_f64(&d.Lx[IL(d, lb + idx, sys)], unsentinel(__ddiv_rn(v, ujj)));
+    }
+    for (int idx = e; idx < nl; idx += E)
+      d.Lv[IL(d, d.Lmap[lb + idx], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + idx) * S + s], ujj));
+    for (int idx = e; idx < nu; idx += E) {
+      const double v = x[idx * S + s];
+      d.Ux[IL(d, ub + idx, sys)] = v;
+      d.Uv[IL(d, d.Umap[ub + idx], sys)] = v;
+      gm = fmax(gm, fabs(v));
+    }
+    for (int o = S; o < 32; o <<= 1) gm = fmax(gm, __shfl_xor_sync(FULL, gm, o));
+    if (e == 0) {
+      d.udiag[IL(d, j, sys)] = ujj;
+      unsigned long long *sc = d.scal + (size_t)sys * SCAL_STRIDE;
+      if (patched) atomicAdd(&sc[SC_PATCHED], 1ull);
+      if (gm > 0.0 && dbits(gm) > __ldcg(&sc[SC_GMAX])) atomicMax(&sc[SC_GMAX], dbits(gm));
+    }
+    __syncwarp();
+    PROF_MARK(5);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_b_diag_stats(DevPlan d) {
+  __shared__ double sh[BY][32];
+  const int sys = blockIdx.y * 32 + threadIdx.x;
+  double mx = 0.0, mn = INFINITY;
+  for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
+    const double a = fabs(d.udiag[IL(d, i, sys)]);
+    mx = fmax(mx, a);
+    mn = fmin(mn, a);
+  }
+  mx = reduce_y<true>(mx, sh);
+  mn = -reduce_y<true>(-mn, sh);
+  if (threadIdx.y == 0) {
+    atomic_max_nonneg(&d.scal[(size_t)sys * SCAL_STRIDE + SC_MAXPIV], mx);
+    if (mn < INFINITY) atomic_min_nonneg(&d.scal[(size_t)sys * SCAL_STRIDE + SC_MINPIV], mn);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Triangular solves (direct_lu.py:359-379).  Same phase split and per-row order as the
+// single-system kernels (trisolve.cu), lanes = systems.
+// ----------------------------------------------------------------------------
+template <bool IS_U>
+__global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__restrict__ b,
+                                                     double *__restrict__ xout) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int *order = IS_U ? d.U_grid_order : d.L_grid_order;
+  const int *crit = IS_U ? d.U_crit : d.L_crit;
+  const int nrows = IS_U ? d.nUg : d.nLg;
+  const int *rp = IS_U ? d.Urp : d.Lrp;
+  const int *ci = IS_U ? d.Uci : d.Lci;
+  const double *vals = IS_U ? d.Uv : d.Lv;
+  double *ysrc = IS_U ? d.yU : d.yL;  // published by this sweep
+  double *yres = IS_U ? d.yL : d.yU;  // reset for the next solve
+  const int ngroups = d.nbp >> 5;
+  const int ntask = nrows * ngroups;
+  const int gstart = IS_U ? 0 : d.L_sync_ptr[d.L_nsync];  // leading levels ran row-parallel
+  for (int task = gstart * ngroups + gwarp; task < ntask; task += nwarps) {
+    const int idx = task / ngroups;
+    const int sys = (task - idx * ngroups) * 32 + lane;
+    const unsigned amask = __ballot_sync(FULL, sys_active(d, sys));
+    if (!amask) continue;
+    const bool act = (amask >> lane) & 1u;
+    const int r = order[idx];
+    const int cr = crit[idx];
+    const int beg = rp[r], end = rp[r + 1];
+    // Everything that does not depend on the critical dependency is loaded first: the
+    // initial value, the pivot, the first 8 entries and (speculatively) their y values —
+    // the non-critical dependencies are normally published already.
+    double acc = 0.0, piv = 1.0;
+    int cols[8];
+    double vs[8], ys[8];
+    if (act) {
+      acc = IS_U ? ldcg(&d.yL[IL(d, r, sys)]) : b[IL(d, d.row_perm[r], sys)];
+      if (IS_U) piv = d.udiag[IL(d, r, sys)];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (beg + q < end) {
+          cols[q] = ci[beg + q];
+          vs[q] = vals[IL(d, beg + q, sys)];
+        }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (beg + q < end) ys[q] = ld_relaxed_f64(&ysrc[IL(d, cols[q], sys)]);
+    }
+    // one lane waits (with back-off) on the critical dependency of one system: the 32
+    // systems' values of a row are published by one warp store, so the others follow
+    if (cr >= 0 && lane == 31 - __clz(amask)) wait_value_bo(&ysrc[IL(d, cr, sys)], d.poll_ns);
+    __syncwarp();
+    if (!act) continue;  // per lane from here: systems are independent
+    // software pipeline over 8-entry chunks: the next chunk's columns and values are in
+    // flight while this chunk is consumed, so a long row costs ~one round trip per chunk
+    for (int c0 = beg; c0 < end; c0 += 8) {
+      int ncols[8];
+      double nvs[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (c0 + 8 + q < end) {
+          ncols[q] = ci[c0 + 8 + q];
+          nvs[q] = vals[IL(d, c0 + 8 + q, sys)];
+        }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (c0 + q < end) {
+          double y = ys[q];
+          if (is_sentinel(y)) y = wait_value_bo(&ysrc[IL(d, cols[q], sys)], d.poll_ns);
+          acc = __dsub_rn(acc, __dmul_rn(vs[q], y));
+        }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (c0 + 8 + q < end) {
+          cols[q] = ncols[q];
+          vs[q] = nvs[q];
+          ys[q] = ld_relaxed_f64(&ysrc[IL(d, cols[q], sys)]);
+        }
+    }
+    const double w = IS_U ? __ddiv_rn(acc, piv) : acc;
+    st_relaxed_f64(&ysrc[IL(d, r, sys)], unsentinel(w));  // publish first
+    if (d.trace_trsv && sys == 0) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
+    st_relaxed_f64(&yres[IL(d, r, sys)], sentinel_value());
+    if (IS_U) {
+      xout[IL(d, d.col_perm[r], sys)] = w;
+      if (!isfinite(w)) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
+    }
+  }
+}
+
+cudaError_t b_launch_grid_L(const DevPlan &d, const double *b, double *x, int grid_blocks, cudaStream_t s) {
+  k_b_trsv_grid<false><<<grid_blocks, 256, 0, s>>>(d, b, x);
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,
+                          cudaStream_t s, long long *launches) {
+  if (!d.n) return cudaSuccess;
+  const int TL = d.n - d.pL, TU = d.n - d.pU;
+  {
+    cudaError_t e = launch_L_front(d, b, x, grid_blocks, s, launches);
+    if (e != cudaSuccess) return e;
+  }
+  if (TL) {
+    cudaError_t e = launch_sweep_blocked(d, false, x, s);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+  }
+  if (TU) {
+    cudaError_t e = launch_sweep_blocked(d, true, x, s);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+  }
+  if (d.nUg) {
+    k_b_trsv_grid<true><<<grid_blocks, 256, 0, s>>>(d, b, x);
+    ++*launches;
+  }
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------
+// SpMV and residual statistics (sparsecore.spmv order; refine.py:62-92)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double row_dot_b(const DevPlan &d, const double *__restrict__ x, int i,
+                                            int sys) {
+  const int b = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
+  double s1 = 0.0, s2 = 0.0;
+  if (d.sym_lower) {
+    for (int p = b; p < s; ++p)
+      s1 = __dadd_rn(s1, __dmul_rn(d.A_vals[IL(d, p, sys)], x[IL(d, d.A_ci[p], sys)]));
+    for (int p = s; p < e; ++p)
+      s2 = __dadd_rn(s2, __dmul_rn(d.A_vals[IL(d, p, sys)], x[IL(d, d.A_ci[p], sys)]));
+    return __dadd_rn(s1, s2);
+  }
+  for (int p = b; p < e; ++p)
+    s1 = __dadd_rn(s1, __dmul_rn(d.A_vals[IL(d, p, sys)], x[IL(d, d.A_ci[p], sys)]));
+  return s1;
+}
+
+__global__ void __launch_bounds__(256) k_b_spmv(DevPlan d, const double *__restrict__ x,
+                                                double *__restrict__ out,
+                                                const double *__restrict__ bsub,
+                                                double *__restrict__ nrm_out) {
+  __shared__ double sh[BY][32];
+  const int sys = blockIdx.y * 32 + threadIdx.x;
+  const bool act = sys_active(d, sys);
+  if (!__syncthreads_or(act)) return;
+  double loc = 0.0;
+  bool bad = false;
+  if (act) {
+    for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
+      const double y = row_dot_b(d, x, i, sys);
+      if (!isfinite(y)) bad = true;
+      const double o = bsub ? __dsub_rn(bsub[IL(d, i, sys)], y) : y;
+      out[IL(d, i, sys)] = o;
+      loc = __dadd_rn(loc, __dmul_rn(o, o));
+    }
+  }
+  if (bad) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
+  if (nrm_out) {
+    const double t = reduce_y<false>(loc, sh);
+    if (threadIdx.y == 0 && act) nrm_out[(size_t)sys * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_b_resid_stats(DevPlan d, const double *__restrict__ r,
+                                                       const double *__restrict__ x,
+                                                       double *__restrict__ partials) {
+  __shared__ double sh[BY][32];
+  const int sys = blockIdx.y * 32 + threadIdx.x, nblk = gridDim.x;
+  double e2 = 0.0, emax = 0.0, x2 = 0.0, xmax = 0.0, r2 = 0.0;
+  for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
+    const double ri = r[IL(d, i, sys)], xi = x[IL(d, i, sys)];
+    const double ei = __dsub_rn(ri, row_dot_b(d, x, i, sys));
+    e2 += ei * ei;
+    emax = fmax(emax, fabs(ei));
+    x2 += xi * xi;
+    xmax = fmax(xmax, fabs(xi));
+    r2 += ri * ri;
+  }
+  double *part = partials + (size_t)sys * 5 * nblk;
+  e2 = reduce_y<false>(e2, sh);
+  emax = reduce_y<true>(emax, sh);
+  x2 = reduce_y<false>(x2, sh);
+  xmax = reduce_y<true>(xmax, sh);
+  r2 = reduce_y<false>(r2, sh);
+  if (threadIdx.y == 0) {
+    part[0 * nblk + blockIdx.x] = e2;
+    part[1 * nblk + blockIdx.x] = emax;
+    part[2 * nblk + blockIdx.x] = x2;
+    part[3 * nblk + blockIdx.x] = xmax;
+    part[4 * nblk + blockIdx.x] = r2;
+  }
+}
+
+// out[sys][5] = {||e||_2, ||e||_inf, ||x||_2, ||x||_inf, ||r||_2}
+__global__ void k_b_resid_final(const double *__restrict__ partials, int nblk, double *__restrict__ out) {
+  const int v = blockIdx.x, sys = blockIdx.y;
+  const double *p = partials + ((size_t)sys * 5 + v) * nblk;
+  double s = 0.0;
+  const bool is_max = (v == 1 || v == 3);
+  for (int b = threadIdx.x; b < nblk; b += 32) s = is_max ? fmax(s, p[b]) : s + p[b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double q = __shfl_down_sync(FULL, s, o);
+    s = is_max ? fmax(s, q) : s + q;
+  }
+  if (threadIdx.x == 0) out[(size_t)sys * 5 + v] = is_max ? s : sqrt(s);
+}
+
+// ----------------------------------------------------------------------------
+// FGMRES vector kernels (krylov.py:93-105, :187-190) on [n][nbp] vectors.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_b_dots(DevPlan d, const double *__restrict__ V, int nvec,
+                                                const double *__restrict__ w, const int *__restrict__ mask,
+                                                double *__restrict__ partials) {
+  __shared__ double sh[BY][32];
+  const int sys = blockIdx.y * 32 + threadIdx.x;
+  const bool act = mask[sys] != 0;
+  if (!__syncthreads_or(act)) return;
+  const size_t vstride = (size_t)d.n * d.nbp;
+  for (int g0 = 0; g0 < nvec; g0 += 8) {
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int gn = min(8, nvec - g0);
+    if (act)
+      for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
+        const double wi = w[IL(d, i, sys)];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < gn) acc[q] += V[(size_t)(g0 + q) * vstride + IL(d, i, sys)] * wi;
+      }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < gn) {
+        const double t = reduce_y<false>(acc[q], sh);
+        if (threadIdx.y == 0 && act) partials[((size_t)sys * nvec + g0 + q) * gridDim.x + blockIdx.x] = t;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_b_cgs(DevPlan d, const double *__restrict__ V, int nvec,
+                                               const double *__restrict__ w_in, const double *__restrict__ h,
+                                               int hstride, double *__restrict__ w_out, int mode,
+                                               const int *__restrict__ mask, double *__restrict__ partials) {
+  __shared__ double sh[BY][32];
+  __shared__ double hs[64][32];
+  const int sys = blockIdx.y * 32 + threadIdx.x;
+  const bool act = mask[sys] != 0;
+  if (!__syncthreads_or(act)) return;
+  for (int q = threadIdx.y; q < nvec; q += BY) hs[q][threadIdx.x] = act ? h[(size_t)sys * hstride + q] : 0.0;
+  __syncthreads();
+  const size_t vstride = (size_t)d.n * d.nbp;
+  double acc = 0.0;
+  if (act)
+    for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
+      double t = 0.0;
+      for (int q = 0; q < nvec; ++q) t += V[(size_t)q * vstride + IL(d, i, sys)] * hs[q][threadIdx.x];
+      const double o = w_in[IL(d, i, sys)] - t;
+      w_out[IL(d, i, sys)] = o;
+      acc += o * o;
+    }
+  if (mode == 1) {
+    const double t = reduce_y<false>(acc, sh);
+    if (threadIdx.y == 0 && act) partials[(size_t)sys * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_b_scale(DevPlan d, const double *__restrict__ in,
+                                                 double *__restrict__ out, const double *__restrict__ den,
+                                                 int dstride, const int *__restrict__ mask) {
+  const int sys = blockIdx.y * 32 + threadIdx.x;
+  if (!mask[sys]) return;
+  const double dv = den[(size_t)sys * dstride];
+  for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY)
+    out[IL(d, i, sys)] = __ddiv_rn(in[IL(d, i, sys)], dv);
+}
+
+__global__ void __launch_bounds__(256) k_b_update_x(DevPlan d, double *__restrict__ x,
+                                                    const double *__restrict__ Z,
+                                                    const double *__restrict__ y, int ystride,
+                                                    const int *__restrict__ jused) {
+  const int sys = blockIdx.y * 32 + threadIdx.x;
+  const int k = jused[sys];
+  if (!k) return;
+  const size_t vstride = (size_t)d.n * d.nbp;
+  const double *ys = y + (size_t)sys * ystride;
+  for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
+    double t = 0.0;
+    for (int q = 0; q < k; ++q) t = __dadd_rn(t, __dmul_rn(Z[(size_t)q * vstride + IL(d, i, sys)], ys[q]));
+    x[IL(d, i, sys)] = __dadd_rn(x[IL(d, i, sys)], t);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Caller layout <-> interleaved (32 x 32 tiles through shared memory)
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_b_to_il(DevPlan d, const double *__restrict__ src,
+                                                 double *__restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int g = blockIdx.y;
+  for (int i0 = blockIdx.x * 32; i0 < d.n; i0 += gridDim.x * 32) {
+    for (int q = threadIdx.y; q < 32; q += BY) {  // q: system within the group
+      const int sys = g * 32 + q, i = i0 + threadIdx.x;
+      if (i < d.n) tile[q][threadIdx.x] = src[(size_t)(sys < d.nb ? sys : 0) * d.n + i];
+    }
+    __syncthreads();
+    for (int q = threadIdx.y; q < 32; q += BY) {  // q: row within the tile
+      const int i = i0 + q;
+      if (i < d.n) dst[IL(d, i, g * 32 + threadIdx.x)] = tile[threadIdx.x][q];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_b_from_il(DevPlan d, const double *__restrict__ src,
+                                                   double *__restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int g = blockIdx.y;
+  for (int i0 = blockIdx.x * 32; i0 < d.n; i0 += gridDim.x * 32) {
+    for (int q = threadIdx.y; q < 32; q += BY) {
+      const int i = i0 + q;
+      if (i < d.n) tile[q][threadIdx.x] = src[IL(d, i, g * 32 + threadIdx.x)];
+    }
+    __syncthreads();
+    for (int q = threadIdx.y; q < 32; q += BY) {
+      const int sys = g * 32 + q, i = i0 + threadIdx.x;
+      if (sys < d.nb && i < d.n) dst[(size_t)sys * d.n + i] = tile[threadIdx.x][q];
+    }
+    __syncthreads();
+  }
+}
+
+// dst[i][s] = src[i] for every system (initial factors of the first factorization)
+__global__ void k_b_broadcast(const double *__restrict__ src, int64_t count, int nbp,
+                              double *__restrict__ dst) {
+  const int64_t total = count * nbp;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total;
+       f += (int64_t)gridDim.x * blockDim.x)
+    dst[f] = src[f / nbp];
+}
+
+cudaError_t b_launch_broadcast(const double *src, int64_t count, int nbp, double *dst, cudaStream_t s) {
+  if (count) k_b_broadcast<<<4 * 148, 256, 0, s>>>(src, count, nbp, dst);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------
+// launchers
+// ----------------------------------------------------------------------------
+static dim3 row_grid(const DevPlan &d, int per_group) {
+  const int rows = (d.n + BY - 1) / BY;
+  return dim3((unsigned)max(1, min(rows, per_group)), (unsigned)(d.nbp >> 5));
+}
+static const dim3 ROW_BLOCK(32, BY);
+
+cudaError_t b_configure(size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm) {
+  const int sm = (int)refactor_smem;
+  cudaError_t e = cudaFuncSetAttribute(k_b_refactor, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  // the occupancy is shared-memory bound: ask for the largest carveout
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_b_refactor, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(refactor_blocks_per_sm, k_b_refactor, 32 * B_WARPS, sm);
+  int a = 0, b = 0;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_b_trsv_grid<false>, 256, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_b_trsv_grid<true>, 256, 0);
+  *trsv_blocks_per_sm = a < b ? a : b;
+  return e;
+}
+
+cudaError_t b_launch_expand_norms(const DevPlan &d, cudaStream_t s) {
+  if (d.n) k_b_expand_norms<<<row_grid(d, 8 * 148 / (d.nbp >> 5) + 1), ROW_BLOCK, 0, s>>>(d);
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, cudaStream_t s, long long *launches) {
+  if (!d.n) return cudaSuccess;
+  // (KKT_NO_RESET=1, diagnostics only: keep the previous factors so no task ever waits)
+  static const bool no_reset = std::getenv("KKT_NO_RESET") != nullptr;
+  cudaError_t e = no_reset ? cudaSuccess : cudaMemsetAsync(d.Lx, 0xFF, 8 * (size_t)d.nnz_L * d.nbp, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d.ticket, 0, 4, s);
+  if (e != cudaSuccess) return e;
+  for (int l = 0; l < d.n_small_levels; ++l) {
+    const int b = d.lev_ptr[l], en = d.lev_ptr[l + 1];
+    if (en > b) {
+      const int rows = (en - b + BY - 1) / BY;
+      const dim3 grid((unsigned)max(1, min(rows, 8 * 148 / (d.nbp >> 5) + 1)), (unsigned)(d.nbp >> 5));
+      k_b_refactor_small<<<grid, ROW_BLOCK, 0, s>>>(d, b, en);
+      ++*launches;
+    }
+  }
+  if (d.n_btask) {
+    if (d.prof) cudaMemsetAsync(d.prof, 0, 8 * 8 * (size_t)blocks * B_WARPS, s);
+    k_b_refactor<<<blocks, 32 * B_WARPS, smem, s>>>(d);
+    ++*launches;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_diag_stats(const DevPlan &d, cudaStream_t s) {
+  if (d.n) k_b_diag_stats<<<row_grid(d, 4 * 148 / (d.nbp >> 5) + 1), ROW_BLOCK, 0, s>>>(d);
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_spmv(const DevPlan &d, const double *x, double *out, const double *bsub,
+                          double *nrm_partials, cudaStream_t s) {
+  k_b_spmv<<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, x, out, bsub, nrm_partials);
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_resid_stats(const DevPlan &d, const double *r, const double *x,
+                                 double *partials, double *out5, cudaStream_t s) {
+  k_b_resid_stats<<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, r, x, partials);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_b_resid_final<<<dim3(5, d.nbp), 32, 0, s>>>(partials, d.rb, out5);
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_to_il(const DevPlan &d, const double *src, double *dst, cudaStream_t s) {
+  if (d.n) k_b_to_il<<<dim3((unsigned)min((d.n + 31) / 32, 1184), d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, src, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_from_il(const DevPlan &d, const double *src, double *dst, cudaStream_t s) {
+  if (d.n) k_b_from_il<<<dim3((unsigned)min((d.n + 31) / 32, 1184), d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, src, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_dots(const DevPlan &d, const double *V, int nvec, const double *w,
+                          const int *mask, double *partials, cudaStream_t s) {
+  k_b_dots<<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, V, nvec, w, mask, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_cgs(const DevPlan &d, const double *V, int nvec, const double *w_in,
+                         const double *h, int hstride, double *w_out, int mode, const int *mask,
+                         double *partials, cudaStream_t s) {
+  k_b_cgs<<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, V, nvec, w_in, h, hstride, w_out, mode, mask,
+                                                       partials);
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_scale(const DevPlan &d, const double *in, double *out, const double *den,
+                           int dstride, const int *mask, cudaStream_t s) {
+  k_b_scale<<<row_grid(d, 4 * 148 / (d.nbp >> 5) + 1), ROW_BLOCK, 0, s>>>(d, in, out, den, dstride, mask);
+  return cudaGetLastError();
+}
+
+cudaError_t b_launch_update_x(const DevPlan &d, double *x, const double *Z, const double *y,
+                              int ystride, const int *jused, cudaStream_t s) {
+  k_b_update_x<<<row_grid(d, 4 * 148 / (d.nbp >> 5) + 1), ROW_BLOCK, 0, s>>>(d, x, Z, y, ystride, jused);
+  return cudaGetLastError();
+}
+
+}  // namespace kkt

@@ -54,6 +54,36 @@ static void destroy(Device *dev) {
   delete dev;
 }
 
+// Batched refactor tasks (k_b_refactor): for every column past the thread-per-column levels
+// (DAG-level order), chunks of S systems.  S trades coalescing (lanes over systems) against
+// the per-column critical path (lanes over entries): the workspace x[np][S] must fit the
+// per-warp budget, and heavy columns (many update pairs) get more entry lanes.
+// KKT_B_SCHED="lo,mid,hi" overrides the pair thresholds for S <= 8 / 4 / 1.
+static int build_batch_tasks(const HostPlan &h, int nbp, int xbudget, std::vector<int2> &tasks) {
+  int lo = 64, mid = 256, hi = 1024;
+  if (const char *e = std::getenv("KKT_B_SCHED")) std::sscanf(e, "%d,%d,%d", &lo, &mid, &hi);
+  const int start = h.small_lev_ptr[h.n_small_levels];
+  tasks.clear();
+  for (int c = start; c < h.n; ++c) {
+    const int j = h.col_order[c];
+    const int64_t np = (h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j]);
+    if (np > xbudget)
+      return set_error(KKT_ERR_BAD_SHAPE, "column pattern too large for the batched workspace");
+    int64_t pairs = 0;
+    for (int64_t t = h.so_ptr[j]; t < h.so_ptr[j + 1]; ++t) pairs += h.so_meta[4 * t + 1];
+    int S = 32;
+    while (S > 1 && np * S > xbudget) S >>= 1;
+    if (pairs > hi) S = 1;
+    else if (pairs > mid) S = std::min(S, 4);
+    else if (pairs > lo) S = std::min(S, 8);
+    int lg = 0;
+    while ((1 << lg) < S) ++lg;
+    for (int s0 = 0; s0 < nbp; s0 += S) tasks.push_back(make_int2(j, (s0 << 8) | lg));
+  }
+  if (tasks.size() >= (size_t)INT32_MAX) return set_error(KKT_ERR_BAD_SHAPE, "too many batched tasks");
+  return KKT_OK;
+}
+
 static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int64_t in_nnz,
                   const int64_t *gen_src, const kkt_device_opts *opts, Device *&out) {
   out = nullptr;
@@ -67,10 +97,11 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   dev->device = opts ? opts->device : 0;
   dev->restart_m = (opts && opts->restart_m > 0) ? opts->restart_m : 10;
   const int nb = (opts && opts->batch > 1) ? opts->batch : 1;
-  if (nb > 64) {
+  if (nb > 4096) {
     delete dev;
-    return set_error(KKT_ERR_BAD_ARG, "batch must be <= 64");
+    return set_error(KKT_ERR_BAD_ARG, "batch must be <= 4096");
   }
+  const int nbp = nb > 1 ? (nb + 31) / 32 * 32 : 1;  // interleaved width (batch.cu)
   cudaError_t ce = cudaSetDevice(dev->device);
   if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&dev->stream, cudaStreamNonBlocking);
   if (ce != cudaSuccess) {
@@ -81,7 +112,21 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   DevPlan &d = dev->d;
   d.n = h.n;
   d.nb = nb;
-  d.rb = std::max(8, RED_BLOCKS / nb);  // reduction blocks per system
+  d.nbp = nbp;
+  d.rb = nb == 1 ? RED_BLOCKS : std::max(8, RED_BLOCKS / (nbp / 32));  // blocks per group
+  std::vector<int2> btask;
+  d.b_xbudget = B_XBUDGET;
+  d.b_stage = B_STAGE;  // doubles per stage buffer (two buffers per warp)
+  if (const char *e = std::getenv("KKT_B_SMEM")) std::sscanf(e, "%d,%d", &d.b_xbudget, &d.b_stage);
+  d.b_xbudget = std::max(d.b_xbudget, h.maxpat);
+  if (nb > 1) {
+    int rc2 = build_batch_tasks(h, nbp, d.b_xbudget, btask);
+    if (rc2 != KKT_OK) {
+      delete dev;
+      return rc2;
+    }
+  }
+  d.n_btask = (int)btask.size();
   d.sym_lower = 0;
   d.has_lower = h.has_lower;
   d.nnz_a = h.nnz_a;
@@ -95,20 +140,22 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.n_small_levels = h.n_small_levels;
   for (int l = 0; l <= h.n_small_levels; ++l) d.lev_ptr[l] = h.small_lev_ptr[l];
   d.ref_start = h.small_lev_ptr[h.n_small_levels];
-  d.poll_ns = std::getenv("KKT_POLL_NS") ? std::atoi(std::getenv("KKT_POLL_NS")) : 0;
+  d.poll_ns = std::getenv("KKT_POLL_NS") ? std::atoi(std::getenv("KKT_POLL_NS")) : (nbp > 1 ? 256 : 0);
   d.pL = h.pL;
   d.pU = h.pU;
   d.nLg = (int)h.L_grid_order.size();
+  d.L_nsync = (int)h.L_sync_ptr.size() - 1;
+  for (int l = 0; l <= d.L_nsync; ++l) d.L_sync_ptr[l] = h.L_sync_ptr[l];
   d.nUg = (int)h.U_grid_order.size();
   d.sweep_maxL = h.sweep_maxL;
   d.sweep_maxU = h.sweep_maxU;
-  const size_t n = (size_t)h.n, B = (size_t)nb;
+  const size_t n = (size_t)h.n, B = (size_t)nbp;
   const size_t in_cap = (size_t)std::max(d.in_nnz, d.nnz_a);
   d.in_cap = (int64_t)in_cap;
   size_t bytes = 0;
   auto acc = [&](size_t b) { bytes += align_up(b + 1); };
   acc(4 * (n + 1)); acc(4 * d.nnz_a); acc(4 * n); acc(4 * d.nnz_a);  // A_rp ci split gen_src
-  acc(8 * in_cap * B); acc(8 * d.nnz_a * B);                         // in_vals A_vals
+  acc(8 * in_cap * nb); acc(8 * d.nnz_a * B);                        // in_vals A_vals
   acc(4 * (n + 1)); acc(4 * (n + 1)); acc(4 * d.n_ap); acc(4 * n);   // so_ptr ap_ptr a_src order
   acc(4 * (n + 1)); acc(4 * (n + 1)); acc(4 * d.nnz_L); acc(4 * d.nnz_U);  // Lp Up Lmap Umap
   acc(4 * d.n_upd); acc(16 * d.n_so); acc(2 * d.n_upd); acc(2 * d.n_ap);   // lidx meta slots
@@ -122,6 +169,12 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   acc(4 * h.Ltail_split.size()); acc(8 * h.Ltail_split.size() * B);        // split, tacc
   acc(8 * d.nnz_L * B); acc(8 * d.nnz_U * B); acc(8 * n * B); acc(8 * n * B);  // Lv Uv yL yU
   acc(8 * SCAL_STRIDE * B); acc(64); acc(8 * 8 * (size_t)d.rb * B);        // scal ticket partials
+  acc(8 * btask.size());                                                   // batched tasks
+  for (const HostSweep *hs : {&h.swL, &h.swU}) {
+    acc(4 * hs->dptr.size()); acc(4 * hs->dsrc.size()); acc(2 * hs->ddst.size());
+    acc(4 * hs->dmask.size()); acc(4 * hs->bptr.size()); acc(4 * hs->brow.size());
+    acc(4 * hs->bbeg.size()); acc(4 * hs->bcnt.size()); acc(4 * hs->bofs.size());
+  }
   ce = cudaMalloc(&dev->arena, bytes);
   if (ce != cudaSuccess) {
     destroy(dev);
@@ -133,7 +186,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.A_ci = carve<int>(cur, d.nnz_a);
   d.A_split = carve<int>(cur, n);
   d.gen_src = carve<int>(cur, d.nnz_a);
-  d.in_vals = carve<double>(cur, in_cap * B);
+  d.in_vals = carve<double>(cur, in_cap * nb);
   d.A_vals = carve<double>(cur, d.nnz_a * B);
   d.so_ptr = carve<int>(cur, n + 1);
   d.ap_ptr = carve<int>(cur, n + 1);
@@ -174,6 +227,24 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.scal = carve<unsigned long long>(cur, SCAL_STRIDE * B);
   d.ticket = carve<int>(cur, 16);
   d.partials = carve<double>(cur, 8 * (size_t)d.rb * B);
+  d.btask = carve<int2>(cur, btask.size());
+  {
+    const HostSweep *hs[2] = {&h.swL, &h.swU};
+    SweepDev *sd[2] = {&d.swL, &d.swU};
+    for (int k = 0; k < 2; ++k) {
+      sd[k]->nblk = hs[k]->nblk;
+      sd[k]->dptr = carve<int>(cur, hs[k]->dptr.size());
+      sd[k]->dsrc = carve<int>(cur, hs[k]->dsrc.size());
+      sd[k]->ddst = carve<uint16_t>(cur, hs[k]->ddst.size());
+      sd[k]->dmask = carve<unsigned>(cur, hs[k]->dmask.size());
+      sd[k]->bptr = carve<int>(cur, hs[k]->bptr.size());
+      sd[k]->brow = carve<int>(cur, hs[k]->brow.size());
+      sd[k]->bbeg = carve<int>(cur, hs[k]->bbeg.size());
+      sd[k]->bcnt = carve<int>(cur, hs[k]->bcnt.size());
+      sd[k]->bofs = carve<int>(cur, hs[k]->bofs.size());
+      sd[k]->max_stage = hs[k]->max_stage;
+    }
+  }
   d.trace_ref = d.trace_trsv = d.trace_step = nullptr;
   if (std::getenv("KKT_TRACE") && std::atoi(std::getenv("KKT_TRACE")) > 0) {
     const size_t tb = 4 * 8 * n + 8 * (size_t)d.n_so;
@@ -197,7 +268,14 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   UP(d.Up, to_i32(h.Up));
   UP(d.Lmap, h.Lmap);
   UP(d.Umap, h.Umap);
-  UP(d.upd_lidx, h.upd_lidx);
+  if (nbp > 1) {  // the batched replay derives L indices from the step metadata
+    d.upd_slot32 = d.upd_lidx;
+    d.upd_lidx = nullptr;
+    const std::vector<int> slot32 = narrow<uint16_t, int>(h.upd_slot);
+    UP(d.upd_slot32, slot32);
+  } else {
+    UP(d.upd_lidx, h.upd_lidx);
+  }
   UP(d.so_meta, h.so_meta);
   UP(d.upd_slot, h.upd_slot);
   UP(d.a_slot, h.a_slot);
@@ -217,30 +295,72 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   UP(d.Li, h.Li32);
   UP(d.Ui, h.Ui32);
   UP(d.Ltail_split, h.Ltail_split);
-  // the first factorization's values, so solve() works before any refactor (LuFactors)
-  UP(d.Lx, h.Lx0);
-  UP(d.Ux, h.Ux0);
-  UP(d.udiag, h.Udiag0);
+  UP(d.btask, btask);
+  UP(d.swL.dptr, h.swL.dptr); UP(d.swL.dsrc, h.swL.dsrc); UP(d.swL.ddst, h.swL.ddst);
+  UP(d.swL.dmask, h.swL.dmask); UP(d.swL.bptr, h.swL.bptr); UP(d.swL.brow, h.swL.brow);
+  UP(d.swL.bbeg, h.swL.bbeg); UP(d.swL.bcnt, h.swL.bcnt); UP(d.swL.bofs, h.swL.bofs);
+  UP(d.swU.dptr, h.swU.dptr); UP(d.swU.dsrc, h.swU.dsrc); UP(d.swU.ddst, h.swU.ddst);
+  UP(d.swU.dmask, h.swU.dmask); UP(d.swU.bptr, h.swU.bptr); UP(d.swU.brow, h.swU.brow);
+  UP(d.swU.bbeg, h.swU.bbeg); UP(d.swU.bcnt, h.swU.bcnt); UP(d.swU.bofs, h.swU.bofs);
+  // the first factorization's values, so solve() works before any refactor (LuFactors);
+  // a batch starts every system from them (broadcast into the interleaved layout)
   {
     std::vector<double> lv(h.nnz_L), uv(h.nnz_U);
     for (int64_t p = 0; p < h.nnz_L; ++p) lv[h.Lmap[p]] = h.Lx0[p];
     for (int64_t p = 0; p < h.nnz_U; ++p) uv[h.Umap[p]] = h.Ux0[p];
-    UP(d.Lv, lv);
-    UP(d.Uv, uv);
-    CUDA_TRY(cudaStreamSynchronize(dev->stream));
-  }
-  for (size_t q = 1; q < B; ++q) {  // every system starts from the first factorization
-    CUDA_TRY(cudaMemcpyAsync(d.Lx + q * d.nnz_L, d.Lx, 8 * d.nnz_L, cudaMemcpyDeviceToDevice, dev->stream));
-    CUDA_TRY(cudaMemcpyAsync(d.Ux + q * d.nnz_U, d.Ux, 8 * d.nnz_U, cudaMemcpyDeviceToDevice, dev->stream));
-    CUDA_TRY(cudaMemcpyAsync(d.Lv + q * d.nnz_L, d.Lv, 8 * d.nnz_L, cudaMemcpyDeviceToDevice, dev->stream));
-    CUDA_TRY(cudaMemcpyAsync(d.Uv + q * d.nnz_U, d.Uv, 8 * d.nnz_U, cudaMemcpyDeviceToDevice, dev->stream));
-    CUDA_TRY(cudaMemcpyAsync(d.udiag + q * n, d.udiag, 8 * n, cudaMemcpyDeviceToDevice, dev->stream));
+    if (nbp == 1) {
+      UP(d.Lx, h.Lx0);
+      UP(d.Ux, h.Ux0);
+      UP(d.udiag, h.Udiag0);
+      UP(d.Lv, lv);
+      UP(d.Uv, uv);
+      CUDA_TRY(cudaStreamSynchronize(dev->stream));
+    } else {
+      const size_t mx = std::max<size_t>({(size_t)h.nnz_L, (size_t)h.nnz_U, n, 1});
+      double *tmp = nullptr;
+      ce = cudaMalloc(&tmp, 8 * mx);
+      if (ce != cudaSuccess) {
+        destroy(dev);
+        return set_error(KKT_ERR_OOM, "cudaMalloc of the upload buffer failed");
+      }
+      struct Arr { const std::vector<double> *v; double *dst; } arrs[5] = {
+          {&h.Lx0, d.Lx}, {&h.Ux0, d.Ux}, {&h.Udiag0, d.udiag}, {&lv, d.Lv}, {&uv, d.Uv}};
+      for (auto &a : arrs) {
+        if (a.v->empty()) continue;
+        ce = cudaMemcpyAsync(tmp, a.v->data(), 8 * a.v->size(), cudaMemcpyHostToDevice, dev->stream);
+        if (ce == cudaSuccess) ce = b_launch_broadcast(tmp, (int64_t)a.v->size(), nbp, a.dst, dev->stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(dev->stream);
+        if (ce != cudaSuccess) break;
+      }
+      cudaFree(tmp);
+      if (ce != cudaSuccess) {
+        destroy(dev);
+        return set_error(KKT_ERR_CUDA, std::string("initial factors: ") + cudaGetErrorString(ce));
+      }
+    }
   }
   CUDA_TRY(launch_fill_sentinel(d.yL, (int64_t)(n * B), dev->stream));
   CUDA_TRY(launch_fill_sentinel(d.yU, (int64_t)(n * B), dev->stream));
   CUDA_TRY(cudaMemsetAsync(d.scal, 0, 8 * SCAL_STRIDE * B, dev->stream));
   CUDA_TRY(cudaMemsetAsync(d.ticket, 0, 64, dev->stream));
   // launch shapes
+  CUDA_TRY(sweep_configure());
+  if (nbp > 1) {
+    int rbps = 0, tbps = 0;
+    dev->refactor_smem = b_refactor_smem(d.b_xbudget, d.b_stage);
+    CUDA_TRY(b_configure(dev->refactor_smem, &rbps, &tbps));
+    dev->refactor_warps = B_WARPS;
+    if (d.trace_step) d.prof = d.trace_step;  // per-warp cycle counters
+    dev->refactor_blocks = std::max(1, rbps) * dev->sm_count;
+    dev->trsv_blocks = std::max(1, tbps) * dev->sm_count;
+    dev->pinned_bytes = 64 * 1024 + 64 * (size_t)nbp;
+    CUDA_TRY(cudaMallocHost(&dev->pinned, dev->pinned_bytes));
+    rc = alloc_krylov(dev, dev->restart_m);
+    if (rc != KKT_OK) return rc;
+    CUDA_TRY(cudaStreamSynchronize(dev->stream));
+    out = dev;
+    return KKT_OK;
+  }
   dev->refactor_warps = 8;
   dev->refactor_smem = refactor_smem_bytes(dev->refactor_warps, d.maxpat);
   while (dev->refactor_smem > 200 * 1024 && dev->refactor_warps > 1) {
@@ -279,7 +399,7 @@ static int set_values(Device *dev, const double *vals, int layout, int on_device
                              (size_t)d.nb, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                              dev->stream));
   LAUNCH(launch_reset_scal(d, 0, dev->stream));
-  LAUNCH(launch_expand_norms(d, dev->stream));
+  LAUNCH(d.nbp > 1 ? b_launch_expand_norms(d, dev->stream) : launch_expand_norms(d, dev->stream));
   return KKT_OK;
 }
 
@@ -289,11 +409,14 @@ static int refactor(Device *dev, const double *vals, int layout, int on_device, 
   if (rc != KKT_OK) return rc;
   LAUNCH(launch_reset_scal(d, 1, dev->stream));  // min |u_jj| starts at +inf
   {
-    cudaError_t e = launch_refactor(d, dev->refactor_blocks, dev->refactor_warps, dev->refactor_smem,
-                                    dev->stream, &dev->launches);
+    cudaError_t e = d.nbp > 1
+                        ? b_launch_refactor(d, dev->refactor_blocks, dev->refactor_smem, dev->stream,
+                                            &dev->launches)
+                        : launch_refactor(d, dev->refactor_blocks, dev->refactor_warps,
+                                          dev->refactor_smem, dev->stream, &dev->launches);
     if (e != cudaSuccess) return set_error(KKT_ERR_CUDA, std::string("refactor: ") + cudaGetErrorString(e));
   }
-  LAUNCH(launch_diag_stats(d, dev->sm_count, dev->stream));
+  LAUNCH(d.nbp > 1 ? b_launch_diag_stats(d, dev->stream) : launch_diag_stats(d, dev->sm_count, dev->stream));
   if (diag_out) {  // [nb][4] = {max|u|, min|u|, patched, growth}
     CUDA_TRY(cudaMemcpyAsync(dev->pinned, d.scal, 8 * SCAL_STRIDE * (size_t)d.nb, cudaMemcpyDeviceToHost,
                              dev->stream));
@@ -314,13 +437,15 @@ static int refactor(Device *dev, const double *vals, int layout, int on_device, 
 }
 
 int dev_solve(Device *dev, const double *b, double *x) {
-  cudaError_t e = launch_trsv(dev->d, b, x, dev->trsv_blocks, dev->stream, &dev->launches);
+  cudaError_t e = dev->d.nbp > 1 ? b_launch_trsv(dev->d, b, x, dev->trsv_blocks, dev->stream, &dev->launches)
+                                 : launch_trsv(dev->d, b, x, dev->trsv_blocks, dev->stream, &dev->launches);
   if (e != cudaSuccess) return set_error(KKT_ERR_CUDA, std::string("trisolve: ") + cudaGetErrorString(e));
   return KKT_OK;
 }
 
 int dev_spmv(Device *dev, const double *x, double *y, const double *bsub, double *nrm_partials) {
-  LAUNCH(launch_spmv(dev->d, x, y, bsub, nrm_partials, dev->stream));
+  LAUNCH(dev->d.nbp > 1 ? b_launch_spmv(dev->d, x, y, bsub, nrm_partials, dev->stream)
+                        : launch_spmv(dev->d, x, y, bsub, nrm_partials, dev->stream));
   return KKT_OK;
 }
 
@@ -328,8 +453,9 @@ int dev_spmv(Device *dev, const double *x, double *y, const double *bsub, double
 int dev_residual_norms(Device *dev, const double *r, const double *x, double *out6) {
   DevPlan &d = dev->d;
   const size_t nb = (size_t)d.nb;
-  double *out5 = d.partials + 5 * (size_t)d.rb * nb;  // after the [nb][5][rb] partials
-  LAUNCH(launch_resid_stats(d, r, x, d.partials, out5, dev->stream));
+  double *out5 = d.partials + 5 * (size_t)d.rb * d.nbp;  // after the [nbp][5][rb] partials
+  LAUNCH(d.nbp > 1 ? b_launch_resid_stats(d, r, x, d.partials, out5, dev->stream)
+                   : launch_resid_stats(d, r, x, d.partials, out5, dev->stream));
   dev->launches++;
   CUDA_TRY(cudaMemcpyAsync(dev->pinned, out5, 8 * 5 * nb, cudaMemcpyDeviceToHost, dev->stream));
   CUDA_TRY(cudaMemcpyAsync(dev->pinned + 5 * nb, d.scal, 8 * SCAL_STRIDE * nb, cudaMemcpyDeviceToHost,
@@ -508,6 +634,21 @@ int kkt_dev_download_factors(kkt_device *d, double *Lx, double *Ux, double *Udia
   const size_t nb = (size_t)p.nb;
   cudaStream_t s = dev->stream;
   cudaError_t e = cudaSuccess;
+  if (p.nbp > 1) {  // interleaved [entry][nbp] -> caller [nb][entry]
+    const size_t nbp = (size_t)p.nbp;
+    struct Arr { const double *src; double *dst; size_t cnt; } arrs[3] = {
+        {p.Lx, Lx, (size_t)p.nnz_L}, {p.Ux, Ux, (size_t)p.nnz_U}, {p.udiag, Udiag, (size_t)p.n}};
+    for (auto &a : arrs) {
+      if (!a.dst || !a.cnt) continue;
+      std::vector<double> tmp(a.cnt * nbp);
+      e = cudaMemcpyAsync(tmp.data(), a.src, 8 * tmp.size(), cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
+      for (size_t q = 0; q < nb; ++q)
+        for (size_t i = 0; i < a.cnt; ++i) a.dst[q * a.cnt + i] = tmp[i * nbp + q];
+    }
+    return KKT_OK;
+  }
   if (Lx && p.nnz_L) e = cudaMemcpyAsync(Lx, p.Lx, 8 * (size_t)p.nnz_L * nb, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && Ux && p.nnz_U)
     e = cudaMemcpyAsync(Ux, p.Ux, 8 * (size_t)p.nnz_U * nb, cudaMemcpyDeviceToHost, s);
@@ -518,10 +659,32 @@ int kkt_dev_download_factors(kkt_device *d, double *Lx, double *Ux, double *Udia
   return KKT_OK;
 }
 
+// Batched handles keep vectors interleaved internally; the ABI takes [nb][n] and converts
+// through the handle's staging vectors.
+#define IL_IN(src, dst)                                                                   \
+  do {                                                                                    \
+    cudaError_t _e = kkt::b_launch_to_il(dev->d, src, dst, dev->stream);                  \
+    dev->launches++;                                                                      \
+    if (_e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(_e));   \
+  } while (0)
+#define IL_OUT(src, dst)                                                                  \
+  do {                                                                                    \
+    cudaError_t _e = kkt::b_launch_from_il(dev->d, src, dst, dev->stream);                \
+    dev->launches++;                                                                      \
+    if (_e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(_e));   \
+  } while (0)
+
 int kkt_dev_solve(kkt_device *d, const double *b_dev, double *x_dev) {
   Device *dev = reinterpret_cast<Device *>(d);
   if (!dev || !b_dev || !x_dev) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
   cudaSetDevice(dev->device);
+  if (dev->d.nbp > 1) {
+    IL_IN(b_dev, dev->kry->w);
+    int rc = kkt::dev_solve(dev, dev->kry->w, dev->kry->w1);
+    if (rc) return rc;
+    IL_OUT(dev->kry->w1, x_dev);
+    return KKT_OK;
+  }
   return kkt::dev_solve(dev, b_dev, x_dev);
 }
 
@@ -529,6 +692,13 @@ int kkt_dev_spmv(kkt_device *d, const double *x_dev, double *y_dev) {
   Device *dev = reinterpret_cast<Device *>(d);
   if (!dev || !x_dev || !y_dev) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
   cudaSetDevice(dev->device);
+  if (dev->d.nbp > 1) {
+    IL_IN(x_dev, dev->kry->w);
+    int rc = kkt::dev_spmv(dev, dev->kry->w, dev->kry->w1, nullptr, nullptr);
+    if (rc) return rc;
+    IL_OUT(dev->kry->w1, y_dev);
+    return KKT_OK;
+  }
   return kkt::dev_spmv(dev, x_dev, y_dev, nullptr, nullptr);
 }
 
@@ -536,6 +706,11 @@ int kkt_dev_residual_norms(kkt_device *d, const double *r_dev, const double *x_d
   Device *dev = reinterpret_cast<Device *>(d);
   if (!dev || !r_dev || !x_dev || !out_host) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
   cudaSetDevice(dev->device);
+  if (dev->d.nbp > 1) {
+    IL_IN(r_dev, dev->kry->w);
+    IL_IN(x_dev, dev->kry->w1);
+    return kkt::dev_residual_norms(dev, dev->kry->w, dev->kry->w1, out_host);
+  }
   return kkt::dev_residual_norms(dev, r_dev, x_dev, out_host);
 }
 
@@ -545,19 +720,25 @@ int kkt_dev_fgmres(kkt_device *d, const double *b_dev, const double *x0_dev, dou
   if (!dev || !b_dev || !x0_dev || !x_dev || !cfg || !rep)
     return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
   cudaSetDevice(dev->device);
+  if (dev->d.nbp > 1) {
+    kkt::Krylov &K = *dev->kry;
+    IL_IN(b_dev, K.sr);
+    IL_IN(x0_dev, K.sx0);
+    int rc = kkt::dev_fgmres(dev, K.sr, K.sx0, K.sx, cfg, rep, history_host, hist_cap, nullptr);
+    if (rc) return rc;
+    IL_OUT(K.sx, x_dev);
+    return KKT_OK;
+  }
   return kkt::dev_fgmres(dev, b_dev, x0_dev, x_dev, cfg, rep, history_host, hist_cap, nullptr);
 }
 
 // refine_fgmres for every system of the handle (refine.py:103-132): per-system trigger
 // ||r - K x0||_2 > delta ||r||_2; untriggered systems return x0; the triggered ones run
 // FGMRES(tol = delta) together.
-int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_dev, double *x_dev,
-                          const kkt_krylov_cfg *cfg, kkt_krylov_report *rep) {
-  Device *dev = reinterpret_cast<Device *>(d);
-  if (!dev || !r_dev || !x0_dev || !x_dev || !cfg || !rep)
-    return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
+// (vectors in the handle's native layout)
+static int refine_native(Device *dev, const double *r_dev, const double *x0_dev, double *x_dev,
+                         const kkt_krylov_cfg *cfg, kkt_krylov_report *rep) {
   if (!(cfg->delta_tol > 0)) return kkt::set_error(KKT_ERR_BAD_ARG, "delta_tol must be positive");
-  cudaSetDevice(dev->device);
   const int nb = dev->d.nb;
   std::vector<double> st(6 * (size_t)nb);
   int rc = kkt::dev_residual_norms(dev, r_dev, x0_dev, st.data());
@@ -575,8 +756,8 @@ int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_d
       std::memset(&rep[q], 0, sizeof rep[q]);
       rep[q].converged = 1;
     }
-    cudaError_t e = cudaMemcpyAsync(x_dev, x0_dev, 8 * (size_t)dev->d.n * nb, cudaMemcpyDeviceToDevice,
-                                    dev->stream);
+    cudaError_t e = cudaMemcpyAsync(x_dev, x0_dev, 8 * (size_t)dev->d.n * dev->d.nbp,
+                                    cudaMemcpyDeviceToDevice, dev->stream);
     if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
     return KKT_OK;
   }
@@ -590,6 +771,24 @@ int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_d
   return rc;
 }
 
+int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_dev, double *x_dev,
+                          const kkt_krylov_cfg *cfg, kkt_krylov_report *rep) {
+  Device *dev = reinterpret_cast<Device *>(d);
+  if (!dev || !r_dev || !x0_dev || !x_dev || !cfg || !rep)
+    return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
+  cudaSetDevice(dev->device);
+  if (dev->d.nbp > 1) {
+    kkt::Krylov &K = *dev->kry;
+    IL_IN(r_dev, K.sr);
+    IL_IN(x0_dev, K.sx0);
+    int rc = refine_native(dev, K.sr, K.sx0, K.sx, cfg, rep);
+    if (rc) return rc;
+    IL_OUT(K.sx, x_dev);
+    return KKT_OK;
+  }
+  return refine_native(dev, r_dev, x0_dev, x_dev, cfg, rep);
+}
+
 int kkt_dev_step(kkt_device *d, const double *values_in, int layout, const double *r_in,
                  double *x_out, int io_on_device, const kkt_krylov_cfg *cfg, kkt_krylov_report *rep,
                  double *diag_out) {
@@ -600,20 +799,33 @@ int kkt_dev_step(kkt_device *d, const double *values_in, int layout, const doubl
   int rc = kkt::refactor(dev, values_in, layout, io_on_device, diag_out);
   if (rc) return rc;
   kkt::Krylov &K = *dev->kry;
-  const size_t bytes = 8 * (size_t)dev->d.n * dev->d.nb;
+  const bool il = dev->d.nbp > 1;
+  const size_t bytes = 8 * (size_t)dev->d.n * dev->d.nb;  // caller layout [nb][n]
   const double *r_dev = r_in;
-  if (!io_on_device) {
-    cudaError_t e = cudaMemcpyAsync(K.sr, r_in, bytes, cudaMemcpyHostToDevice, dev->stream);
+  cudaError_t e = cudaSuccess;
+  if (!io_on_device) {  // H2D into the (system-major) staging vector
+    double *dst = il ? K.w : K.sr;
+    e = cudaMemcpyAsync(dst, r_in, bytes, cudaMemcpyHostToDevice, dev->stream);
     if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
+    r_dev = dst;
+  }
+  if (il) {
+    IL_IN(r_dev, K.sr);
     r_dev = K.sr;
   }
   rc = kkt::dev_solve(dev, r_dev, K.sx0);  // x0 = lu_solve(r)      (harness.py:234)
   if (rc) return rc;
-  rc = kkt_dev_refine_fgmres(d, r_dev, K.sx0, K.sx, cfg, rep);  // (harness.py:240)
+  rc = refine_native(dev, r_dev, K.sx0, K.sx, cfg, rep);  // (harness.py:240)
   if (rc) return rc;
-  cudaError_t e = cudaMemcpyAsync(x_out, K.sx, bytes,
-                                  io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                                  dev->stream);
+  const double *xs = K.sx;
+  if (il) {
+    double *dst = io_on_device ? x_out : K.w;
+    IL_OUT(K.sx, dst);
+    xs = dst;
+  }
+  if (xs != x_out)
+    e = cudaMemcpyAsync(x_out, xs, bytes, io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                        dev->stream);
   if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
   e = cudaStreamSynchronize(dev->stream);
   if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));

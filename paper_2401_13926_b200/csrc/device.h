@@ -19,10 +19,27 @@ constexpr double PATCH_RELATIVE_FLOOR = 1e-12;   // direct_lu.py:32
 constexpr int REFACTOR_STAGE = 512;              // update pairs staged per warp chunk
 constexpr int SCAL_STRIDE = 16;                  // per-system scalar block
 
+// Blocked tail sweep tables (HostSweep, plan.h)
+struct SweepDev {
+  int nblk = 0, max_stage = 0;
+  int *dptr = nullptr, *dsrc = nullptr, *bptr = nullptr, *brow = nullptr, *bbeg = nullptr,
+      *bcnt = nullptr, *bofs = nullptr;
+  uint16_t *ddst = nullptr;
+  unsigned *dmask = nullptr;
+};
+
 // Device-side view of the plan + workspaces.  int32 indices on the device.
 struct DevPlan {
   int n = 0, sym_lower = 0, has_lower = 0;
   int nb = 1;   // systems held
+  // nb > 1: per-system arrays are INTERLEAVED [entry][nbp] (nbp = nb rounded up to 32; the
+  // padding systems replicate system 0), so one warp serves 32 systems with coalesced
+  // 256-byte accesses and SIMT-uniform control flow (batch.cu).  nb == 1: nbp == 1.
+  int nbp = 1;
+  int2 *btask = nullptr;  // batched refactor tasks {column, sys0 << 8 | log2(systems)}
+  int n_btask = 0;
+  int b_xbudget = 0, b_stage = 0;  // per-warp shared workspace / stage (doubles), k_b_refactor
+  unsigned long long *prof = nullptr;  // optional per-warp cycle counters (KKT_TRACE, batched)
   int rb = RED_BLOCKS;  // reduction blocks per system
   int64_t nnz_a = 0, in_nnz = 0, in_cap = 0, nnz_L = 0, nnz_U = 0, n_so = 0, n_upd = 0, n_ap = 0;
   int maxpat = 1;
@@ -37,6 +54,7 @@ struct DevPlan {
   int *so_ptr, *ap_ptr, *a_src, *col_order, *Lp, *Up, *Lmap, *Umap, *upd_lidx;
   int4 *so_meta;
   uint16_t *upd_slot, *a_slot;
+  int *upd_slot32 = nullptr;               // batched: int32 slots (in the upd_lidx buffer)
   double *Lx, *Ux, *udiag;                  // [nb][nnz_L], [nb][nnz_U], [nb][n]
   // trisolves (pattern/schedule shared)
   int *Lrp, *Lci, *Urp, *Uci, *row_perm, *col_perm;
@@ -44,7 +62,9 @@ struct DevPlan {
   int *L_crit, *U_crit, *Uhead_off, *Li, *Ui, *Ltail_split;
   double *tacc;                             // [nb][n - pL] tail partial sums (grid -> sweep)
   int pL, pU, nLg, nUg;                     // split positions and grid-phase row counts
+  int L_nsync = 0, L_sync_ptr[5] = {0, 0, 0, 0, 0};  // level-synchronous leading L levels
   int sweep_maxL, sweep_maxU;
+  SweepDev swL, swU;                        // blocked sweeps of the trailing blocks
   double *Lv, *Uv;                          // [nb][nnz_L], [nb][nnz_U] (CSR order)
   double *yL, *yU;                          // [nb][n] sentinel-reset (value == readiness)
   // optional timeline (KKT_TRACE=1), system 0 only
@@ -57,6 +77,10 @@ struct DevPlan {
   // solve yL is all-sentinel and yU published, which is exactly the state a solve expects.
   const int *sys_mask = nullptr;
 };
+
+__host__ __device__ __forceinline__ size_t IL(const DevPlan &d, int64_t i, int sys) {
+  return (size_t)i * d.nbp + sys;
+}
 
 __device__ __forceinline__ bool sys_active(const DevPlan &d, int sys) {
   return d.sys_mask == nullptr || d.sys_mask[sys] != 0;
@@ -108,7 +132,44 @@ size_t refactor_smem_bytes(int warps, int maxpat);
 cudaError_t launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,
                         cudaStream_t s, long long *launches);
 cudaError_t trsv_configure(int *grid_blocks_per_sm);
+// L phase up to the sweep (row-parallel leading levels, sync-free grid, tail partial sums)
+cudaError_t launch_L_front(const DevPlan &d, const double *b, double *x, int grid_blocks, cudaStream_t s,
+                           long long *launches);
+cudaError_t b_launch_grid_L(const DevPlan &d, const double *b, double *x, int grid_blocks, cudaStream_t s);
 cudaError_t launch_fill_sentinel(double *p, int64_t n, cudaStream_t s);
+// blocked sweep of the trailing block (sweep.cu), single and batched handles
+cudaError_t sweep_configure();
+cudaError_t launch_sweep_blocked(const DevPlan &d, bool upper, double *x, cudaStream_t s);
+
+// ---- batched (interleaved, nb > 1) kernels: batch.cu ----
+constexpr int B_XBUDGET = 768;   // default refactor workspace doubles per warp (np * systems)
+constexpr int B_STAGE = 256;     // default stage buffer doubles (pairs * systems), x2 buffers
+constexpr int B_WARPS = 4;       // warps per refactor CTA
+size_t b_refactor_smem(int xbudget, int stage);
+cudaError_t b_configure(size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm);
+cudaError_t b_launch_expand_norms(const DevPlan &d, cudaStream_t s);
+cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, cudaStream_t s, long long *launches);
+cudaError_t b_launch_diag_stats(const DevPlan &d, cudaStream_t s);
+cudaError_t b_launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,
+                          cudaStream_t s, long long *launches);
+cudaError_t b_launch_spmv(const DevPlan &d, const double *x, double *out, const double *bsub,
+                          double *nrm_partials, cudaStream_t s);
+cudaError_t b_launch_resid_stats(const DevPlan &d, const double *r, const double *x,
+                                 double *partials, double *out5, cudaStream_t s);
+// [nb][n] (system-major, caller layout) <-> [n][nbp] (interleaved); padding <- system 0
+cudaError_t b_launch_to_il(const DevPlan &d, const double *src, double *dst, cudaStream_t s);
+cudaError_t b_launch_from_il(const DevPlan &d, const double *src, double *dst, cudaStream_t s);
+cudaError_t b_launch_broadcast(const double *src, int64_t count, int nbp, double *dst, cudaStream_t s);
+// FGMRES vector kernels on interleaved [n][nbp] vectors (partials [nbp][nvec][rb])
+cudaError_t b_launch_dots(const DevPlan &d, const double *V, int nvec, const double *w,
+                          const int *mask, double *partials, cudaStream_t s);
+cudaError_t b_launch_cgs(const DevPlan &d, const double *V, int nvec, const double *w_in,
+                         const double *h, int hstride, double *w_out, int mode, const int *mask,
+                         double *partials, cudaStream_t s);
+cudaError_t b_launch_scale(const DevPlan &d, const double *in, double *out, const double *den,
+                           int dstride, const int *mask, cudaStream_t s);
+cudaError_t b_launch_update_x(const DevPlan &d, double *x, const double *Z, const double *y,
+                              int ystride, const int *jused, cudaStream_t s);
 
 // vectors are [nb][n]; partials are [nb][nvec][rb]; out is [nb][nvec]
 cudaError_t launch_spmv(const DevPlan &d, const double *x, double *out, const double *bsub,

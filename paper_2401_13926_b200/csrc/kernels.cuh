@@ -66,6 +66,19 @@ __device__ __forceinline__ double wait_value_backoff(const double *p) {
   return v;
 }
 
+// Back-off poll for batched kernels, where hundreds of warps can be waiting at once: a tight
+// spin from every waiter saturates L2 and slows the very producers being waited on.
+__device__ __forceinline__ double wait_value_bo(const double *p, int cap_ns) {
+  double v = ld_relaxed_f64(p);
+  unsigned ns = 32;
+  while (is_sentinel(v)) {
+    __nanosleep(ns);
+    ns = ns < (unsigned)cap_ns ? 2 * ns : (unsigned)cap_ns;
+    v = ld_relaxed_f64(p);
+  }
+  return v;
+}
+
 // ---- cp.async (LDGSTS) helpers for shared-memory prefetch rings ----------------------
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);

@@ -192,7 +192,7 @@ int alloc_krylov(Device *dev, int m) {
   Krylov *K = new Krylov();
   K->m = m;
   K->n = dev->d.n;
-  const size_t n = (size_t)dev->d.n, nb = (size_t)dev->d.nb, rb = (size_t)dev->d.rb;
+  const size_t n = (size_t)dev->d.n, nb = (size_t)dev->d.nbp, rb = (size_t)dev->d.rb;
   size_t bytes = align_up(8 * (m + 1) * nb * n + 1) + align_up(8 * m * nb * n + 1) +
                  7 * align_up(8 * nb * n + 1);
   bytes += 6 * align_up(8 * nb * (m + 1) + 1) + align_up(8 * nb * (m + 1) * m + 1);
@@ -240,8 +240,12 @@ static int read_block(Device *dev, const double *src, size_t count) {
   return KKT_OK;
 }
 
+// per-system int flags [nb] -> device [nbp] (padding systems are never active).  A pageable
+// source: cudaMemcpyAsync has consumed it when it returns.
 static int upload_mask(Device *dev, const std::vector<int> &mask, int *dst) {
-  CUDA_TRY(cudaMemcpyAsync(dst, mask.data(), 4 * mask.size(), cudaMemcpyHostToDevice, dev->stream));
+  std::vector<int> pad(dev->d.nbp, 0);
+  for (size_t q = 0; q < mask.size() && q < pad.size(); ++q) pad[q] = mask[q];
+  CUDA_TRY(cudaMemcpyAsync(dst, pad.data(), 4 * pad.size(), cudaMemcpyHostToDevice, dev->stream));
   return KKT_OK;
 }
 
@@ -264,7 +268,8 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
     ~MaskGuard() { d.sys_mask = nullptr; }
   } guard{d};
   cudaStream_t s = dev->stream;
-  const size_t nbn = (size_t)nb * n;
+  const size_t nbn = (size_t)d.nbp * n;
+  const bool il = d.nbp > 1;
   std::vector<int> hn(nb, 0), active(nb, 1), running(nb, 0), jused(nb, 0);
   std::vector<double> beta(nb, 0.0), target(nb, 0.0), est(nb, 0.0);
   std::vector<int> iters(nb, 0), converged(nb, 0), restarts(nb, 0);
@@ -326,7 +331,8 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
     }
     if (!any) break;
     if ((rc = upload_mask(dev, running, K.mask))) return rc;
-    LAUNCH((k_scale<<<dim3(G, nb), T, 0, s>>>(K.r, K.V, n, K.beta, 1, K.mask), cudaGetLastError()));
+    LAUNCH(il ? b_launch_scale(d, K.r, K.V, K.beta, 1, K.mask, s)
+              : (k_scale<<<dim3(G, nb), T, 0, s>>>(K.r, K.V, n, K.beta, 1, K.mask), cudaGetLastError()));
     LAUNCH((k_cycle_init<<<nb, 128, 0, s>>>(K.g, K.H, M, K.beta, K.mask, d.scal), cudaGetLastError()));
     std::vector<int> cycle(running);
     for (int j = 0; j < m; ++j) {
@@ -341,14 +347,23 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
       d.sys_mask = nullptr;
       const int nv = j + 1;
       // cgs2_step (:93-105): h1 = V^T w; w1 = w - V h1; h2 = V^T w1; w2 = w1 - V h2
-      LAUNCH((k_dots<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w, K.mask, K.partials), cudaGetLastError()));
-      LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h1, M + 1, 0, s));
-      LAUNCH((k_cgs<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w, K.h1, M + 1, K.w1, 0, K.mask, nullptr),
-              cudaGetLastError()));
-      LAUNCH((k_dots<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w1, K.mask, K.partials), cudaGetLastError()));
-      LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h2, M + 1, 0, s));
-      LAUNCH((k_cgs<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w1, K.h2, M + 1, K.w, 1, K.mask, K.partials),
-              cudaGetLastError()));
+      if (il) {
+        LAUNCH(b_launch_dots(d, K.V, nv, K.w, K.mask, K.partials, s));
+        LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h1, M + 1, 0, s));
+        LAUNCH(b_launch_cgs(d, K.V, nv, K.w, K.h1, M + 1, K.w1, 0, K.mask, nullptr, s));
+        LAUNCH(b_launch_dots(d, K.V, nv, K.w1, K.mask, K.partials, s));
+        LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h2, M + 1, 0, s));
+        LAUNCH(b_launch_cgs(d, K.V, nv, K.w1, K.h2, M + 1, K.w, 1, K.mask, K.partials, s));
+      } else {
+        LAUNCH((k_dots<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w, K.mask, K.partials), cudaGetLastError()));
+        LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h1, M + 1, 0, s));
+        LAUNCH((k_cgs<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w, K.h1, M + 1, K.w1, 0, K.mask, nullptr),
+                cudaGetLastError()));
+        LAUNCH((k_dots<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w1, K.mask, K.partials), cudaGetLastError()));
+        LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h2, M + 1, 0, s));
+        LAUNCH((k_cgs<<<dim3(G, nb), T, 0, s>>>(K.V, nb, nv, n, K.w1, K.h2, M + 1, K.w, 1, K.mask, K.partials),
+                cudaGetLastError()));
+      }
       LAUNCH(launch_reduce_partials(d, K.partials, 1, K.nrm, 1, 0, s));
       LAUNCH((k_givens<<<nb, 32, 0, s>>>(K.st, j, M, K.h1, K.h2, K.nrm, K.H, K.cs, K.sn, K.g, K.status,
                                          K.mask, d.scal),
@@ -374,15 +389,17 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
       if (j + 1 < m) {
         if (changed && (rc = upload_mask(dev, running, K.mask))) return rc;
         // V_{j+1} = w / hj1 for the systems still running
-        LAUNCH((k_scale<<<dim3(G, nb), T, 0, s>>>(K.w, K.V + (size_t)(j + 1) * nbn, n, K.status + 2, 4,
-                                                  K.mask),
-                cudaGetLastError()));
+        LAUNCH(il ? b_launch_scale(d, K.w, K.V + (size_t)(j + 1) * nbn, K.status + 2, 4, K.mask, s)
+                  : (k_scale<<<dim3(G, nb), T, 0, s>>>(K.w, K.V + (size_t)(j + 1) * nbn, n, K.status + 2, 4,
+                                                       K.mask),
+                     cudaGetLastError()));
       }
     }
     // y = R^{-1} g; x += Z y; r = b - K x; beta = ||r||                      (:189-192)
-    CUDA_TRY(cudaMemcpyAsync(K.jused, jused.data(), 4 * nb, cudaMemcpyHostToDevice, s));
+    if ((rc = upload_mask(dev, jused, K.jused))) return rc;
     LAUNCH((k_solve_upper<<<nb, 32, 0, s>>>(K.H, M, K.g, K.jused, K.yv), cudaGetLastError()));
-    LAUNCH((k_update_x<<<dim3(G, nb), T, 0, s>>>(K.x, K.Z, nb, n, K.yv, M + 1, K.jused), cudaGetLastError()));
+    LAUNCH(il ? b_launch_update_x(d, K.x, K.Z, K.yv, M + 1, K.jused, s)
+              : (k_update_x<<<dim3(G, nb), T, 0, s>>>(K.x, K.Z, nb, n, K.yv, M + 1, K.jused), cudaGetLastError()));
     if ((rc = upload_mask(dev, cycle, K.mask))) return rc;
     d.sys_mask = K.mask;
     if ((rc = dev_spmv(dev, K.x, K.r, b, K.partials))) return rc;

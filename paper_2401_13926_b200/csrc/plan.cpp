@@ -26,6 +26,63 @@ static std::vector<int32_t> order_by_level(const std::vector<int32_t> &lev) {
   return out;
 }
 
+// L: blocks ascend from p (rows r >= block end receive the off-diagonal updates);
+// U: blocks descend from n (rows p <= r < block start receive them).  CSR rows are column-
+// ascending for L and column-descending for U, so each row's entries inside a block are one
+// contiguous run, already in the reference's per-row order.
+static void build_sweep(const HostPlan &P, bool upper, HostSweep &H) {
+  const int32_t n = P.n, p = upper ? P.pU : P.pL, T = n - p;
+  const std::vector<int32_t> &rp = upper ? P.Urp : P.Lrp, &ci = upper ? P.Uci : P.Lci;
+  H = HostSweep();
+  H.nblk = (T + 31) / 32;
+  H.dptr.assign(1, 0);
+  H.bptr.assign(1, 0);
+  H.dmask.assign((size_t)H.nblk * 32, 0u);
+  for (int32_t c = 0; c < H.nblk; ++c) {
+    int32_t lo, w;
+    if (!upper) {
+      lo = p + 32 * c;
+      w = std::min(32, n - lo);
+    } else {
+      const int32_t hi = n - 32 * c;
+      lo = std::max(p, hi - 32);
+      w = hi - lo;
+    }
+    auto run = [&](int32_t r, int32_t &beg, int32_t &cnt) {  // entries of row r in [lo, lo+w)
+      beg = rp[r];
+      while (beg < rp[r + 1] && !(ci[beg] >= lo && ci[beg] < lo + w)) ++beg;
+      cnt = 0;
+      while (beg + cnt < rp[r + 1] && ci[beg + cnt] >= lo && ci[beg + cnt] < lo + w) ++cnt;
+    };
+    for (int32_t i = 0; i < w; ++i) {
+      int32_t beg, cnt;
+      run(lo + i, beg, cnt);
+      for (int32_t k = 0; k < cnt; ++k) {
+        const int32_t t = ci[beg + k] - lo;
+        H.dsrc.push_back(beg + k);
+        H.ddst.push_back((uint16_t)(i * 32 + t));
+        H.dmask[(size_t)c * 32 + i] |= 1u << t;
+      }
+    }
+    H.dptr.push_back((int32_t)H.dsrc.size());
+    const int32_t r0 = upper ? p : lo + w, r1 = upper ? lo : n;
+    int32_t staged = 0;
+    for (int32_t r = r0; r < r1; ++r) {
+      int32_t beg, cnt;
+      run(r, beg, cnt);
+      if (cnt) {
+        H.brow.push_back(r);
+        H.bbeg.push_back(beg);
+        H.bcnt.push_back(cnt);
+        H.bofs.push_back(staged);  // position of the run in the block's shared-memory stage
+        staged += cnt;
+      }
+    }
+    H.max_stage = std::max(H.max_stage, staged);
+    H.bptr.push_back((int32_t)H.brow.size());
+  }
+}
+
 int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int64_t in_nnz,
                const int64_t *gen_src, HostPlan &P) {
   const int64_t n = S.n;
@@ -206,22 +263,30 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     const int TL = choose_tail(P, false), TU = choose_tail(P, true);
     P.pL = (int32_t)(n - TL);
     P.pU = (int32_t)(n - TU);
-    // L grid phase: the rows < pL, plus, for every tail row, its leading entries (columns
-    // < pL) as a partial row whose result seeds the sweep (level = 1 + max level used).
+    // L grid phase: the rows < pL.  Every tail row's leading entries (columns < pL) are
+    // summed by a separate row-parallel launch after it (nothing in the grid waits on them),
+    // whose result seeds the sweep.
     std::vector<int32_t> lg(levL.begin(), levL.begin() + P.pL);
     P.Ltail_split.assign(n - P.pL, 0);
     for (int64_t r = P.pL; r < n; ++r) {
-      int32_t q = P.Lrp[r], l = 0;
-      while (q < P.Lrp[r + 1] && P.Lci[q] < P.pL) l = std::max(l, levL[P.Lci[q++]] + 1);
+      int32_t q = P.Lrp[r];
+      while (q < P.Lrp[r + 1] && P.Lci[q] < P.pL) ++q;
       P.Ltail_split[r - P.pL] = q;
-      lg.push_back(l);
     }
-    P.L_grid_order = order_by_level(lg);  // indices >= pL are the tail partial rows
+    P.L_grid_order = order_by_level(lg);
+    P.L_grid_levels = 0;
+    for (int32_t l : lg) P.L_grid_levels = std::max(P.L_grid_levels, l + 1);
+    // wide leading levels (>= 4096 rows, at most 4) run level-synchronously, row-parallel
+    {
+      std::vector<int64_t> cnt(P.L_grid_levels + 1, 0);
+      for (int32_t l : lg) cnt[l]++;
+      P.L_sync_ptr.assign(1, 0);
+      for (int32_t l = 0; l < P.L_grid_levels && l < 4 && cnt[l] >= 4096; ++l)
+        P.L_sync_ptr.push_back(P.L_sync_ptr.back() + (int32_t)cnt[l]);
+    }
     std::vector<int32_t> lt(levL.begin() + P.pL, levL.end());
     P.L_tail_order = order_by_level(lt);
     for (auto &v : P.L_tail_order) v += P.pL;
-    P.L_grid_levels = 0;
-    for (int32_t l : lg) P.L_grid_levels = std::max(P.L_grid_levels, l + 1);
     // U: head rows [pU, n) keep their levels; grid rows' levels ignore head dependencies
     std::vector<int32_t> uh(levU.begin() + P.pU, levU.end());
     P.U_head_order = order_by_level(uh);
@@ -241,8 +306,7 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     for (size_t i = 0; i < P.L_grid_order.size(); ++i) {
       const int32_t r = P.L_grid_order[i];
       int32_t best = -1, bl = -1;
-      const int32_t qend = r >= P.pL ? P.Ltail_split[r - P.pL] : P.Lrp[r + 1];
-      for (int32_t q = P.Lrp[r]; q < qend; ++q) {
+      for (int32_t q = P.Lrp[r]; q < P.Lrp[r + 1]; ++q) {
         const int32_t c = P.Lci[q];
         if (levL[c] > bl || (levL[c] == bl && c > best)) {
           bl = levL[c];
@@ -278,6 +342,8 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
                                        (int32_t)(S.Up[j + 1] - S.Up[j] - P.Uhead_off[j - P.pU]));
     P.Li32.assign(S.Li.begin(), S.Li.end());
     P.Ui32.assign(S.Ui.begin(), S.Ui.end());
+    build_sweep(P, false, P.swL);
+    build_sweep(P, true, P.swU);
   }
   P.Lx0.assign(S.Lx.begin(), S.Lx.end());
   P.Ux0.assign(S.Ux.begin(), S.Ux.end());

@@ -9,6 +9,18 @@
 
 namespace kkt {
 
+// Blocked sweep of the dense trailing block (sweep.cu): 32-column blocks in processing
+// order.  Per block: the diagonal-triangle entries (CSR index -> tile position i*32+t) with a
+// per-row presence mask, and the off-diagonal row segments (row, first CSR index, count)
+// whose entries fall in the block's columns.
+struct HostSweep {
+  int32_t nblk = 0;
+  int32_t max_stage = 0;  // largest number of off-diagonal entries of one block
+  std::vector<int32_t> dptr, dsrc, bptr, brow, bbeg, bcnt, bofs;
+  std::vector<uint16_t> ddst;
+  std::vector<uint32_t> dmask;
+};
+
 struct HostPlan {
   int32_t n = 0;
   int64_t nnz_a = 0, in_nnz = 0, nnz_L = 0, nnz_U = 0;
@@ -36,6 +48,8 @@ struct HostPlan {
   // U: rows [pU, n) one CTA first (head), rows [0, pU) grid-wide.  Row orders by level.
   int32_t pL = 0, pU = 0, L_grid_levels = 0, U_grid_levels = 0;
   std::vector<int32_t> L_grid_order, L_tail_order, U_head_order, U_grid_order;
+  // L_grid_order offsets of the leading levels run level-synchronously (L_sync_ptr.size()-1)
+  std::vector<int32_t> L_sync_ptr;
   // per grid-order index: the row's critical (highest-level) grid dependency, or -1
   std::vector<int32_t> L_crit, U_crit;
   // per head column j >= pU: offset in U(:,j) (CSC, rows ascending) of the first row >= pU
@@ -43,6 +57,7 @@ struct HostPlan {
   std::vector<int32_t> Li32, Ui32;  // CSC row indices (int32) for the sweep phase
   std::vector<int32_t> Ltail_split;  // tail row r: CSR index of its first entry >= pL
   int32_t sweep_maxL = 0, sweep_maxU = 0;  // longest column inside each sweep block
+  HostSweep swL, swU;
 };
 
 // Tunables of the phase split (env KKT_TAIL_ROWS / KKT_HEAD_ROWS override the model).

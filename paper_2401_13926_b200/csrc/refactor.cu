@@ -172,11 +172,26 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
               if (lane + 32 * q < cnt) st_l[off + lane + 32 * q] = lv[q];
             for (int e = lane + 256; e < cnt; e += 32) st_l[off + e] = ld_relaxed_f64(&Lx[lbk + e]);
           }
-          for (int e = lane; e < cnt; e += 32) {
-            double l = st_l[off + e];
-            if (is_sentinel(l)) l = wait_value(&Lx[lbk + e]);  // rare: store not yet visible
-            const int s = st_s[off + e];
-            x[s] = __dsub_rn(x[s], __dmul_rn(l, xk));
+          // the targets of one step are distinct slots: 4 RMWs per lane in flight
+          for (int e0 = lane; e0 < cnt; e0 += 128) {
+            double lv[4], xv[4];
+            int sl[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (e0 + 32 * q < cnt) {
+                lv[q] = st_l[off + e0 + 32 * q];
+                sl[q] = st_s[off + e0 + 32 * q];
+              }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (e0 + 32 * q < cnt) xv[q] = x[sl[q]];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (e0 + 32 * q < cnt) {
+                double l = lv[q];
+                if (is_sentinel(l)) l = wait_value(&Lx[lbk + e0 + 32 * q]);  // rare: not yet visible
+                x[sl[q]] = __dsub_rn(xv[q], __dmul_rn(l, xk));
+              }
           }
           if (d.trace_step && sys == 0 && lane == 0)
             d.trace_step[t0 + i] = globaltimer() | (mm ? 1ull : 0ull);
@@ -345,7 +360,7 @@ __global__ void k_reset_scal(unsigned long long *scal, int nb, int mode) {
 }
 
 cudaError_t launch_reset_scal(const DevPlan &d, int mode, cudaStream_t s) {
-  k_reset_scal<<<1, 64, 0, s>>>(d.scal, d.nb, mode);
+  k_reset_scal<<<1, 64, 0, s>>>(d.scal, d.nbp, mode);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,248 @@
+// Blocked sweep over the dense trailing block of the triangular solves (direct_lu.py:359-379),
+// for the single-system and the batched interleaved handles (S systems per CTA).
+//
+// The reference sweeps columns one at a time; every row accumulates its updates in column
+// order (ascending for L, descending for U) with separately rounded products.  Here the
+// block's columns are taken 32 at a time:
+//   phase A (one warp per system): the 32x32 diagonal triangle as a register chain — lane i
+//     owns row lo+i; at step t lane t's value is final (y_t; for U after the division by
+//     u_tt) and is broadcast with one shuffle, and every lane holding L(i,t) / U(i,t)
+//     subtracts its product.  The triangle's values were prefetched into shared memory with
+//     cp.async while the previous block ran.
+//   phase B (all threads): every later row with entries in the block's columns applies them
+//     in its CSR order from the block's y values in shared memory.
+// Per row the subtractions therefore happen in exactly the reference's order (bitwise), but
+// the sweep costs one shuffle chain step per column and two CTA barriers per 32 columns,
+// instead of one barrier per column.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "device.h"
+#include "kernels.cuh"
+
+namespace kkt {
+
+constexpr int BS_THREADS = 256;
+
+template <bool IS_U, int S, bool STAGED>
+__global__ void __launch_bounds__(BS_THREADS) k_trsv_blocked(DevPlan d, double *__restrict__ xout) {
+  extern __shared__ double sm[];
+  const SweepDev &sw = IS_U ? d.swU : d.swL;
+  const int sys0 = blockIdx.x * S;
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < S; ++q) any |= sys_active(d, sys0 + q);
+  if (!any) return;  // uniform over the CTA (inactive systems of an active CTA are harmless:
+                     // they replay their previous solve's tail from their own state)
+  const int p = IS_U ? d.pU : d.pL;
+  const int T = d.n - p;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double *acc = sm;                          // [T][S]
+  double *tile = acc + (size_t)T * S;        // [2][32*32][S]
+  double *yb = tile + 2 * 1024 * S;          // [32][S]
+  double *sv = yb + 32 * S;                  // [max_stage][S]   (STAGED)
+  int *scol = reinterpret_cast<int *>(sv + (size_t)sw.max_stage * S);  // [max_stage]
+  const double *vals = IS_U ? d.Uv : d.Lv;
+  const int *ci = IS_U ? d.Uci : d.Lci;
+  for (int f = tid; f < T * S; f += BS_THREADS) {
+    const int r = p + f / S, q = f % S, sys = sys0 + q;
+    if (IS_U) {
+      acc[f] = ldcg(&d.yL[IL(d, r, sys)]);  // L result of the head rows
+      d.yL[IL(d, r, sys)] = __longlong_as_double((long long)SENTINEL_BITS);  // next solve
+    } else {
+      acc[f] = ldcg(&d.tacc[IL(d, r - p, sys)]);  // b_perm - sum over columns < p (grid phase)
+      d.yU[IL(d, r, sys)] = __longlong_as_double((long long)SENTINEL_BITS);
+    }
+  }
+  auto issue_tile = [&](int c) {
+    if (c < sw.nblk) {
+      double *tl = tile + (size_t)(c & 1) * 1024 * S;
+      const int k0 = sw.dptr[c], k1 = sw.dptr[c + 1];
+      for (int f = tid; f < (k1 - k0) * S; f += BS_THREADS) {
+        const int k = k0 + f / S, q = f % S;
+        cp_async8(&tl[(size_t)sw.ddst[k] * S + q], &vals[IL(d, sw.dsrc[k], sys0 + q)]);
+      }
+    }
+    cp_async_commit();
+  };
+  issue_tile(0);
+  bool bad = false;
+  // optional timeline (KKT_TRACE, single system): per block {top, tiles ready, y ready, end}
+  unsigned long long *tr = (d.trace_trsv && blockIdx.x == 0 && tid == 0)
+                               ? d.trace_trsv + (IS_U ? (size_t)d.n : 0) + p : nullptr;
+#pragma unroll 1
+  for (int c = 0; c < sw.nblk; ++c) {
+    if (tr) tr[4 * c] = globaltimer();
+    int lo, w;
+    if (!IS_U) {
+      lo = p + 32 * c;
+      w = min(32, d.n - lo);
+    } else {
+      const int hi = d.n - 32 * c;
+      lo = max(p, hi - 32);
+      w = hi - lo;
+    }
+    // per-lane inputs of phase A, loaded before the barrier (independent of the chain)
+    const int s = warp;
+    const bool chain = warp < S;
+    unsigned mask = 0;
+    double piv = 1.0;
+    if (chain && lane < w) {
+      mask = sw.dmask[c * 32 + lane];
+      if (IS_U) piv = d.udiag[IL(d, lo + lane, sys0 + s)];
+    }
+    issue_tile(c + 1);
+    cp_async_wait<1>();  // this thread's copies of tile c have landed
+    __syncthreads();     // ... everyone's; and phase B of block c-1 is complete
+    if (tr) tr[4 * c + 1] = globaltimer();
+    const int b0 = sw.bptr[c], b1 = sw.bptr[c + 1];
+    if (STAGED && warp >= S) {  // the other warps stream the block's off-diagonal runs
+      for (int k = b0 + tid - 32 * S; k < b1; k += BS_THREADS - 32 * S) {
+        const int beg = sw.bbeg[k], cnt = sw.bcnt[k], o = sw.bofs[k];
+        for (int e = 0; e < cnt; ++e) {
+#pragma unroll
+          for (int q = 0; q < S; ++q) cp_async8(&sv[(size_t)(o + e) * S + q], &vals[IL(d, beg + e, sys0 + q)]);
+          cp_async4(&scol[o + e], &ci[beg + e]);
+        }
+      }
+    }
+    if (STAGED) cp_async_commit();
+    if (chain) {
+      // the lane's row of the diagonal triangle in registers, then a pure register chain
+      const double *tl = tile + (size_t)(c & 1) * 1024 * S;
+      double lrow[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) lrow[t] = ((mask >> t) & 1u) ? tl[(size_t)(lane * 32 + t) * S + s] : 0.0;
+      double a = lane < w ? acc[(size_t)(lo + lane - p) * S + s] : 0.0;
+      double y = 0.0;
+      if (!IS_U) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          if (t >= w) break;
+          const double yt = __shfl_sync(0xffffffffu, a, t);  // row lo+t is final
+          if ((mask >> t) & 1u) a = __dsub_rn(a, __dmul_rn(lrow[t], yt));
+        }
+        y = a;
+      } else {
+#pragma unroll
+        for (int t = 31; t >= 0; --t) {
+          if (t >= w) continue;
+          double yl = 0.0;
+          if (lane == t) yl = __ddiv_rn(a, piv);  // y_t = acc_t / u_tt
+          const double yt = __shfl_sync(0xffffffffu, yl, t);
+          if (lane == t) y = yt;
+          if ((mask >> t) & 1u) a = __dsub_rn(a, __dmul_rn(lrow[t], yt));
+        }
+      }
+      if (tr) tr[4 * c + 2] = globaltimer();
+      if (lane < w) {
+        const int j = lo + lane, sys = sys0 + s;
+        yb[lane * S + s] = y;
+        if (IS_U) {
+          st_relaxed_f64(&d.yU[IL(d, j, sys)], unsentinel(y));
+          xout[IL(d, d.col_perm[j], sys)] = y;
+          if (!isfinite(y)) bad = true;
+        } else {
+          st_relaxed_f64(&d.yL[IL(d, j, sys)], unsentinel(y));
+        }
+      }
+    }
+    if (STAGED) cp_async_wait<0>();
+    __syncthreads();  // the block's y values (and staged runs) are in shared memory
+    // phase B: later rows (L: below the block; U: above it, inside the head) in CSR order
+    if (STAGED) {
+      for (int f = tid; f < (b1 - b0) * S; f += BS_THREADS) {
+        const int k = b0 + f / S, q = f % S;
+        const int r = sw.brow[k], cnt = sw.bcnt[k], o = sw.bofs[k];
+        double a = acc[(size_t)(r - p) * S + q];
+#pragma unroll 4
+        for (int e = 0; e < cnt; ++e)
+          a = __dsub_rn(a, __dmul_rn(sv[(size_t)(o + e) * S + q], yb[(scol[o + e] - lo) * S + q]));
+        acc[(size_t)(r - p) * S + q] = a;
+      }
+      if (tr) tr[4 * c + 3] = globaltimer();
+      continue;
+    }
+    for (int f = tid; f < (b1 - b0) * S; f += BS_THREADS) {
+      const int k = b0 + f / S, q = f % S, sys = sys0 + q;
+      const int r = sw.brow[k], beg = sw.bbeg[k], cnt = sw.bcnt[k];
+      double a = acc[(size_t)(r - p) * S + q];
+      for (int e0 = 0; e0 < cnt; e0 += 8) {
+        int cl[8];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e0 + u < cnt) {
+            cl[u] = ci[beg + e0 + u];
+            v[u] = vals[IL(d, beg + e0 + u, sys)];
+          }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e0 + u < cnt) a = __dsub_rn(a, __dmul_rn(v[u], yb[(cl[u] - lo) * S + q]));
+      }
+      acc[(size_t)(r - p) * S + q] = a;
+    }
+  }
+  cp_async_wait<0>();
+  if (IS_U && bad) atomicOr(&d.scal[(size_t)(sys0 + warp) * SCAL_STRIDE + SC_NONFINITE], 1ull);
+}
+
+constexpr size_t SMEM_CAP = 227 * 1024;
+
+static size_t blocked_smem(int T, int S, int stage) {
+  return ((size_t)T * S + 2 * 1024 * S + 32 * S + (size_t)stage * S) * sizeof(double) +
+         (size_t)stage * sizeof(int);
+}
+
+template <bool IS_U, int S, bool STAGED>
+static cudaError_t set_attr() {
+  return cudaFuncSetAttribute(k_trsv_blocked<IS_U, S, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)SMEM_CAP);
+}
+
+template <int S>
+static cudaError_t set_attrs() {
+  cudaError_t e = set_attr<false, S, false>();
+  if (e == cudaSuccess) e = set_attr<true, S, false>();
+  if (e == cudaSuccess) e = set_attr<false, S, true>();
+  if (e == cudaSuccess) e = set_attr<true, S, true>();
+  return e;
+}
+
+cudaError_t sweep_configure() {
+  cudaError_t e = set_attrs<1>();
+  if (e == cudaSuccess) e = set_attrs<2>();
+  if (e == cudaSuccess) e = set_attrs<4>();
+  return e;
+}
+
+// the staged variant when the largest block's runs fit in shared memory
+template <int S>
+static void launch_s(const DevPlan &d, bool upper, double *x, int T, cudaStream_t s) {
+  const SweepDev &sw = upper ? d.swU : d.swL;
+  static const bool no_stage = std::getenv("KKT_SWEEP_NOSTAGE") != nullptr;
+  const size_t st = blocked_smem(T, S, sw.max_stage);
+  if (!no_stage && st <= SMEM_CAP) {
+    if (upper) k_trsv_blocked<true, S, true><<<d.nbp / S, BS_THREADS, st, s>>>(d, x);
+    else k_trsv_blocked<false, S, true><<<d.nbp / S, BS_THREADS, st, s>>>(d, x);
+  } else {
+    const size_t sm = blocked_smem(T, S, 0);
+    if (upper) k_trsv_blocked<true, S, false><<<d.nbp / S, BS_THREADS, sm, s>>>(d, x);
+    else k_trsv_blocked<false, S, false><<<d.nbp / S, BS_THREADS, sm, s>>>(d, x);
+  }
+}
+
+cudaError_t launch_sweep_blocked(const DevPlan &d, bool upper, double *x, cudaStream_t s) {
+  const int T = d.n - (upper ? d.pU : d.pL);
+  if (T <= 0) return cudaSuccess;
+  // systems per CTA: one CTA per system spreads a batch over the SMs (the sweep is a chain
+  // of short steps, so parallel CTAs beat coalescing); KKT_SWEEP_S=2|4 packs more
+  static const int SB = std::getenv("KKT_SWEEP_S") ? std::atoi(std::getenv("KKT_SWEEP_S")) : 1;
+  if (d.nbp == 1 || SB <= 1) launch_s<1>(d, upper, x, T, s);
+  else if (SB == 2) launch_s<2>(d, upper, x, T, s);
+  else launch_s<4>(d, upper, x, T, s);
+  return cudaGetLastError();
+}
+
+}  // namespace kkt

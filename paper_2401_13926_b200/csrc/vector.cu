@@ -139,7 +139,7 @@ cudaError_t launch_spmv(const DevPlan &d, const double *x, double *out, const do
 
 cudaError_t launch_reduce_partials(const DevPlan &d, const double *partials, int nvec, double *out,
                                    int ostride, int op_sqrt, cudaStream_t s) {
-  k_reduce_partials<<<dim3(nvec, d.nb), 32, 0, s>>>(partials, nvec, d.rb, out, ostride, op_sqrt);
+  k_reduce_partials<<<dim3(nvec, d.nbp), 32, 0, s>>>(partials, nvec, d.rb, out, ostride, op_sqrt);
   return cudaGetLastError();
 }
 
