@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) k_b_refactor_small(DevPlan d, int begin, 
       const double xk = x[m.x];
       for (int e = 0; e < m.y; ++e) {
         const int s = d.upd_slot[m.z + e];
-        x[s] = __dsub_rn(x[s], __dmul_rn(ldcg(&d.Lx[IL(d, m.w + e, sys)]), xk));
+        x[s] = __dsub_rn(x[s], __dmul_rn(ldcg(lx_ptr(d, m.w + e, sys)), xk));
       }
     }
     for (int s = 0; s < nu; ++s) {
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256) k_b_refactor_small(DevPlan d, int begin, 
       gm = fmax(gm, fabs(v));
       const double l = unsentinel(__ddiv_rn(v, ujj));
       d.Lv[IL(d, d.Lmap[lb + s], sys)] = l;
-      d.Lx[IL(d, lb + s, sys)] = l;
+      *lx_ptr(d, lb + s, sys) = l;
     }
     d.udiag[IL(d, j, sys)] = ujj;
   }
@@ -156,20 +156,29 @@ size_t b_refactor_smem(int xbudget, int stage) {
     tmark = _t;                                                 \
   }
 
-// One chunk of replay steps whose update pairs fit a stage buffer.
+// One chunk of replay steps whose update pairs fit a stage buffer.  A step larger than the
+// stage is replayed in pieces (its targets are distinct slots and x[k] is not among them, so
+// any split of one step is exact).
 struct Chunk {
-  int t0, nsteps, npairs;
-  bool big;   // a single step larger than the stage: replayed straight from global memory
+  int t0, e0, nsteps, npairs;  // e0: first entry of step t0 (pieces of a large step)
+  int next_t0, next_e0;
   int4 m;     // this lane's step metadata {slot of k, |L(:,k)|, first pair, first L index}
   int incl;   // inclusive prefix of the pair counts
 };
 
-__device__ __forceinline__ Chunk chunk_meta(const DevPlan &d, int t0, int t_end, int stp, int lane) {
+__device__ __forceinline__ Chunk chunk_meta(const DevPlan &d, int t0, int e0, int t_end, int stp,
+                                            int lane) {
   Chunk c;
   c.t0 = t0;
+  c.e0 = e0;
   const int t = t0 + lane;
   c.m = make_int4(0, 0, 0, 0);
   if (t < t_end) c.m = d.so_meta[t];
+  if (lane == 0) {  // resume inside step t0
+    c.m.y -= e0;
+    c.m.z += e0;
+    c.m.w += e0;
+  }
   c.incl = c.m.y;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -177,9 +186,20 @@ __device__ __forceinline__ Chunk chunk_meta(const DevPlan &d, int t0, int t_end,
     if (lane >= o) c.incl += v;
   }
   c.nsteps = __popc(__ballot_sync(FULL, t < t_end && c.incl <= stp));
-  c.big = c.nsteps == 0;
-  if (c.big) c.nsteps = 1;
-  c.npairs = c.big ? 0 : __shfl_sync(FULL, c.incl, c.nsteps - 1);
+  if (c.nsteps == 0) {  // step t0 alone exceeds the stage: take a piece of stp entries
+    if (lane == 0) {
+      c.m.y = stp;
+      c.incl = stp;
+    }
+    c.nsteps = 1;
+    c.npairs = stp;
+    c.next_t0 = t0;
+    c.next_e0 = e0 + stp;
+  } else {
+    c.npairs = __shfl_sync(FULL, c.incl, c.nsteps - 1);
+    c.next_t0 = t0 + c.nsteps;
+    c.next_e0 = 0;
+  }
   return c;
 }
 
@@ -188,12 +208,12 @@ __device__ __forceinline__ Chunk chunk_meta(const DevPlan &d, int t0, int t_end,
 __device__ __forceinline__ void chunk_issue(const DevPlan &d, const Chunk &c, double *stv, int *sts,
                                             int lgS, int sys0, int lane) {
   const int S = 1 << lgS;
-  for (int i = 0; i < c.nsteps && !c.big; ++i) {
+  for (int i = 0; i < c.nsteps; ++i) {
     const int cnt = __shfl_sync(FULL, c.m.y, i);
     const int off = __shfl_sync(FULL, c.incl - c.m.y, i);
     const int lbk = __shfl_sync(FULL, c.m.w, i);
     for (int f = lane; f < (cnt << lgS); f += 32)
-      cp_async8(&stv[(off << lgS) + f], &d.Lx[IL(d, lbk + (f >> lgS), sys0 + (f & (S - 1)))]);
+      cp_async8(&stv[(off << lgS) + f], lx_ptr(d, lbk + (f >> lgS), sys0 + (f & (S - 1))));
   }
   const int pair0 = __shfl_sync(FULL, c.m.z, 0);
   for (int p = lane; p < c.npairs; p += 32) cp_async4(&sts[p], &d.upd_slot32[pair0 + p]);
@@ -235,12 +255,19 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
   long long tmark = prof ? clock64() : 0;
   // The next task's descriptor is fetched while the current one runs (the dispatch chain
   // ticket -> task -> column pointers is four dependent global round trips).
-  int ticket = 0;
-  if (lane == 0) ticket = atomicAdd(d.ticket, 1);
+  // d.b_static: warp w takes tasks w, w + W, ... (no shared ticket; all warps are resident,
+  // so the smallest unfinished task is always at the head of its warp's sequence)
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  int ticket = gw;
+  if (!d.b_static && lane == 0) ticket = atomicAdd(d.ticket, 1);
   TaskInfo nt = load_task(d, __shfl_sync(FULL, ticket, 0));
+  int cur_task = __shfl_sync(FULL, ticket, 0);
   while (nt.j >= 0) {
     const TaskInfo ti = nt;
-    if (lane == 0) ticket = atomicAdd(d.ticket, 1);
+    const long long t_task = prof ? clock64() : 0;
+    const int my_task = cur_task;
+    if (d.b_static) ticket += nw;
+    else if (lane == 0) ticket = atomicAdd(d.ticket, 1);
     const int j = ti.j, lgS = ti.lgS, sys0 = ti.sys0;
     const int S = 1 << lgS, E = 32 >> lgS;
     const int s = lane & (S - 1), e = lane >> lgS;
@@ -250,7 +277,7 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
     const int stp = STG >> lgS;  // pairs per stage buffer
     const int t_end = ti.t_end;
     // first chunk in flight before the A scatter
-    Chunk cur = chunk_meta(d, ti.t0, t_end, stp, lane);
+    Chunk cur = chunk_meta(d, ti.t0, 0, t_end, stp, lane);
     int buf = 0;
     chunk_issue(d, cur, stv0, sts0, lgS, sys0, lane);
     PROF_MARK(0);
@@ -261,16 +288,17 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
     for (int q = ti.a0 + e; q < ti.a1; q += E)
       x[d.a_slot[q] * S + s] = d.A_vals[IL(d, d.a_src[q], sys)];
     __syncwarp();
-    nt = load_task(d, __shfl_sync(FULL, ticket, 0));  // consumed next iteration
+    cur_task = __shfl_sync(FULL, ticket, 0);
+    nt = load_task(d, cur_task);  // consumed next iteration
     PROF_MARK(1);
     // for k in so(j) (topological): x[Li(k)] -= Lx(k) * x[k]                  (:324-326)
     while (cur.t0 < t_end) {
       // the next chunk's loads overlap this chunk's replay (double-buffered stage)
-      const int tn = cur.t0 + cur.nsteps;
+      const int tn = cur.next_t0;
       Chunk nxt;
       nxt.t0 = tn;
       if (tn < t_end) {
-        nxt = chunk_meta(d, tn, t_end, stp, lane);
+        nxt = chunk_meta(d, tn, cur.next_e0, t_end, stp, lane);
         chunk_issue(d, nxt, stv0 + (buf ^ 1) * STG, sts0 + (buf ^ 1) * STG, lgS, sys0, lane);
         if (prof && lane == 0) prof[7] += (unsigned long long)nxt.npairs << lgS;
         PROF_MARK(2);
@@ -282,44 +310,35 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
       PROF_MARK(3);
       const double *stv = stv0 + buf * STG;
       const int *sts = sts0 + buf * STG;
-      const int pair0 = __shfl_sync(FULL, cur.m.z, 0);
       for (int i = 0; i < cur.nsteps; ++i) {
         const int kslot = __shfl_sync(FULL, cur.m.x, i);
         const int cnt = __shfl_sync(FULL, cur.m.y, i);
         const int off = __shfl_sync(FULL, cur.incl - cur.m.y, i);
         const int lbk = __shfl_sync(FULL, cur.m.w, i);  // L(:,k) = Lx[lbk, lbk+cnt)
         const double xk = x[kslot * S + s];
-        if (!cur.big) {
-          // the targets of one step are distinct slots: 4 RMWs per lane in flight
-          for (int idx0 = e; idx0 < cnt; idx0 += 4 * E) {
-            double lv[4], xv[4];
-            int sl[4];
+        // the targets of one step are distinct slots: 4 RMWs per lane in flight
+        for (int idx0 = e; idx0 < cnt; idx0 += 4 * E) {
+          double lv[4], xv[4];
+          int sl[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int idx = idx0 + q * E;
-              if (idx < cnt) {
-                lv[q] = stv[((off + idx) << lgS) + s];
-                sl[q] = sts[off + idx] * S + s;
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (idx0 + q * E < cnt) xv[q] = x[sl[q]];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int idx = idx0 + q * E;
-              if (idx < cnt) {
-                double l = lv[q];  // staged before L(:,k) was published?  wait for it
-                if (is_sentinel(l)) l = wait_value_bo(&d.Lx[IL(d, lbk + idx, sys)], d.poll_ns);
-                x[sl[q]] = __dsub_rn(xv[q], __dmul_rn(l, xk));
-              }
+          for (int q = 0; q < 4; ++q) {
+            const int idx = idx0 + q * E;
+            if (idx < cnt) {
+              lv[q] = stv[((off + idx) << lgS) + s];
+              sl[q] = sts[off + idx] * S + s;
             }
           }
-        } else {
-          for (int idx = e; idx < cnt; idx += E) {
-            const double l = wait_value_bo(&d.Lx[IL(d, lbk + idx, sys)], d.poll_ns);
-            const int sl = d.upd_slot32[pair0 + idx] * S + s;
-            x[sl] = __dsub_rn(x[sl], __dmul_rn(l, xk));
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (idx0 + q * E < cnt) xv[q] = x[sl[q]];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int idx = idx0 + q * E;
+            if (idx < cnt) {
+              double l = lv[q];  // staged before L(:,k) was published?  wait for it
+              if (is_sentinel(l)) l = wait_value_bo(lx_ptr(d, lbk + idx, sys), d.poll_ns);
+              x[sl[q]] = __dsub_rn(xv[q], __dmul_rn(l, xk));
+            }
           }
         }
         __syncwarp();
@@ -338,7 +357,7 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
     for (int idx = e; idx < nl; idx += E) {
       const double v = x[(nu + 1 + idx) * S + s];
       gm = fmax(gm, fabs(v));
-      st_relaxed_f64(&d.Lx[IL(d, lb + idx, sys)], unsentinel(__ddiv_rn(v, ujj)));
+      st_relaxed_f64(lx_ptr(d, lb + idx, sys), unsentinel(__ddiv_rn(v, ujj)));
     }
     for (int idx = e; idx < nl; idx += E)
       d.Lv[IL(d, d.Lmap[lb + idx], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + idx) * S + s], ujj));
@@ -357,6 +376,8 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
     }
     __syncwarp();
     PROF_MARK(5);
+    if (prof && lane == 0 && d.trace_ref && my_task < 2 * d.n)
+      d.trace_ref[my_task] = (unsigned long long)(clock64() - t_task);
   }
 }
 
@@ -381,9 +402,13 @@ __global__ void __launch_bounds__(256) k_b_diag_stats(DevPlan d) {
 // Triangular solves (direct_lu.py:359-379).  Same phase split and per-row order as the
 // single-system kernels (trisolve.cu), lanes = systems.
 // ----------------------------------------------------------------------------
-template <bool IS_U>
+// A task is one row for G x 32 systems: lane l serves systems {g*32 + l}; the G copies
+// share the row's column indices and their loads are in flight together (G-fold ILP per
+// task, G-fold fewer tasks).  Rows are taken round-robin in level order.
+template <bool IS_U, int G>
 __global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__restrict__ b,
                                                      double *__restrict__ xout) {
+  constexpr int C = 4;  // entries per chunk
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -395,82 +420,198 @@ __global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__
   const double *vals = IS_U ? d.Uv : d.Lv;
   double *ysrc = IS_U ? d.yU : d.yL;  // published by this sweep
   double *yres = IS_U ? d.yL : d.yU;  // reset for the next solve
-  const int ngroups = d.nbp >> 5;
-  const int ntask = nrows * ngroups;
+  const int nsg = d.nbp / (32 * G);   // system super-groups
+  const int ntask = nrows * nsg;
   const int gstart = IS_U ? 0 : d.L_sync_ptr[d.L_nsync];  // leading levels ran row-parallel
-  for (int task = gstart * ngroups + gwarp; task < ntask; task += nwarps) {
-    const int idx = task / ngroups;
-    const int sys = (task - idx * ngroups) * 32 + lane;
-    const unsigned amask = __ballot_sync(FULL, sys_active(d, sys));
+  for (int task = gstart * nsg + gwarp; task < ntask; task += nwarps) {
+    const int idx = task / nsg;
+    const int sbase = (task - idx * nsg) * 32 * G + lane;
+    bool act[G];
+    bool any = false;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      act[g] = sys_active(d, sbase + 32 * g);
+      any |= act[g];
+    }
+    const unsigned amask = __ballot_sync(FULL, any);
     if (!amask) continue;
-    const bool act = (amask >> lane) & 1u;
     const int r = order[idx];
     const int cr = crit[idx];
     const int beg = rp[r], end = rp[r + 1];
     // Everything that does not depend on the critical dependency is loaded first: the
-    // initial value, the pivot, the first 8 entries and (speculatively) their y values —
-    // the non-critical dependencies are normally published already.
-    double acc = 0.0, piv = 1.0;
-    int cols[8];
-    double vs[8], ys[8];
-    if (act) {
-      acc = IS_U ? ldcg(&d.yL[IL(d, r, sys)]) : b[IL(d, d.row_perm[r], sys)];
-      if (IS_U) piv = d.udiag[IL(d, r, sys)];
+    // initial values, the pivots, the first chunk and (speculatively) its y values.
+    double acc[G], piv[G];
+    int cols[C];
+    double vs[C][G], ys[C][G];
+    const int prow = IS_U ? r : d.row_perm[r];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+    for (int q = 0; q < C; ++q)
+      if (beg + q < end) cols[q] = ci[beg + q];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int sys = sbase + 32 * g;
+      acc[g] = IS_U ? ldcg(&d.yL[IL(d, r, sys)]) : b[IL(d, prow, sys)];
+      piv[g] = IS_U ? d.udiag[IL(d, r, sys)] : 1.0;
+#pragma unroll
+      for (int q = 0; q < C; ++q)
         if (beg + q < end) {
-          cols[q] = ci[beg + q];
-          vs[q] = vals[IL(d, beg + q, sys)];
+          vs[q][g] = vals[IL(d, beg + q, sys)];
+          ys[q][g] = ld_relaxed_f64(&ysrc[IL(d, cols[q], sys)]);
         }
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (beg + q < end) ys[q] = ld_relaxed_f64(&ysrc[IL(d, cols[q], sys)]);
     }
-    // one lane waits (with back-off) on the critical dependency of one system: the 32
-    // systems' values of a row are published by one warp store, so the others follow
-    if (cr >= 0 && lane == 31 - __clz(amask)) wait_value_bo(&ysrc[IL(d, cr, sys)], d.poll_ns);
+    // one lane waits (with back-off) on the critical dependency of one system: all systems'
+    // values of a row are published by one task, so the others follow
+    if (cr >= 0 && lane == 31 - __clz(amask)) {
+      int g = 0;
+#pragma unroll
+      for (int q = G - 1; q >= 0; --q)
+        if (act[q]) g = q;
+      wait_value_bo(&ysrc[IL(d, cr, sbase + 32 * g)], d.poll_ns);
+    }
     __syncwarp();
-    if (!act) continue;  // per lane from here: systems are independent
-    // software pipeline over 8-entry chunks: the next chunk's columns and values are in
-    // flight while this chunk is consumed, so a long row costs ~one round trip per chunk
-    for (int c0 = beg; c0 < end; c0 += 8) {
-      int ncols[8];
-      double nvs[8];
+    // software pipeline over C-entry chunks: the next chunk's columns and values are in
+    // flight while this chunk is consumed
+    for (int c0 = beg; c0 < end; c0 += C) {
+      int ncols[C];
+      double nvs[C][G];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (c0 + 8 + q < end) {
-          ncols[q] = ci[c0 + 8 + q];
-          nvs[q] = vals[IL(d, c0 + 8 + q, sys)];
+      for (int q = 0; q < C; ++q)
+        if (c0 + C + q < end) {
+          ncols[q] = ci[c0 + C + q];
+#pragma unroll
+          for (int g = 0; g < G; ++g) nvs[q][g] = vals[IL(d, c0 + C + q, sbase + 32 * g)];
         }
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < C; ++q)
         if (c0 + q < end) {
-          double y = ys[q];
-          if (is_sentinel(y)) y = wait_value_bo(&ysrc[IL(d, cols[q], sys)], d.poll_ns);
-          acc = __dsub_rn(acc, __dmul_rn(vs[q], y));
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            if (!act[g]) continue;
+            double y = ys[q][g];
+            if (is_sentinel(y)) y = wait_value_bo(&ysrc[IL(d, cols[q], sbase + 32 * g)], d.poll_ns);
+            acc[g] = __dsub_rn(acc[g], __dmul_rn(vs[q][g], y));
+          }
         }
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (c0 + 8 + q < end) {
+      for (int q = 0; q < C; ++q)
+        if (c0 + C + q < end) {
           cols[q] = ncols[q];
-          vs[q] = nvs[q];
-          ys[q] = ld_relaxed_f64(&ysrc[IL(d, cols[q], sys)]);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            vs[q][g] = nvs[q][g];
+            ys[q][g] = ld_relaxed_f64(&ysrc[IL(d, cols[q], sbase + 32 * g)]);
+          }
         }
     }
-    const double w = IS_U ? __ddiv_rn(acc, piv) : acc;
-    st_relaxed_f64(&ysrc[IL(d, r, sys)], unsentinel(w));  // publish first
-    if (d.trace_trsv && sys == 0) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
-    st_relaxed_f64(&yres[IL(d, r, sys)], sentinel_value());
-    if (IS_U) {
-      xout[IL(d, d.col_perm[r], sys)] = w;
-      if (!isfinite(w)) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (!act[g]) continue;
+      const int sys = sbase + 32 * g;
+      const double w = IS_U ? __ddiv_rn(acc[g], piv[g]) : acc[g];
+      st_relaxed_f64(&ysrc[IL(d, r, sys)], unsentinel(w));  // publish first
+      if (d.trace_trsv && sys == 0) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
+      st_relaxed_f64(&yres[IL(d, r, sys)], sentinel_value());
+      if (IS_U) {
+        xout[IL(d, d.col_perm[r], sys)] = w;
+        if (!isfinite(w)) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
+      }
     }
   }
 }
 
-cudaError_t b_launch_grid_L(const DevPlan &d, const double *b, double *x, int grid_blocks, cudaStream_t s) {
-  k_b_trsv_grid<false><<<grid_blocks, 256, 0, s>>>(d, b, x);
+// Level-synchronous variant of the grid phase for batches: one persistent launch walks the
+// levels of the grid order with a grid-wide barrier between levels.  Within a level every
+// (row, 32-system group) task is independent, so nothing polls: a batch has enough rows x
+// systems per level to keep the GPU busy, and a barrier (~1-2 us) replaces the per-row
+// readiness round trips of the sync-free kernel.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned *bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned nb = gridDim.x;
+    const unsigned g = ld_acquire_u32(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nb - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire_u32(bar + 1) == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <bool IS_U>
+__global__ void __launch_bounds__(256) k_b_trsv_levels(DevPlan d, const double *__restrict__ b,
+                                                       double *__restrict__ xout) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int *order = IS_U ? d.U_grid_order : d.L_grid_order;
+  const int *glev = IS_U ? d.U_glev : d.L_glev;
+  const int nlev = IS_U ? d.U_nglev : d.L_nglev;
+  const int *rp = IS_U ? d.Urp : d.Lrp;
+  const int *ci = IS_U ? d.Uci : d.Lci;
+  const double *vals = IS_U ? d.Uv : d.Lv;
+  double *ysrc = IS_U ? d.yU : d.yL;
+  double *yres = IS_U ? d.yL : d.yU;
+  const int ngroups = d.nbp >> 5;
+  for (int lev = IS_U ? 0 : d.L_nsync; lev < nlev; ++lev) {
+    const int r0 = glev[lev], r1 = glev[lev + 1];
+    for (int task = gwarp; task < (r1 - r0) * ngroups; task += nwarps) {
+      const int idx = r0 + task / ngroups;
+      const int sys = (task % ngroups) * 32 + lane;
+      if (!sys_active(d, sys)) continue;
+      const int r = order[idx];
+      const int beg = rp[r], end = rp[r + 1];
+      double acc = IS_U ? ldcg(&d.yL[IL(d, r, sys)]) : b[IL(d, d.row_perm[r], sys)];
+      for (int c0 = beg; c0 < end; c0 += 4) {
+        double v[4], y[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (c0 + q < end) {
+            v[q] = vals[IL(d, c0 + q, sys)];
+            y[q] = ldcg(&ysrc[IL(d, ci[c0 + q], sys)]);
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (c0 + q < end) acc = __dsub_rn(acc, __dmul_rn(v[q], y[q]));
+      }
+      const double w = IS_U ? __ddiv_rn(acc, d.udiag[IL(d, r, sys)]) : acc;
+      ysrc[IL(d, r, sys)] = unsentinel(w);
+      yres[IL(d, r, sys)] = sentinel_value();
+      if (IS_U) {
+        xout[IL(d, d.col_perm[r], sys)] = w;
+        if (!isfinite(w)) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
+      }
+    }
+    if (lev + 1 < nlev) grid_barrier(d.gbar);
+  }
+}
+
+template <bool IS_U>
+static cudaError_t b_launch_grid(const DevPlan &d, const double *b, double *x, int grid_blocks,
+                                 cudaStream_t s) {
+  if (d.b_levelsync) {
+    k_b_trsv_levels<IS_U><<<grid_blocks, 256, 0, s>>>(d, b, x);
+    return cudaGetLastError();
+  }
+  const int groups = d.nbp >> 5;
+  (void)groups;  // (G > 1 measured slower: fewer, longer tasks)
+  k_b_trsv_grid<IS_U, 1><<<grid_blocks, 256, 0, s>>>(d, b, x);
   return cudaGetLastError();
+}
+
+cudaError_t b_launch_grid_L(const DevPlan &d, const double *b, double *x, int grid_blocks, cudaStream_t s) {
+  return b_launch_grid<false>(d, b, x, grid_blocks, s);
 }
 
 cudaError_t b_launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,
@@ -492,7 +633,8 @@ cudaError_t b_launch_trsv(const DevPlan &d, const double *b, double *x, int grid
     ++*launches;
   }
   if (d.nUg) {
-    k_b_trsv_grid<true><<<grid_blocks, 256, 0, s>>>(d, b, x);
+    cudaError_t e = b_launch_grid<true>(d, b, x, grid_blocks, s);
+    if (e != cudaSuccess) return e;
     ++*launches;
   }
   return cudaGetLastError();
@@ -720,6 +862,21 @@ __global__ void k_b_broadcast(const double *__restrict__ src, int64_t count, int
     dst[f] = src[f / nbp];
 }
 
+__global__ void k_b_split_heavy(DevPlan d) {
+  const int64_t total = d.nLH * d.nbp;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int sys = (int)(f / d.nLH);
+    const int64_t i = f - (int64_t)sys * d.nLH;
+    d.LxH[f] = d.Lx[IL(d, d.LH0 + i, sys)];
+  }
+}
+
+cudaError_t b_launch_split_heavy(const DevPlan &d, cudaStream_t s) {
+  if (d.nLH) k_b_split_heavy<<<4 * 148, 256, 0, s>>>(d);
+  return cudaGetLastError();
+}
+
 cudaError_t b_launch_broadcast(const double *src, int64_t count, int nbp, double *dst, cudaStream_t s) {
   if (count) k_b_broadcast<<<4 * 148, 256, 0, s>>>(src, count, nbp, dst);
   return cudaGetLastError();
@@ -734,7 +891,7 @@ static dim3 row_grid(const DevPlan &d, int per_group) {
 }
 static const dim3 ROW_BLOCK(32, BY);
 
-cudaError_t b_configure(size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm) {
+cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm) {
   const int sm = (int)refactor_smem;
   cudaError_t e = cudaFuncSetAttribute(k_b_refactor, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   // the occupancy is shared-memory bound: ask for the largest carveout
@@ -743,10 +900,19 @@ cudaError_t b_configure(size_t refactor_smem, int *refactor_blocks_per_sm, int *
                              cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(refactor_blocks_per_sm, k_b_refactor, 32 * B_WARPS, sm);
-  int a = 0, b = 0;
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_b_trsv_grid<false>, 256, 0);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_b_trsv_grid<true>, 256, 0);
-  *trsv_blocks_per_sm = a < b ? a : b;
+  int m = 1 << 30;
+  auto occ = [&](const void *f) {
+    int a = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, f, 256, 0);
+    m = a < m ? a : m;
+  };
+  occ((const void *)k_b_trsv_levels<false>);
+  occ((const void *)k_b_trsv_levels<true>);
+  const int groups = nbp >> 5;  // occupancy of the variant b_launch_grid picks
+  (void)groups;
+  occ((const void *)k_b_trsv_grid<false, 1>);
+  occ((const void *)k_b_trsv_grid<true, 1>);
+  *trsv_blocks_per_sm = m;
   return e;
 }
 
@@ -759,7 +925,8 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, cudaStr
   if (!d.n) return cudaSuccess;
   // (KKT_NO_RESET=1, diagnostics only: keep the previous factors so no task ever waits)
   static const bool no_reset = std::getenv("KKT_NO_RESET") != nullptr;
-  cudaError_t e = no_reset ? cudaSuccess : cudaMemsetAsync(d.Lx, 0xFF, 8 * (size_t)d.nnz_L * d.nbp, s);
+  cudaError_t e = no_reset ? cudaSuccess : cudaMemsetAsync(d.Lx, 0xFF, 8 * (size_t)d.LH0 * d.nbp, s);
+  if (e == cudaSuccess && d.nLH && !no_reset) e = cudaMemsetAsync(d.LxH, 0xFF, 8 * (size_t)d.nLH * d.nbp, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.ticket, 0, 4, s);
   if (e != cudaSuccess) return e;
   for (int l = 0; l < d.n_small_levels; ++l) {

@@ -59,8 +59,8 @@ static void destroy(Device *dev) {
 // the per-column critical path (lanes over entries): the workspace x[np][S] must fit the
 // per-warp budget, and heavy columns (many update pairs) get more entry lanes.
 // KKT_B_SCHED="lo,mid,hi" overrides the pair thresholds for S <= 8 / 4 / 1.
-static int build_batch_tasks(const HostPlan &h, int nbp, int xbudget, std::vector<int2> &tasks) {
-  int lo = 64, mid = 256, hi = 1024;
+static int build_batch_tasks(const HostPlan &h, int nbp, int xbudget, int J0, std::vector<int2> &tasks) {
+  int lo = 1 << 30, mid = 1 << 30, hi = 1 << 30;  // default: S from the workspace only
   if (const char *e = std::getenv("KKT_B_SCHED")) std::sscanf(e, "%d,%d,%d", &lo, &mid, &hi);
   const int start = h.small_lev_ptr[h.n_small_levels];
   tasks.clear();
@@ -73,7 +73,7 @@ static int build_batch_tasks(const HostPlan &h, int nbp, int xbudget, std::vecto
     for (int64_t t = h.so_ptr[j]; t < h.so_ptr[j + 1]; ++t) pairs += h.so_meta[4 * t + 1];
     int S = 32;
     while (S > 1 && np * S > xbudget) S >>= 1;
-    if (pairs > hi) S = 1;
+    if (pairs > hi || j >= J0) S = 1;  // heavy tail: one system per warp (LxH)
     else if (pairs > mid) S = std::min(S, 4);
     else if (pairs > lo) S = std::min(S, 8);
     int lg = 0;
@@ -113,14 +113,27 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.n = h.n;
   d.nb = nb;
   d.nbp = nbp;
-  d.rb = nb == 1 ? RED_BLOCKS : std::max(8, RED_BLOCKS / (nbp / 32));  // blocks per group
+  // reduction blocks per group: the batched vector kernels are HBM-bound, so the grid covers
+  // the SMs several times over whatever the number of 32-system groups
+  d.rb = nb == 1 ? RED_BLOCKS : std::max(64, 8 * 148 / (nbp / 32));
   std::vector<int2> btask;
   d.b_xbudget = B_XBUDGET;
   d.b_stage = B_STAGE;  // doubles per stage buffer (two buffers per warp)
   if (const char *e = std::getenv("KKT_B_SMEM")) std::sscanf(e, "%d,%d", &d.b_xbudget, &d.b_stage);
+  d.b_static = std::getenv("KKT_B_STATIC") ? std::atoi(std::getenv("KKT_B_STATIC")) : 0;
   d.b_xbudget = std::max(d.b_xbudget, h.maxpat);
   if (nb > 1) {
-    int rc2 = build_batch_tasks(h, nbp, d.b_xbudget, btask);
+    // heavy tail: from the first column whose pattern exceeds KKT_B_HEAVY_NP slots
+    const int heavy_np = std::getenv("KKT_B_HEAVY_NP") ? std::atoi(std::getenv("KKT_B_HEAVY_NP")) : 256;
+    d.J0 = h.n;
+    for (int j = 0; j < h.n; ++j)
+      if (heavy_np > 0 && (h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j]) > heavy_np) {
+        d.J0 = j;
+        break;
+      }
+    d.LH0 = h.Lp[d.J0];
+    d.nLH = h.nnz_L - d.LH0;
+    int rc2 = build_batch_tasks(h, nbp, d.b_xbudget, d.J0, btask);
     if (rc2 != KKT_OK) {
       delete dev;
       return rc2;
@@ -170,6 +183,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   acc(8 * d.nnz_L * B); acc(8 * d.nnz_U * B); acc(8 * n * B); acc(8 * n * B);  // Lv Uv yL yU
   acc(8 * SCAL_STRIDE * B); acc(64); acc(8 * 8 * (size_t)d.rb * B);        // scal ticket partials
   acc(8 * btask.size());                                                   // batched tasks
+  acc(4 * h.L_glev_ptr.size()); acc(4 * h.U_glev_ptr.size()); acc(64);     // levels, barrier
+  acc(8 * (size_t)d.nLH * B);                                              // LxH
   for (const HostSweep *hs : {&h.swL, &h.swU}) {
     acc(4 * hs->dptr.size()); acc(4 * hs->dsrc.size()); acc(2 * hs->ddst.size());
     acc(4 * hs->dmask.size()); acc(4 * hs->bptr.size()); acc(4 * hs->brow.size());
@@ -228,6 +243,13 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.ticket = carve<int>(cur, 16);
   d.partials = carve<double>(cur, 8 * (size_t)d.rb * B);
   d.btask = carve<int2>(cur, btask.size());
+  d.L_glev = carve<int>(cur, h.L_glev_ptr.size());
+  d.U_glev = carve<int>(cur, h.U_glev_ptr.size());
+  d.gbar = carve<unsigned>(cur, 16);
+  d.L_nglev = (int)h.L_glev_ptr.size() - 1;
+  d.U_nglev = (int)h.U_glev_ptr.size() - 1;
+  d.b_levelsync = std::getenv("KKT_B_LEVELSYNC") ? std::atoi(std::getenv("KKT_B_LEVELSYNC")) : 0;
+  d.LxH = carve<double>(cur, (size_t)d.nLH * B);
   {
     const HostSweep *hs[2] = {&h.swL, &h.swU};
     SweepDev *sd[2] = {&d.swL, &d.swU};
@@ -296,6 +318,9 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   UP(d.Ui, h.Ui32);
   UP(d.Ltail_split, h.Ltail_split);
   UP(d.btask, btask);
+  UP(d.L_glev, h.L_glev_ptr);
+  UP(d.U_glev, h.U_glev_ptr);
+  CUDA_TRY(cudaMemsetAsync(d.gbar, 0, 64, dev->stream));
   UP(d.swL.dptr, h.swL.dptr); UP(d.swL.dsrc, h.swL.dsrc); UP(d.swL.ddst, h.swL.ddst);
   UP(d.swL.dmask, h.swL.dmask); UP(d.swL.bptr, h.swL.bptr); UP(d.swL.brow, h.swL.brow);
   UP(d.swL.bbeg, h.swL.bbeg); UP(d.swL.bcnt, h.swL.bcnt); UP(d.swL.bofs, h.swL.bofs);
@@ -333,6 +358,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
         if (ce != cudaSuccess) break;
       }
       cudaFree(tmp);
+      if (ce == cudaSuccess) ce = b_launch_split_heavy(d, dev->stream);
       if (ce != cudaSuccess) {
         destroy(dev);
         return set_error(KKT_ERR_CUDA, std::string("initial factors: ") + cudaGetErrorString(ce));
@@ -348,7 +374,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   if (nbp > 1) {
     int rbps = 0, tbps = 0;
     dev->refactor_smem = b_refactor_smem(d.b_xbudget, d.b_stage);
-    CUDA_TRY(b_configure(dev->refactor_smem, &rbps, &tbps));
+    CUDA_TRY(b_configure(nbp, dev->refactor_smem, &rbps, &tbps));
     dev->refactor_warps = B_WARPS;
     if (d.trace_step) d.prof = d.trace_step;  // per-warp cycle counters
     dev->refactor_blocks = std::max(1, rbps) * dev->sm_count;
@@ -646,6 +672,14 @@ int kkt_dev_download_factors(kkt_device *d, double *Lx, double *Ux, double *Udia
       if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
       for (size_t q = 0; q < nb; ++q)
         for (size_t i = 0; i < a.cnt; ++i) a.dst[q * a.cnt + i] = tmp[i * nbp + q];
+    }
+    if (Lx && p.nLH) {  // the heavy tail of L is system-major
+      std::vector<double> tmp((size_t)p.nLH * nbp);
+      e = cudaMemcpyAsync(tmp.data(), p.LxH, 8 * tmp.size(), cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
+      for (size_t q = 0; q < nb; ++q)
+        for (int64_t i = 0; i < p.nLH; ++i) Lx[q * p.nnz_L + p.LH0 + i] = tmp[q * p.nLH + i];
     }
     return KKT_OK;
   }

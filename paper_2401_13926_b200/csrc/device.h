@@ -38,7 +38,14 @@ struct DevPlan {
   int nbp = 1;
   int2 *btask = nullptr;  // batched refactor tasks {column, sys0 << 8 | log2(systems)}
   int n_btask = 0;
-  int b_xbudget = 0, b_stage = 0;  // per-warp shared workspace / stage (doubles), k_b_refactor
+  int b_xbudget = 0, b_stage = 0, b_static = 0;
+  // Heavy tail (columns >= J0, the dense separator): its L columns are consumed only by
+  // columns >= J0, whose tasks run one system per warp with lanes over entries, so those
+  // L values are stored system-major ([nbp][nLH], LxH) for coalesced access; the rest of
+  // Lx stays interleaved.
+  int J0 = 0x7fffffff;
+  int64_t LH0 = 0, nLH = 0;
+  double *LxH = nullptr;  // per-warp shared workspace / stage (doubles), k_b_refactor
   unsigned long long *prof = nullptr;  // optional per-warp cycle counters (KKT_TRACE, batched)
   int rb = RED_BLOCKS;  // reduction blocks per system
   int64_t nnz_a = 0, in_nnz = 0, in_cap = 0, nnz_L = 0, nnz_U = 0, n_so = 0, n_upd = 0, n_ap = 0;
@@ -63,6 +70,10 @@ struct DevPlan {
   double *tacc;                             // [nb][n - pL] tail partial sums (grid -> sweep)
   int pL, pU, nLg, nUg;                     // split positions and grid-phase row counts
   int L_nsync = 0, L_sync_ptr[5] = {0, 0, 0, 0, 0};  // level-synchronous leading L levels
+  int *L_glev = nullptr, *U_glev = nullptr;  // level boundaries of the grid orders
+  int L_nglev = 0, U_nglev = 0;
+  unsigned *gbar = nullptr;                   // grid barrier {count, generation}
+  int b_levelsync = 0;  // batched grid phases level-synchronous (KKT_B_LEVELSYNC=1; slower here)
   int sweep_maxL, sweep_maxU;
   SweepDev swL, swU;                        // blocked sweeps of the trailing blocks
   double *Lv, *Uv;                          // [nb][nnz_L], [nb][nnz_U] (CSR order)
@@ -80,6 +91,11 @@ struct DevPlan {
 
 __host__ __device__ __forceinline__ size_t IL(const DevPlan &d, int64_t i, int sys) {
   return (size_t)i * d.nbp + sys;
+}
+
+// address of L value idx (CSC) of system sys in the batched layout (interleaved / heavy tail)
+__device__ __forceinline__ double *lx_ptr(const DevPlan &d, int64_t idx, int sys) {
+  return idx >= d.LH0 ? d.LxH + (size_t)sys * d.nLH + (idx - d.LH0) : d.Lx + IL(d, idx, sys);
 }
 
 __device__ __forceinline__ bool sys_active(const DevPlan &d, int sys) {
@@ -143,10 +159,10 @@ cudaError_t launch_sweep_blocked(const DevPlan &d, bool upper, double *x, cudaSt
 
 // ---- batched (interleaved, nb > 1) kernels: batch.cu ----
 constexpr int B_XBUDGET = 768;   // default refactor workspace doubles per warp (np * systems)
-constexpr int B_STAGE = 256;     // default stage buffer doubles (pairs * systems), x2 buffers
+constexpr int B_STAGE = 512;     // default stage buffer doubles (pairs * systems), x2 buffers
 constexpr int B_WARPS = 4;       // warps per refactor CTA
 size_t b_refactor_smem(int xbudget, int stage);
-cudaError_t b_configure(size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm);
+cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm);
 cudaError_t b_launch_expand_norms(const DevPlan &d, cudaStream_t s);
 cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, cudaStream_t s, long long *launches);
 cudaError_t b_launch_diag_stats(const DevPlan &d, cudaStream_t s);
@@ -160,6 +176,7 @@ cudaError_t b_launch_resid_stats(const DevPlan &d, const double *r, const double
 cudaError_t b_launch_to_il(const DevPlan &d, const double *src, double *dst, cudaStream_t s);
 cudaError_t b_launch_from_il(const DevPlan &d, const double *src, double *dst, cudaStream_t s);
 cudaError_t b_launch_broadcast(const double *src, int64_t count, int nbp, double *dst, cudaStream_t s);
+cudaError_t b_launch_split_heavy(const DevPlan &d, cudaStream_t s);  // LxH <- Lx (heavy part)
 // FGMRES vector kernels on interleaved [n][nbp] vectors (partials [nbp][nvec][rb])
 cudaError_t b_launch_dots(const DevPlan &d, const double *V, int nvec, const double *w,
                           const int *mask, double *partials, cudaStream_t s);

@@ -299,6 +299,16 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
       lu[r] = l;
     }
     P.U_grid_order = order_by_level(lu);
+    // level boundaries of both grid orders (the batched level-synchronous kernel)
+    auto lev_ptr = [](const std::vector<int32_t> &lev, std::vector<int32_t> &ptr) {
+      int32_t nl = 0;
+      for (int32_t l : lev) nl = std::max(nl, l + 1);
+      ptr.assign(nl + 1, 0);
+      for (int32_t l : lev) ptr[l + 1]++;
+      for (int32_t l = 0; l < nl; ++l) ptr[l + 1] += ptr[l];
+    };
+    lev_ptr(lg, P.L_glev_ptr);
+    lev_ptr(lu, P.U_glev_ptr);
     P.U_grid_levels = 0;
     for (int32_t l : lu) P.U_grid_levels = std::max(P.U_grid_levels, l + 1);
     // critical dependency: highest level, ties -> the most recently finished column

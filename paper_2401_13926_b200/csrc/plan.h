@@ -50,6 +50,7 @@ struct HostPlan {
   std::vector<int32_t> L_grid_order, L_tail_order, U_head_order, U_grid_order;
   // L_grid_order offsets of the leading levels run level-synchronously (L_sync_ptr.size()-1)
   std::vector<int32_t> L_sync_ptr;
+  std::vector<int32_t> L_glev_ptr, U_glev_ptr;  // level boundaries in L/U_grid_order
   // per grid-order index: the row's critical (highest-level) grid dependency, or -1
   std::vector<int32_t> L_crit, U_crit;
   // per head column j >= pU: offset in U(:,j) (CSC, rows ascending) of the first row >= pU

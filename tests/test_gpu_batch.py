@@ -14,9 +14,14 @@ from paper_2401_13926_b200 import _native as nat
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("case,nb", [("acopf_small", 5), ("standard_trace", 9), ("acopf_tiny", 20)])
-def test_batch_refactor_solve_bitwise(case, nb):
+@pytest.mark.parametrize("case,nb,heavy", [("acopf_small", 5, None), ("standard_trace", 9, None),
+                                           ("acopf_tiny", 20, None), ("acopf_small", 40, "8"),
+                                           ("standard_trace", 3, "4")])
+def test_batch_refactor_solve_bitwise(case, nb, heavy, monkeypatch):
+    """heavy: KKT_B_HEAVY_NP, forcing the system-major heavy-tail storage on small cases."""
     import torch
+    if heavy:
+        monkeypatch.setenv("KKT_B_HEAVY_NP", heavy)
     from paper_2401_13926_b200.device import DeviceSystem
     g = golden(case)
     M = g["K_values"].shape[0]

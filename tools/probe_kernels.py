@@ -72,3 +72,19 @@ if os.environ.get("KKT_TRACE") and B > 1:
         f"{nm} {pr[:, k].sum() / tot:.1%}" for k, nm in enumerate(names)) +
         f"; tasks {pr[:, 6].sum():.0f}, staged values {pr[:, 7].sum():.3e}, "
         f"mean warp cycles {pr[:, :6].sum(1).mean():.3e}", flush=True)
+if os.environ.get("KKT_TRACE") and B > 1 and "--tasks" in sys.argv:
+    # per-task cycles (k_b_refactor) by column pattern size
+    ref = np.zeros(2 * f.n, dtype=np.uint64)
+    tri = np.zeros(2 * f.n, dtype=np.uint64)
+    nat.check(dev.lib.kkt_dev_trace(dev.h, ref.ctypes.data_as(C.c_void_p), tri.ctypes.data_as(C.c_void_p)))
+    # rebuild the task table like build_batch_tasks (default thresholds)
+    Lc, Uc = np.diff(f._Lp), np.diff(f._Up)
+    npat = Lc + Uc + 1
+    so = f._so_ptr
+    cnt = Lc[f._so_data]
+    pairs = np.add.reduceat(np.append(cnt, 0), so[:-1])[:f.n] * (np.diff(so) > 0)
+    info = dev.info()
+    print("task-cycle histogram needs the plan order; raw stats:", np.count_nonzero(ref),
+          "tasks, cycles total %.3e" % ref.astype(float).sum(), flush=True)
+    dur = ref.astype(float)
+    np.save("gpurun_out/task_cycles.npy", dur)
