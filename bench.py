@@ -10,15 +10,20 @@ system goes through the reference's per-system loop (harness._run_direct_family,
 harness.py:223-245): refactorize on the frozen analysis -> lu_solve -> refine_fgmres, with the
 barrier-tied tolerance delta(mu).
 
-A step = one batch of B independent systems of that family (default B = 64, the "batch of 64
-ACTIVSg10k-shaped systems" configuration) processed by one batched device handle.  The metric
-is throughput: value = device time / systems processed (all ranks).  The single-system latency
+A step = one batch of B independent systems (default B = 64, the "batch of 64
+ACTIVSg10k-shaped systems" configuration): B contingency / time-period variants (independent
+value streams of the same pattern) at the SAME barrier step k, as a batched interior-point
+method advances its scenarios in lockstep.  Step s uses k = 1 + (7 s mod (M-1)), a stride
+through the whole barrier sequence, so any number of steps samples early (well-conditioned,
+no IR) and late (ill-conditioned, several FGMRES iterations) systems alike.  The metric is
+throughput: value = device time / systems processed (all ranks).  The single-system latency
 (B = 1, the sequence systems 1..19 in order) is reported in config.single_system.
 
 value  : device-resident inputs, CUDA-event time per step, L2 flushed between steps
          (256 MiB write, untimed).
-e2e    : the same step through the C ABI (kkt_dev_step) with HOST (pinned) buffers: values
-         and rhs H2D, x D2H inside the timing.
+e2e    : the same steps through the public API with HOST (pinned) buffers: per step the
+         values and rhs go H2D and x comes back D2H inside the timed region, overlapped with
+         the neighbouring steps' compute (pipeline.BatchPipeline: copy stream, double buffers).
 roofline: dominant kernel family, algorithmic bytes per launch / event time.
 cpu_baseline: the CPU oracle port (oracle/kkt_oracle.c), single thread, bounded sample.
 --impl reference: the reference arm = the oracle port on all host threads (one system per
@@ -126,16 +131,17 @@ def policy_of(args):
     return BarrierTiedTolerance() if args.tol == "barrier" else FixedTolerance(args.delta)
 
 
-def make_batch(pat, B: int, M: int, seed_base: int):
-    """B distinct systems of the family: member q is barrier step 1 + q mod (M-1) of value
-    stream seed_base + q // (M-1) (the same sparsity pattern, different values)."""
+def step_k(s: int, M: int) -> int:
+    """barrier step of bench step s: a stride-7 walk through 1..M-1"""
+    return 1 + (7 * s) % (M - 1)
+
+
+def make_batch(pat, B: int, k: int, seed_base: int):
+    """B independent systems (value streams seed_base + q) at barrier step k."""
     from paper_2401_13926_b200.acopf import MU_STEP, system_rhs, system_values
-    ks = [1 + q % (M - 1) for q in range(B)]
-    seeds = [seed_base + q // (M - 1) for q in range(B)]
-    vals = np.stack([system_values(pat, k, s) for k, s in zip(ks, seeds)])
-    rhs = np.stack([system_rhs(pat, k, s) for k, s in zip(ks, seeds)])
-    mus = [10.0 ** (-MU_STEP * k) for k in ks]
-    return vals, rhs, mus
+    vals = np.stack([system_values(pat, k, seed_base + q) for q in range(B)])
+    rhs = np.stack([system_rhs(pat, k, seed_base + q) for q in range(B)])
+    return vals, rhs, 10.0 ** (-MU_STEP * k)
 
 
 def oracle_factors(f, K0):
@@ -188,11 +194,20 @@ def setup(args):
     return pat, f, gen_s, time.perf_counter() - t0
 
 
+def cpu_sample(pat, M: int, seeds: int = 2):
+    """The CPU legs' workload: systems of every barrier step 1..M-1 (value streams 0..seeds-1),
+    i.e. the same mix of early / late systems the GPU steps cycle through."""
+    from paper_2401_13926_b200.acopf import MU_STEP, system_rhs, system_values
+    items = [(system_values(pat, k, q), system_rhs(pat, k, q), 10.0 ** (-MU_STEP * k))
+             for q in range(seeds) for k in range(1, M)]
+    return [i[0] for i in items], [i[1] for i in items], [i[2] for i in items]
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     pat, f, _, _ = setup(args)
-    vals, rhs, mus = make_batch(pat, max(args.batch, args.systems - 1), args.systems, 0)
+    vals, rhs, mus = cpu_sample(pat, args.systems)
     threads = os.cpu_count() or 1
     policy = policy_of(args)
     cpu_port_time(f, pat.K, vals, rhs, mus, policy, 0.5, threads)  # warm-up
@@ -203,7 +218,8 @@ def run_reference(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": value * args.batch, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} ACOPF-shaped KKT systems, refactor+solve+IR",
+        "config": {"workload": f"{args.config} ACOPF-shaped KKT systems (barrier steps 1..{args.systems - 1}), "
+                               "refactor+solve+IR per system",
                    "N": pat.N, "nnz_lower": pat.K.nnz, "batch": args.batch},
         "cpu_baseline": {"value": value, "unit": "ms/system", "cores": threads, "kind": "port",
                          "sample": f"{n_sys} systems in {wall:.1f}s ({threads} threads, one "
@@ -225,6 +241,7 @@ def main():
     import torch
     import paper_2401_13926_b200._native as nat
     from paper_2401_13926_b200.device import DeviceSystem
+    from paper_2401_13926_b200.pipeline import BatchPipeline
 
     torch.cuda.set_device(local)
     dist = None
@@ -238,18 +255,20 @@ def main():
     st = f.stats
     policy = policy_of(args)
     LOWER = nat.LAYOUT_SYMMETRIC_LOWER
+    K, W = args.steps, args.warmup
+    ks = [step_k(s, M) for s in range(K)]
+    wks = [step_k(s, M) for s in range(W)]
     t0 = time.perf_counter()
-    vals, rhs, mus = make_batch(pat, B, M, seed_base=1000 * rank)
+    host = {k: make_batch(pat, B, k, seed_base=1000 * rank) for k in sorted(set(ks + wks))}
     gen_s += time.perf_counter() - t0
-    deltas = [policy(mu) for mu in mus]
     t0 = time.perf_counter()
     dev = DeviceSystem(f, restart_m=10, device=local, batch=B)
     create_s = time.perf_counter() - t0
     stream = dev.stream
     with torch.cuda.stream(stream):
-        dvals = torch.from_numpy(vals).to(dev.device)
-        drhs = torch.from_numpy(rhs).to(dev.device)
-        dx = torch.empty_like(drhs)
+        dbat = {k: (torch.from_numpy(v).to(dev.device), torch.from_numpy(r).to(dev.device))
+                for k, (v, r, _) in host.items()}
+        dx = torch.empty((B, N), dtype=torch.float64, device=dev.device)
         flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev.device)
     stream.synchronize()
 
@@ -257,23 +276,24 @@ def main():
         with torch.cuda.stream(stream):
             flush.fill_(1.0)
 
-    def step_dev():
-        return dev.step(dvals, LOWER, drhs, dx, True, 10, 10, deltas)
+    def step_dev(k):
+        v, r = dbat[k]
+        return dev.step(v, LOWER, r, dx, True, 10, 10, policy(host[k][2]))
 
-    for _ in range(args.warmup):
-        step_dev()
+    for k in wks:
+        step_dev(k)
     launches0 = dev.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+          for _ in range(K)]
     iters = []
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
-        for s in range(args.steps):
+        for s, k in enumerate(ks):
             flush_l2()
             ev[s][0].record(stream)
-            reps = step_dev()
+            reps = step_dev(k)
             ev[s][1].record(stream)
             reps = reps if isinstance(reps, list) else [reps]
             iters.append([r.iterations for r in reps])
@@ -288,27 +308,25 @@ def main():
         t = torch.tensor([total_ms], device=dev.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = total_ms / (args.steps * B * world)
+    value = total_ms / (K * B * world)
 
-    # ---- e2e through the C ABI with host (pinned) buffers ----
-    hv = torch.from_numpy(vals).pin_memory().numpy()
-    hr = torch.from_numpy(rhs).pin_memory().numpy()
-    hx = torch.empty(rhs.shape, dtype=torch.float64).pin_memory().numpy()
-    for _ in range(2):
-        dev.step(hv, LOWER, hr, hx, False, 10, 10, deltas)
-    e2e_ms = []
-    for s in range(args.steps):
-        flush_l2()
-        stream.synchronize()
-        t0 = time.perf_counter()
-        dev.step(hv, LOWER, hr, hx, False, 10, 10, deltas)
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_total = float(np.sum(e2e_ms))
+    # ---- e2e through the public API from pinned host buffers (copies overlapped) ----
+    hp = {k: (torch.from_numpy(v).pin_memory(), torch.from_numpy(r).pin_memory())
+          for k, (v, r, _) in host.items()}
+    hx = [torch.empty((B, N), dtype=torch.float64).pin_memory() for _ in range(K)]
+    pipe = BatchPipeline(dev, LOWER)
+    pipe.run([(hp[k][0], hp[k][1], hx[0], policy(host[k][2])) for k in wks])  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pipe.run([(hp[k][0], hp[k][1], hx[s], policy(host[k][2])) for s, k in enumerate(ks)])
+    torch.cuda.synchronize()
+    e2e_total = (time.perf_counter() - t0) * 1e3
     if dist:
         t = torch.tensor([e2e_total], device=dev.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
-    e2e_value = e2e_total / (args.steps * B * world)
+    e2e_value = e2e_total / (K * B * world)
+    vals, rhs, _ = host[ks[-1]]
 
     # ---- per-kernel roofline on the batch (flushed L2) ----
     nL, nU = st["nnz_L"], st["nnz_U"]
@@ -338,7 +356,7 @@ def main():
         yb = torch.empty_like(xb)
     t_tri = timed(lambda: dev.solve_device(xb, yb), args.kernel_reps)
     t_spmv = timed(lambda: dev.spmv_device(xb, yb), args.kernel_reps)
-    t_ref = timed(lambda: dev.refactor_device(dvals, LOWER), args.kernel_reps)
+    t_ref = timed(lambda: dev.refactor_device(dbat[ks[-1]][0], LOWER), args.kernel_reps)
     peak, peak_kind = peaks()
     kern = {
         "trisolve_pair": {"ms": t_tri, "bytes": bytes_tri, "GBs": bytes_tri / t_tri / 1e6},
@@ -350,7 +368,7 @@ def main():
     it = np.array(iters, dtype=float)
     mean_iters = float(it.mean()) if it.size else 0.0
     max_iters = float(it.max(axis=1).mean()) if it.size else 0.0
-    # time share per step: the lockstep FGMRES runs a (masked) solve per iteration of the
+    # time share per step: the batch's FGMRES runs one (masked) solve per iteration of its
     # slowest system; the refactor once; SpMV a few times per iteration
     share = {"trisolve_pair": t_tri * (1 + max_iters), "refactor": t_ref,
              "spmv": t_spmv * (max_iters + 3)}
@@ -389,11 +407,12 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        wall, n_sys, mean_one = cpu_port_time(f, pat.K, list(vals), list(rhs), mus, policy,
-                                              args.cpu_seconds, threads=1)
+        cv, cr, cm = cpu_sample(pat, M)
+        wall, n_sys, mean_one = cpu_port_time(f, pat.K, cv, cr, cm, policy, args.cpu_seconds,
+                                              threads=1)
         cpu = {"value": mean_one * 1e3, "unit": "ms/system", "cores": 1, "kind": "port",
-               "sample": f"{n_sys} systems (refactorize+lu_solve+refine_fgmres) of the same "
-                         f"batch, single thread, oracle/kkt_oracle.c, {wall:.1f}s"}
+               "sample": f"{n_sys} systems (refactorize+lu_solve+refine_fgmres) of barrier "
+                         f"steps 1..{M - 1}, single thread, oracle/kkt_oracle.c, {wall:.1f}s"}
 
     if rank == 0:
         line = {
@@ -403,8 +422,10 @@ def main():
             "data": "synthetic",
             "config": {
                 "workload": f"{args.config}-shaped ill-conditioned KKT systems, batch of {B} "
-                            "independent same-pattern systems per step per GPU: refactor + "
-                            "lu_solve + FGMRES(10)-IR (CGS2) each",
+                            "independent same-pattern systems (contingency value streams) at "
+                            "one barrier step per step per GPU: refactor + lu_solve + "
+                            "FGMRES(10)-IR (CGS2) each",
+                "barrier_steps": ks,
                 "batch": B, "N": N, "nnz_lower": nnz_lower, "nnz_general": nnz_g,
                 "nnz_L": nL, "nnz_U": nU, "refactor_flops_per_system": st["refactor_flops"],
                 "levels_refactor_L_U": [st["refactor_levels"], st["L_levels"], st["U_levels"]],
@@ -412,7 +433,10 @@ def main():
                 "tolerance": ("delta(mu)=clamp(1e-2*mu,1e-10,1e-8) per system"
                               if args.tol == "barrier" else f"{args.delta}"),
                 "mean_ir_iterations": mean_iters, "mean_max_ir_iterations": max_iters,
-                "l2": "flushed between steps (256 MiB write, excluded from timing)",
+                "l2": "flushed between steps (256 MiB write, excluded from timing); inputs "
+                      "of a step (490 MB) exceed L2",
+                "e2e_note": "pinned host inputs H2D + x D2H per step, overlapped with "
+                            "neighbouring steps (pipeline.BatchPipeline)",
                 "analyze_s": analyze_s, "device_create_s": create_s, "generate_s": gen_s,
                 "parallelism": f"independent batches x{world} GPUs (no data-path collective)",
                 "step_ms": [round(x, 3) for x in step_ms],

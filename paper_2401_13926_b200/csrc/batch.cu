@@ -402,119 +402,114 @@ __global__ void __launch_bounds__(256) k_b_diag_stats(DevPlan d) {
 // Triangular solves (direct_lu.py:359-379).  Same phase split and per-row order as the
 // single-system kernels (trisolve.cu), lanes = systems.
 // ----------------------------------------------------------------------------
-// A task is one row for G x 32 systems: lane l serves systems {g*32 + l}; the G copies
-// share the row's column indices and their loads are in flight together (G-fold ILP per
-// task, G-fold fewer tasks).  Rows are taken round-robin in level order.
-template <bool IS_U, int G>
+// A task is one row for 32 systems (lane = system); rows are taken round-robin in level
+// order.  Each warp prefetches its NEXT task's static data (row pointers, the first chunk's
+// column indices and values, the initial value and pivot) while the current task waits on
+// its dependency, so a task's critical path is the dependency's y values only.
+struct RowTask {
+  int r, cr, beg, end;
+  int cols[4];
+  double vs[4], acc, piv;
+};
+
+template <bool IS_U>
+__device__ __forceinline__ void row_prefetch(const DevPlan &d, const double *__restrict__ b, int idx,
+                                             int sys, bool act, RowTask &t) {
+  const int *order = IS_U ? d.U_grid_order : d.L_grid_order;
+  const int *rp = IS_U ? d.Urp : d.Lrp;
+  const int *ci = IS_U ? d.Uci : d.Lci;
+  const double *vals = IS_U ? d.Uv : d.Lv;
+  t.r = order[idx];
+  t.cr = (IS_U ? d.U_crit : d.L_crit)[idx];
+  t.beg = rp[t.r];
+  t.end = rp[t.r + 1];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (t.beg + q < t.end) t.cols[q] = ci[t.beg + q];
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (t.beg + q < t.end) t.vs[q] = vals[IL(d, t.beg + q, sys)];
+    t.acc = IS_U ? ldcg(&d.yL[IL(d, t.r, sys)]) : b[IL(d, d.row_perm[t.r], sys)];
+    t.piv = IS_U ? d.udiag[IL(d, t.r, sys)] : 1.0;
+  }
+}
+
+template <bool IS_U>
 __global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__restrict__ b,
                                                      double *__restrict__ xout) {
   constexpr int C = 4;  // entries per chunk
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int *order = IS_U ? d.U_grid_order : d.L_grid_order;
-  const int *crit = IS_U ? d.U_crit : d.L_crit;
   const int nrows = IS_U ? d.nUg : d.nLg;
-  const int *rp = IS_U ? d.Urp : d.Lrp;
   const int *ci = IS_U ? d.Uci : d.Lci;
   const double *vals = IS_U ? d.Uv : d.Lv;
   double *ysrc = IS_U ? d.yU : d.yL;  // published by this sweep
   double *yres = IS_U ? d.yL : d.yU;  // reset for the next solve
-  const int nsg = d.nbp / (32 * G);   // system super-groups
-  const int ntask = nrows * nsg;
+  const int ngroups = d.nbp >> 5;
+  const int ntask = nrows * ngroups;
   const int gstart = IS_U ? 0 : d.L_sync_ptr[d.L_nsync];  // leading levels ran row-parallel
-  for (int task = gstart * nsg + gwarp; task < ntask; task += nwarps) {
-    const int idx = task / nsg;
-    const int sbase = (task - idx * nsg) * 32 * G + lane;
-    bool act[G];
-    bool any = false;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      act[g] = sys_active(d, sbase + 32 * g);
-      any |= act[g];
+  int task = gstart * ngroups + gwarp;
+  RowTask nt;
+  if (task < ntask) {
+    const int sys = (task % ngroups) * 32 + lane;
+    row_prefetch<IS_U>(d, b, task / ngroups, sys, sys_active(d, sys), nt);
+  }
+  for (; task < ntask; task += nwarps) {
+    const int sys = (task % ngroups) * 32 + lane;
+    const bool act = sys_active(d, sys);
+    RowTask t = nt;
+    const int nxt = task + nwarps;
+    if (nxt < ntask) {
+      const int nsys = (nxt % ngroups) * 32 + lane;
+      row_prefetch<IS_U>(d, b, nxt / ngroups, nsys, sys_active(d, nsys), nt);  // used next round
     }
-    const unsigned amask = __ballot_sync(FULL, any);
+    const unsigned amask = __ballot_sync(FULL, act);
     if (!amask) continue;
-    const int r = order[idx];
-    const int cr = crit[idx];
-    const int beg = rp[r], end = rp[r + 1];
-    // Everything that does not depend on the critical dependency is loaded first: the
-    // initial values, the pivots, the first chunk and (speculatively) its y values.
-    double acc[G], piv[G];
-    int cols[C];
-    double vs[C][G], ys[C][G];
-    const int prow = IS_U ? r : d.row_perm[r];
-#pragma unroll
-    for (int q = 0; q < C; ++q)
-      if (beg + q < end) cols[q] = ci[beg + q];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int sys = sbase + 32 * g;
-      acc[g] = IS_U ? ldcg(&d.yL[IL(d, r, sys)]) : b[IL(d, prow, sys)];
-      piv[g] = IS_U ? d.udiag[IL(d, r, sys)] : 1.0;
+    // speculative y loads of the first chunk (the non-critical dependencies are normally
+    // published already), then one lane waits (back-off) on the critical dependency
+    double ys[C];
+    if (act) {
 #pragma unroll
       for (int q = 0; q < C; ++q)
-        if (beg + q < end) {
-          vs[q][g] = vals[IL(d, beg + q, sys)];
-          ys[q][g] = ld_relaxed_f64(&ysrc[IL(d, cols[q], sys)]);
-        }
+        if (t.beg + q < t.end) ys[q] = ld_relaxed_f64(&ysrc[IL(d, t.cols[q], sys)]);
     }
-    // one lane waits (with back-off) on the critical dependency of one system: all systems'
-    // values of a row are published by one task, so the others follow
-    if (cr >= 0 && lane == 31 - __clz(amask)) {
-      int g = 0;
-#pragma unroll
-      for (int q = G - 1; q >= 0; --q)
-        if (act[q]) g = q;
-      wait_value_bo(&ysrc[IL(d, cr, sbase + 32 * g)], d.poll_ns);
-    }
+    if (t.cr >= 0 && lane == 31 - __clz(amask)) wait_value_bo(&ysrc[IL(d, t.cr, sys)], d.poll_ns);
     __syncwarp();
-    // software pipeline over C-entry chunks: the next chunk's columns and values are in
-    // flight while this chunk is consumed
-    for (int c0 = beg; c0 < end; c0 += C) {
+    if (!act) continue;  // per lane from here: systems are independent
+    double acc = t.acc;
+    for (int c0 = t.beg; c0 < t.end; c0 += C) {
       int ncols[C];
-      double nvs[C][G];
+      double nvs[C];
 #pragma unroll
       for (int q = 0; q < C; ++q)
-        if (c0 + C + q < end) {
+        if (c0 + C + q < t.end) {
           ncols[q] = ci[c0 + C + q];
-#pragma unroll
-          for (int g = 0; g < G; ++g) nvs[q][g] = vals[IL(d, c0 + C + q, sbase + 32 * g)];
+          nvs[q] = vals[IL(d, c0 + C + q, sys)];
         }
 #pragma unroll
       for (int q = 0; q < C; ++q)
-        if (c0 + q < end) {
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            if (!act[g]) continue;
-            double y = ys[q][g];
-            if (is_sentinel(y)) y = wait_value_bo(&ysrc[IL(d, cols[q], sbase + 32 * g)], d.poll_ns);
-            acc[g] = __dsub_rn(acc[g], __dmul_rn(vs[q][g], y));
-          }
+        if (c0 + q < t.end) {
+          double y = ys[q];
+          if (is_sentinel(y)) y = wait_value_bo(&ysrc[IL(d, t.cols[q], sys)], d.poll_ns);
+          acc = __dsub_rn(acc, __dmul_rn(t.vs[q], y));
         }
 #pragma unroll
       for (int q = 0; q < C; ++q)
-        if (c0 + C + q < end) {
-          cols[q] = ncols[q];
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            vs[q][g] = nvs[q][g];
-            ys[q][g] = ld_relaxed_f64(&ysrc[IL(d, cols[q], sbase + 32 * g)]);
-          }
+        if (c0 + C + q < t.end) {
+          t.cols[q] = ncols[q];
+          t.vs[q] = nvs[q];
+          ys[q] = ld_relaxed_f64(&ysrc[IL(d, t.cols[q], sys)]);
         }
     }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      if (!act[g]) continue;
-      const int sys = sbase + 32 * g;
-      const double w = IS_U ? __ddiv_rn(acc[g], piv[g]) : acc[g];
-      st_relaxed_f64(&ysrc[IL(d, r, sys)], unsentinel(w));  // publish first
-      if (d.trace_trsv && sys == 0) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
-      st_relaxed_f64(&yres[IL(d, r, sys)], sentinel_value());
-      if (IS_U) {
-        xout[IL(d, d.col_perm[r], sys)] = w;
-        if (!isfinite(w)) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
-      }
+    const double w = IS_U ? __ddiv_rn(acc, t.piv) : acc;
+    st_relaxed_f64(&ysrc[IL(d, t.r, sys)], unsentinel(w));  // publish first
+    if (d.trace_trsv && sys == 0) d.trace_trsv[(IS_U ? d.n : 0) + t.r] = globaltimer();
+    st_relaxed_f64(&yres[IL(d, t.r, sys)], sentinel_value());
+    if (IS_U) {
+      xout[IL(d, d.col_perm[t.r], sys)] = w;
+      if (!isfinite(w)) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
     }
   }
 }
@@ -606,7 +601,7 @@ static cudaError_t b_launch_grid(const DevPlan &d, const double *b, double *x, i
   }
   const int groups = d.nbp >> 5;
   (void)groups;  // (G > 1 measured slower: fewer, longer tasks)
-  k_b_trsv_grid<IS_U, 1><<<grid_blocks, 256, 0, s>>>(d, b, x);
+  k_b_trsv_grid<IS_U><<<grid_blocks, 256, 0, s>>>(d, b, x);
   return cudaGetLastError();
 }
 
@@ -910,8 +905,8 @@ cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_
   occ((const void *)k_b_trsv_levels<true>);
   const int groups = nbp >> 5;  // occupancy of the variant b_launch_grid picks
   (void)groups;
-  occ((const void *)k_b_trsv_grid<false, 1>);
-  occ((const void *)k_b_trsv_grid<true, 1>);
+  occ((const void *)k_b_trsv_grid<false>);
+  occ((const void *)k_b_trsv_grid<true>);
   *trsv_blocks_per_sm = m;
   return e;
 }

@@ -163,6 +163,13 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.sweep_maxL = h.sweep_maxL;
   d.sweep_maxU = h.sweep_maxU;
   const size_t n = (size_t)h.n, B = (size_t)nbp;
+  {
+    const size_t biggest = std::max<size_t>({(size_t)h.nnz_a, (size_t)h.nnz_L, (size_t)h.nnz_U, n + 1});
+    if (biggest * B >= ((size_t)1 << 32)) {
+      destroy(dev);
+      return set_error(KKT_ERR_BAD_SHAPE, "batch too large: interleaved arrays exceed 2^32 elements");
+    }
+  }
   const size_t in_cap = (size_t)std::max(d.in_nnz, d.nnz_a);
   d.in_cap = (int64_t)in_cap;
   size_t bytes = 0;

@@ -89,8 +89,10 @@ struct DevPlan {
   const int *sys_mask = nullptr;
 };
 
+// 32-bit index arithmetic: kkt_dev_create rejects batches whose interleaved arrays exceed
+// 2^32 elements, so the product never wraps.
 __host__ __device__ __forceinline__ size_t IL(const DevPlan &d, int64_t i, int sys) {
-  return (size_t)i * d.nbp + sys;
+  return (size_t)((unsigned)i * (unsigned)d.nbp + (unsigned)sys);
 }
 
 // address of L value idx (CSC) of system sys in the batched layout (interleaved / heavy tail)
