@@ -21,6 +21,7 @@
 //                   fixed grids and fixed-order reductions (run-to-run deterministic).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "device.h"
@@ -57,19 +58,19 @@ __device__ __forceinline__ double patch_floor_b(const DevPlan &d, int sys) {
 }
 
 // ----------------------------------------------------------------------------
-// Values: caller layout [nb][in_cap] (general or symmetric-lower) -> A_vals [nnz_a][nbp],
+// Values: interleaved caller values [in_nnz][nbp] (general or symmetric-lower) -> A_vals [nnz_a][nbp],
 // plus per-system max|a|, ||A||_inf (general) and the operator norm (entry-order sums).
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_b_expand_norms(DevPlan d) {
   __shared__ double sh[BY][32];
   const int lane = threadIdx.x, sys = blockIdx.y * 32 + lane;
-  const double *in = d.in_vals + (size_t)(sys < d.nb ? sys : 0) * d.in_cap;
+  const double *in = d.in_il;  // [in_nnz][nbp] (b_launch_transpose of the caller's values)
   double mx = 0.0, sg = 0.0, op = 0.0;
   for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
     const int rb = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
     double g = 0.0, s1 = 0.0, s2 = 0.0;
     for (int p = rb; p < e; ++p) {
-      const double v = in[d.sym_lower ? d.gen_src[p] : p];
+      const double v = in[IL(d, d.sym_lower ? d.gen_src[p] : p, sys)];
       d.A_vals[IL(d, p, sys)] = v;
       const double a = fabs(v);
       g = __dadd_rn(g, a);
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(256) k_b_refactor_small(DevPlan d, int begin, 
       const double xk = x[m.x];
       for (int e = 0; e < m.y; ++e) {
         const int s = d.upd_slot[m.z + e];
-        x[s] = __dsub_rn(x[s], __dmul_rn(ldcg(lx_ptr(d, m.w + e, sys)), xk));
+        x[s] = __dsub_rn(x[s], __dmul_rn(ldcg(&d.Lx[IL(d, m.w + e, sys)]), xk));
       }
     }
     for (int s = 0; s < nu; ++s) {
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(256) k_b_refactor_small(DevPlan d, int begin, 
       gm = fmax(gm, fabs(v));
       const double l = unsentinel(__ddiv_rn(v, ujj));
       d.Lv[IL(d, d.Lmap[lb + s], sys)] = l;
-      *lx_ptr(d, lb + s, sys) = l;
+      d.Lx[IL(d, lb + s, sys)] = l;
     }
     d.udiag[IL(d, j, sys)] = ujj;
   }
@@ -213,7 +214,7 @@ __device__ __forceinline__ void chunk_issue(const DevPlan &d, const Chunk &c, do
     const int off = __shfl_sync(FULL, c.incl - c.m.y, i);
     const int lbk = __shfl_sync(FULL, c.m.w, i);
     for (int f = lane; f < (cnt << lgS); f += 32)
-      cp_async8(&stv[(off << lgS) + f], lx_ptr(d, lbk + (f >> lgS), sys0 + (f & (S - 1))));
+      cp_async8(&stv[(off << lgS) + f], &d.Lx[IL(d, lbk + (f >> lgS), sys0 + (f & (S - 1)))]);
   }
   const int pair0 = __shfl_sync(FULL, c.m.z, 0);
   for (int p = lane; p < c.npairs; p += 32) cp_async4(&sts[p], &d.upd_slot32[pair0 + p]);
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
             const int idx = idx0 + q * E;
             if (idx < cnt) {
               double l = lv[q];  // staged before L(:,k) was published?  wait for it
-              if (is_sentinel(l)) l = wait_value_bo(lx_ptr(d, lbk + idx, sys), d.poll_ns);
+              if (is_sentinel(l)) l = wait_value_bo(&d.Lx[IL(d, lbk + idx, sys)], d.poll_ns);
               x[sl[q]] = __dsub_rn(xv[q], __dmul_rn(l, xk));
             }
           }
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
     for (int idx = e; idx < nl; idx += E) {
       const double v = x[(nu + 1 + idx) * S + s];
       gm = fmax(gm, fabs(v));
-      st_relaxed_f64(lx_ptr(d, lb + idx, sys), unsentinel(__ddiv_rn(v, ujj)));
+      st_relaxed_f64(&d.Lx[IL(d, lb + idx, sys)], unsentinel(__ddiv_rn(v, ujj)));
     }
     for (int idx = e; idx < nl; idx += E)
       d.Lv[IL(d, d.Lmap[lb + idx], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + idx) * S + s], ujj));
@@ -378,6 +379,120 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
     PROF_MARK(5);
     if (prof && lane == 0 && d.trace_ref && my_task < 2 * d.n)
       d.trace_ref[my_task] = (unsigned long long)(clock64() - t_task);
+  }
+}
+
+
+// ----------------------------------------------------------------------------
+// Refactor, heavy tail (columns >= J0): one CTA per (column, 32 systems), pull form.
+// Column j's workspace slot r receives x[r] -= L(r,k) * x[k] for the k in so(j) with
+// r in L(:,k), in so(j) order (direct_lu.py:324-326).  Instead of replaying the steps one by
+// one with all lanes on one step, every slot accumulates its own updates in a register, in
+// exactly that order — so the arithmetic per (slot, system) is the reference's — with the
+// slots spread over the CTA's warps and lanes = the 32 systems (coalesced L loads, uniform
+// indices).  A U slot x[k] is a source for later slots only once complete: it publishes a
+// shared-memory flag; slots are processed in pull order (U slots in so(j) order first), so
+// every warp only ever waits on slots earlier in that order (deadlock-free).
+// ----------------------------------------------------------------------------
+constexpr int HW = 16;  // warps per heavy CTA
+
+size_t b_heavy_smem(int xp) {
+  return (size_t)xp * 32 * sizeof(double) + (size_t)xp * sizeof(int) + HW * 32 * sizeof(double) + 64;
+}
+
+__device__ __forceinline__ int ld_volatile_shared_i32(const int *p) {
+  return *reinterpret_cast<const volatile int *>(p);
+}
+
+__global__ void __launch_bounds__(32 * HW, 1) k_b_refactor_heavy(DevPlan d) {
+  extern __shared__ double hsm[];
+  double *x = hsm;                                           // [np][32]
+  double *red = x + (size_t)d.h_xp * 32;                     // [HW][32]
+  int *flag = reinterpret_cast<int *>(red + HW * 32);        // [np]
+  __shared__ int s_task;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ngroups = d.nbp >> 5;
+  const int ntask = d.nhc * ngroups;
+  while (true) {
+    if (threadIdx.x == 0) s_task = atomicAdd(d.ticket2, 1);
+    __syncthreads();
+    const int task = s_task;
+    if (task >= ntask) break;
+    const int hc = task / ngroups;
+    const int sys = (task - hc * ngroups) * 32 + lane;
+    const int j = d.hc_col[hc];
+    const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
+    const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
+    const int np = nu + 1 + nl;
+    const int o0 = d.hc_optr[hc];
+    for (int f = threadIdx.x; f < np * 32; f += 32 * HW) x[f] = 0.0;
+    for (int f = threadIdx.x; f < np; f += 32 * HW) flag[f] = 0;
+    __syncthreads();
+    // x[a_tgt] = avals[a_src]                                                 (:323)
+    for (int q = d.ap_ptr[j] + warp; q < d.ap_ptr[j + 1]; q += HW)
+      x[d.a_slot[q] * 32 + lane] = d.A_vals[IL(d, d.a_src[q], sys)];
+    __syncthreads();
+    for (int o = warp; o < np; o += HW) {
+      const int slot = d.h_ord[o0 + o];
+      const int p0 = d.h_pp[o0 + o], p1 = d.h_pp[o0 + o + 1];
+      double acc = x[slot * 32 + lane];
+      for (int p = p0; p < p1; p += 8) {
+        int2 pr[8];
+        double l[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (p + u < p1) pr[u] = d.h_pairs[p + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (p + u < p1) l[u] = ld_relaxed_f64(&d.Lx[IL(d, pr[u].y, sys)]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (p + u < p1) {
+            double lv = l[u];
+            if (is_sentinel(lv)) lv = wait_value_bo(&d.Lx[IL(d, pr[u].y, sys)], d.poll_ns);
+            while (ld_volatile_shared_i32(&flag[pr[u].x]) == 0) {
+            }
+            const double xk = ld_volatile_shared(&x[pr[u].x * 32 + lane]);
+            acc = __dsub_rn(acc, __dmul_rn(lv, xk));
+          }
+      }
+      x[slot * 32 + lane] = acc;
+      if (slot < nu) {  // a source of later slots: publish
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) *reinterpret_cast<volatile int *>(&flag[slot]) = 1;
+      }
+    }
+    __syncthreads();
+    // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj (published first); U(:,j) = x[Ui]  (:327-344)
+    double ujj = x[nu * 32 + lane];
+    double gm = fabs(ujj);
+    const double eps = patch_floor_b(d, sys);
+    const bool patched = fabs(ujj) < eps;
+    if (patched) ujj = (ujj >= 0.0) ? eps : -eps;
+    for (int i = warp; i < nl; i += HW) {
+      const double v = x[(nu + 1 + i) * 32 + lane];
+      gm = fmax(gm, fabs(v));
+      st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], unsentinel(__ddiv_rn(v, ujj)));
+    }
+    for (int i = warp; i < nl; i += HW)
+      d.Lv[IL(d, d.Lmap[lb + i], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + i) * 32 + lane], ujj));
+    for (int i = warp; i < nu; i += HW) {
+      const double v = x[i * 32 + lane];
+      d.Ux[IL(d, ub + i, sys)] = v;
+      d.Uv[IL(d, d.Umap[ub + i], sys)] = v;
+      gm = fmax(gm, fabs(v));
+    }
+    red[warp * 32 + lane] = gm;
+    __syncthreads();
+    if (warp == 0) {
+      for (int w = 1; w < HW; ++w) gm = fmax(gm, red[w * 32 + lane]);
+      d.udiag[IL(d, j, sys)] = ujj;
+      unsigned long long *sc = d.scal + (size_t)sys * SCAL_STRIDE;
+      if (patched) atomicAdd(&sc[SC_PATCHED], 1ull);
+      if (gm > 0.0 && dbits(gm) > __ldcg(&sc[SC_GMAX])) atomicMax(&sc[SC_GMAX], dbits(gm));
+    }
+    __syncthreads();
   }
 }
 
@@ -813,18 +928,19 @@ __global__ void __launch_bounds__(256) k_b_update_x(DevPlan d, double *__restric
 // Caller layout <-> interleaved (32 x 32 tiles through shared memory)
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_b_to_il(DevPlan d, const double *__restrict__ src,
-                                                 double *__restrict__ dst) {
+                                                 int64_t count, double *__restrict__ dst) {
   __shared__ double tile[32][33];
   const int g = blockIdx.y;
-  for (int i0 = blockIdx.x * 32; i0 < d.n; i0 += gridDim.x * 32) {
+  for (int64_t i0 = blockIdx.x * 32; i0 < count; i0 += (int64_t)gridDim.x * 32) {
     for (int q = threadIdx.y; q < 32; q += BY) {  // q: system within the group
-      const int sys = g * 32 + q, i = i0 + threadIdx.x;
-      if (i < d.n) tile[q][threadIdx.x] = src[(size_t)(sys < d.nb ? sys : 0) * d.n + i];
+      const int sys = g * 32 + q;
+      const int64_t i = i0 + threadIdx.x;
+      if (i < count) tile[q][threadIdx.x] = src[(size_t)(sys < d.nb ? sys : 0) * count + i];
     }
     __syncthreads();
     for (int q = threadIdx.y; q < 32; q += BY) {  // q: row within the tile
-      const int i = i0 + q;
-      if (i < d.n) dst[IL(d, i, g * 32 + threadIdx.x)] = tile[threadIdx.x][q];
+      const int64_t i = i0 + q;
+      if (i < count) dst[IL(d, i, g * 32 + threadIdx.x)] = tile[threadIdx.x][q];
     }
     __syncthreads();
   }
@@ -857,21 +973,6 @@ __global__ void k_b_broadcast(const double *__restrict__ src, int64_t count, int
     dst[f] = src[f / nbp];
 }
 
-__global__ void k_b_split_heavy(DevPlan d) {
-  const int64_t total = d.nLH * d.nbp;
-  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total;
-       f += (int64_t)gridDim.x * blockDim.x) {
-    const int sys = (int)(f / d.nLH);
-    const int64_t i = f - (int64_t)sys * d.nLH;
-    d.LxH[f] = d.Lx[IL(d, d.LH0 + i, sys)];
-  }
-}
-
-cudaError_t b_launch_split_heavy(const DevPlan &d, cudaStream_t s) {
-  if (d.nLH) k_b_split_heavy<<<4 * 148, 256, 0, s>>>(d);
-  return cudaGetLastError();
-}
-
 cudaError_t b_launch_broadcast(const double *src, int64_t count, int nbp, double *dst, cudaStream_t s) {
   if (count) k_b_broadcast<<<4 * 148, 256, 0, s>>>(src, count, nbp, dst);
   return cudaGetLastError();
@@ -889,6 +990,8 @@ static const dim3 ROW_BLOCK(32, BY);
 cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm) {
   const int sm = (int)refactor_smem;
   cudaError_t e = cudaFuncSetAttribute(k_b_refactor, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_b_refactor_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize, B_HEAVY_SMEM_MAX);
   // the occupancy is shared-memory bound: ask for the largest carveout
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_b_refactor, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -920,8 +1023,7 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, cudaStr
   if (!d.n) return cudaSuccess;
   // (KKT_NO_RESET=1, diagnostics only: keep the previous factors so no task ever waits)
   static const bool no_reset = std::getenv("KKT_NO_RESET") != nullptr;
-  cudaError_t e = no_reset ? cudaSuccess : cudaMemsetAsync(d.Lx, 0xFF, 8 * (size_t)d.LH0 * d.nbp, s);
-  if (e == cudaSuccess && d.nLH && !no_reset) e = cudaMemsetAsync(d.LxH, 0xFF, 8 * (size_t)d.nLH * d.nbp, s);
+  cudaError_t e = no_reset ? cudaSuccess : cudaMemsetAsync(d.Lx, 0xFF, 8 * (size_t)d.nnz_L * d.nbp, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d.ticket, 0, 4, s);
   if (e != cudaSuccess) return e;
   for (int l = 0; l < d.n_small_levels; ++l) {
@@ -936,6 +1038,12 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, cudaStr
   if (d.n_btask) {
     if (d.prof) cudaMemsetAsync(d.prof, 0, 8 * 8 * (size_t)blocks * B_WARPS, s);
     k_b_refactor<<<blocks, 32 * B_WARPS, smem, s>>>(d);
+    ++*launches;
+  }
+  if (d.nhc) {  // the heavy tail depends only on earlier columns: a kernel boundary suffices
+    cudaError_t e2 = cudaMemsetAsync(d.ticket2, 0, 4, s);
+    if (e2 != cudaSuccess) return e2;
+    k_b_refactor_heavy<<<148, 32 * HW, b_heavy_smem(d.h_xp), s>>>(d);
     ++*launches;
   }
   return cudaGetLastError();
@@ -962,7 +1070,14 @@ cudaError_t b_launch_resid_stats(const DevPlan &d, const double *r, const double
 }
 
 cudaError_t b_launch_to_il(const DevPlan &d, const double *src, double *dst, cudaStream_t s) {
-  if (d.n) k_b_to_il<<<dim3((unsigned)min((d.n + 31) / 32, 1184), d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, src, dst);
+  return b_launch_transpose(d, src, d.n, dst, s);
+}
+
+cudaError_t b_launch_transpose(const DevPlan &d, const double *src, int64_t count, double *dst,
+                               cudaStream_t s) {
+  if (count > 0)
+    k_b_to_il<<<dim3((unsigned)std::min<int64_t>((count + 31) / 32, 2368), d.nbp >> 5), ROW_BLOCK, 0, s>>>(
+        d, src, count, dst);
   return cudaGetLastError();
 }
 

@@ -73,7 +73,8 @@ static int build_batch_tasks(const HostPlan &h, int nbp, int xbudget, int J0, st
     for (int64_t t = h.so_ptr[j]; t < h.so_ptr[j + 1]; ++t) pairs += h.so_meta[4 * t + 1];
     int S = 32;
     while (S > 1 && np * S > xbudget) S >>= 1;
-    if (pairs > hi || j >= J0) S = 1;  // heavy tail: one system per warp (LxH)
+    if (j >= J0) continue;  // heavy tail: k_b_refactor_heavy
+    if (pairs > hi) S = 1;
     else if (pairs > mid) S = std::min(S, 4);
     else if (pairs > lo) S = std::min(S, 8);
     int lg = 0;
@@ -81,6 +82,52 @@ static int build_batch_tasks(const HostPlan &h, int nbp, int xbudget, int J0, st
     for (int s0 = 0; s0 < nbp; s0 += S) tasks.push_back(make_int2(j, (s0 << 8) | lg));
   }
   if (tasks.size() >= (size_t)INT32_MAX) return set_error(KKT_ERR_BAD_SHAPE, "too many batched tasks");
+  return KKT_OK;
+}
+
+// Heavy tail tables (k_b_refactor_heavy): for every column j >= J0 past the thread-per-
+// column levels, in DAG-level order: its workspace slots in pull order (U slots in the
+// topological so(j) order, the diagonal, the L slots) and, per slot, the updates it
+// receives {source slot, L index} in the reference's step order.
+struct HeavyPlan {
+  std::vector<int> col, optr, pp;
+  std::vector<uint16_t> ord;
+  std::vector<int2> pairs;
+  int xp = 0;
+};
+
+static int build_heavy(const HostPlan &h, int J0, HeavyPlan &H) {
+  const int start = h.small_lev_ptr[h.n_small_levels];
+  H = HeavyPlan();
+  H.optr.assign(1, 0);
+  H.pp.assign(1, 0);
+  std::vector<std::vector<int2>> lists;
+  for (int c = start; c < h.n; ++c) {
+    const int j = h.col_order[c];
+    if (j < J0) continue;
+    const int nu = (int)(h.Up[j + 1] - h.Up[j]), nl = (int)(h.Lp[j + 1] - h.Lp[j]);
+    const int np = nu + 1 + nl;
+    H.col.push_back(j);
+    H.xp = std::max(H.xp, np);
+    lists.assign(np, {});
+    for (int64_t t = h.so_ptr[j]; t < h.so_ptr[j + 1]; ++t) {
+      const int k = h.so_data[t], kslot = h.so_slot[t];
+      const int64_t p0 = h.upd_ptr[t];
+      for (int64_t e = 0; e < h.Lp[k + 1] - h.Lp[k]; ++e)
+        lists[h.upd_slot[p0 + e]].push_back(make_int2(kslot, (int)(h.Lp[k] + e)));
+    }
+    auto emit = [&](int slot) {
+      H.ord.push_back((uint16_t)slot);
+      H.pairs.insert(H.pairs.end(), lists[slot].begin(), lists[slot].end());
+      H.pp.push_back((int)H.pairs.size());
+    };
+    for (int64_t t = h.so_ptr[j]; t < h.so_ptr[j + 1]; ++t) emit(h.so_slot[t]);
+    for (int s = nu; s < np; ++s) emit(s);
+    if ((int)H.ord.size() - H.optr.back() != np)
+      return set_error(KKT_ERR_BAD_SHAPE, "heavy plan: U pattern and so(j) disagree");
+    H.optr.push_back((int)H.ord.size());
+  }
+  if (H.pairs.size() >= (size_t)INT32_MAX) return set_error(KKT_ERR_BAD_SHAPE, "heavy plan too large");
   return KKT_OK;
 }
 
@@ -117,6 +164,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   // the SMs several times over whatever the number of 32-system groups
   d.rb = nb == 1 ? RED_BLOCKS : std::max(64, 8 * 148 / (nbp / 32));
   std::vector<int2> btask;
+  HeavyPlan heavy;
   d.b_xbudget = B_XBUDGET;
   d.b_stage = B_STAGE;  // doubles per stage buffer (two buffers per warp)
   if (const char *e = std::getenv("KKT_B_SMEM")) std::sscanf(e, "%d,%d", &d.b_xbudget, &d.b_stage);
@@ -124,16 +172,19 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.b_xbudget = std::max(d.b_xbudget, h.maxpat);
   if (nb > 1) {
     // heavy tail: from the first column whose pattern exceeds KKT_B_HEAVY_NP slots
-    const int heavy_np = std::getenv("KKT_B_HEAVY_NP") ? std::atoi(std::getenv("KKT_B_HEAVY_NP")) : 256;
+    const int heavy_np = std::getenv("KKT_B_HEAVY_NP") ? std::atoi(std::getenv("KKT_B_HEAVY_NP")) : 0;
     d.J0 = h.n;
     for (int j = 0; j < h.n; ++j)
       if (heavy_np > 0 && (h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j]) > heavy_np) {
         d.J0 = j;
         break;
       }
-    d.LH0 = h.Lp[d.J0];
-    d.nLH = h.nnz_L - d.LH0;
-    int rc2 = build_batch_tasks(h, nbp, d.b_xbudget, d.J0, btask);
+    int rc2 = build_heavy(h, d.J0, heavy);
+    if (rc2 == KKT_OK && b_heavy_smem(heavy.xp) > B_HEAVY_SMEM_MAX) {  // too wide for one CTA
+      d.J0 = h.n;
+      rc2 = build_heavy(h, d.J0, heavy);
+    }
+    if (rc2 == KKT_OK) rc2 = build_batch_tasks(h, nbp, d.b_xbudget, d.J0, btask);
     if (rc2 != KKT_OK) {
       delete dev;
       return rc2;
@@ -176,6 +227,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   auto acc = [&](size_t b) { bytes += align_up(b + 1); };
   acc(4 * (n + 1)); acc(4 * d.nnz_a); acc(4 * n); acc(4 * d.nnz_a);  // A_rp ci split gen_src
   acc(8 * in_cap * nb); acc(8 * d.nnz_a * B);                        // in_vals A_vals
+  if (nbp > 1) acc(8 * in_cap * B);                                    // in_il
   acc(4 * (n + 1)); acc(4 * (n + 1)); acc(4 * d.n_ap); acc(4 * n);   // so_ptr ap_ptr a_src order
   acc(4 * (n + 1)); acc(4 * (n + 1)); acc(4 * d.nnz_L); acc(4 * d.nnz_U);  // Lp Up Lmap Umap
   acc(4 * d.n_upd); acc(16 * d.n_so); acc(2 * d.n_upd); acc(2 * d.n_ap);   // lidx meta slots
@@ -191,7 +243,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   acc(8 * SCAL_STRIDE * B); acc(64); acc(8 * 8 * (size_t)d.rb * B);        // scal ticket partials
   acc(8 * btask.size());                                                   // batched tasks
   acc(4 * h.L_glev_ptr.size()); acc(4 * h.U_glev_ptr.size()); acc(64);     // levels, barrier
-  acc(8 * (size_t)d.nLH * B);                                              // LxH
+  acc(4 * heavy.col.size()); acc(4 * heavy.optr.size()); acc(4 * heavy.pp.size());
+  acc(2 * heavy.ord.size()); acc(8 * heavy.pairs.size()); acc(64);          // heavy tail
   for (const HostSweep *hs : {&h.swL, &h.swU}) {
     acc(4 * hs->dptr.size()); acc(4 * hs->dsrc.size()); acc(2 * hs->ddst.size());
     acc(4 * hs->dmask.size()); acc(4 * hs->bptr.size()); acc(4 * hs->brow.size());
@@ -209,6 +262,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.A_split = carve<int>(cur, n);
   d.gen_src = carve<int>(cur, d.nnz_a);
   d.in_vals = carve<double>(cur, in_cap * nb);
+  if (nbp > 1) d.in_il = carve<double>(cur, in_cap * B);
   d.A_vals = carve<double>(cur, d.nnz_a * B);
   d.so_ptr = carve<int>(cur, n + 1);
   d.ap_ptr = carve<int>(cur, n + 1);
@@ -256,7 +310,14 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.L_nglev = (int)h.L_glev_ptr.size() - 1;
   d.U_nglev = (int)h.U_glev_ptr.size() - 1;
   d.b_levelsync = std::getenv("KKT_B_LEVELSYNC") ? std::atoi(std::getenv("KKT_B_LEVELSYNC")) : 0;
-  d.LxH = carve<double>(cur, (size_t)d.nLH * B);
+  d.nhc = (int)heavy.col.size();
+  d.h_xp = heavy.xp;
+  d.hc_col = carve<int>(cur, heavy.col.size());
+  d.hc_optr = carve<int>(cur, heavy.optr.size());
+  d.h_pp = carve<int>(cur, heavy.pp.size());
+  d.h_ord = carve<uint16_t>(cur, heavy.ord.size());
+  d.h_pairs = carve<int2>(cur, heavy.pairs.size());
+  d.ticket2 = carve<int>(cur, 16);
   {
     const HostSweep *hs[2] = {&h.swL, &h.swU};
     SweepDev *sd[2] = {&d.swL, &d.swU};
@@ -325,6 +386,11 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   UP(d.Ui, h.Ui32);
   UP(d.Ltail_split, h.Ltail_split);
   UP(d.btask, btask);
+  UP(d.hc_col, heavy.col);
+  UP(d.hc_optr, heavy.optr);
+  UP(d.h_pp, heavy.pp);
+  UP(d.h_ord, heavy.ord);
+  UP(d.h_pairs, heavy.pairs);
   UP(d.L_glev, h.L_glev_ptr);
   UP(d.U_glev, h.U_glev_ptr);
   CUDA_TRY(cudaMemsetAsync(d.gbar, 0, 64, dev->stream));
@@ -365,7 +431,6 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
         if (ce != cudaSuccess) break;
       }
       cudaFree(tmp);
-      if (ce == cudaSuccess) ce = b_launch_split_heavy(d, dev->stream);
       if (ce != cudaSuccess) {
         destroy(dev);
         return set_error(KKT_ERR_CUDA, std::string("initial factors: ") + cudaGetErrorString(ce));
@@ -428,9 +493,18 @@ static int set_values(Device *dev, const double *vals, int layout, int on_device
   d.sym_lower = layout == KKT_LAYOUT_SYMMETRIC_LOWER ? 1 : 0;
   const int64_t cnt = d.sym_lower ? d.in_nnz : d.nnz_a;
   // values_in is [nb][cnt]; the device copy has a per-system pitch of in_cap
-  CUDA_TRY(cudaMemcpy2DAsync(d.in_vals, 8 * (size_t)d.in_cap, vals, 8 * (size_t)cnt, 8 * (size_t)cnt,
-                             (size_t)d.nb, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                             dev->stream));
+  if (d.nbp > 1) {  // batched: transpose straight from the caller's device values
+    const double *src = vals;
+    if (!on_device) {
+      CUDA_TRY(cudaMemcpyAsync(d.in_vals, vals, 8 * (size_t)cnt * d.nb, cudaMemcpyHostToDevice, dev->stream));
+      src = d.in_vals;
+    }
+    LAUNCH(b_launch_transpose(d, src, cnt, d.in_il, dev->stream));
+  } else {
+    CUDA_TRY(cudaMemcpy2DAsync(d.in_vals, 8 * (size_t)d.in_cap, vals, 8 * (size_t)cnt, 8 * (size_t)cnt,
+                               (size_t)d.nb, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                               dev->stream));
+  }
   LAUNCH(launch_reset_scal(d, 0, dev->stream));
   LAUNCH(d.nbp > 1 ? b_launch_expand_norms(d, dev->stream) : launch_expand_norms(d, dev->stream));
   return KKT_OK;
@@ -679,14 +753,6 @@ int kkt_dev_download_factors(kkt_device *d, double *Lx, double *Ux, double *Udia
       if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
       for (size_t q = 0; q < nb; ++q)
         for (size_t i = 0; i < a.cnt; ++i) a.dst[q * a.cnt + i] = tmp[i * nbp + q];
-    }
-    if (Lx && p.nLH) {  // the heavy tail of L is system-major
-      std::vector<double> tmp((size_t)p.nLH * nbp);
-      e = cudaMemcpyAsync(tmp.data(), p.LxH, 8 * tmp.size(), cudaMemcpyDeviceToHost, s);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-      if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
-      for (size_t q = 0; q < nb; ++q)
-        for (int64_t i = 0; i < p.nLH; ++i) Lx[q * p.nnz_L + p.LH0 + i] = tmp[q * p.nLH + i];
     }
     return KKT_OK;
   }

@@ -39,13 +39,16 @@ struct DevPlan {
   int2 *btask = nullptr;  // batched refactor tasks {column, sys0 << 8 | log2(systems)}
   int n_btask = 0;
   int b_xbudget = 0, b_stage = 0, b_static = 0;
-  // Heavy tail (columns >= J0, the dense separator): its L columns are consumed only by
-  // columns >= J0, whose tasks run one system per warp with lanes over entries, so those
-  // L values are stored system-major ([nbp][nLH], LxH) for coalesced access; the rest of
-  // Lx stays interleaved.
+  // Heavy tail (columns >= J0, the dense separator; batched only): refactorized by a CTA per
+  // (column, 32 systems) in "pull" form (k_b_refactor_heavy): every workspace slot sums its
+  // own updates in the reference order, the slots spread over the CTA's warps, U slots
+  // signal readiness through shared-memory flags.
   int J0 = 0x7fffffff;
-  int64_t LH0 = 0, nLH = 0;
-  double *LxH = nullptr;  // per-warp shared workspace / stage (doubles), k_b_refactor
+  int nhc = 0, h_xp = 0;                   // heavy columns, their largest pattern
+  int *hc_col = nullptr, *hc_optr = nullptr, *h_pp = nullptr;
+  uint16_t *h_ord = nullptr;               // per heavy column: slots in pull order
+  int2 *h_pairs = nullptr;                 // {source slot, L index}, slot-major, step order
+  int *ticket2 = nullptr;
   unsigned long long *prof = nullptr;  // optional per-warp cycle counters (KKT_TRACE, batched)
   int rb = RED_BLOCKS;  // reduction blocks per system
   int64_t nnz_a = 0, in_nnz = 0, in_cap = 0, nnz_L = 0, nnz_U = 0, n_so = 0, n_upd = 0, n_ap = 0;
@@ -57,6 +60,7 @@ struct DevPlan {
   // operator (pattern shared; values per system)
   int *A_rp, *A_ci, *A_split, *gen_src;
   double *in_vals, *A_vals;                 // [nb][in_cap], [nb][nnz_a]
+  double *in_il = nullptr;                  // batched: caller values interleaved [in_cap][nbp]
   // refactor (schedule shared)
   int *so_ptr, *ap_ptr, *a_src, *col_order, *Lp, *Up, *Lmap, *Umap, *upd_lidx;
   int4 *so_meta;
@@ -93,11 +97,6 @@ struct DevPlan {
 // 2^32 elements, so the product never wraps.
 __host__ __device__ __forceinline__ size_t IL(const DevPlan &d, int64_t i, int sys) {
   return (size_t)((unsigned)i * (unsigned)d.nbp + (unsigned)sys);
-}
-
-// address of L value idx (CSC) of system sys in the batched layout (interleaved / heavy tail)
-__device__ __forceinline__ double *lx_ptr(const DevPlan &d, int64_t idx, int sys) {
-  return idx >= d.LH0 ? d.LxH + (size_t)sys * d.nLH + (idx - d.LH0) : d.Lx + IL(d, idx, sys);
 }
 
 __device__ __forceinline__ bool sys_active(const DevPlan &d, int sys) {
@@ -177,8 +176,11 @@ cudaError_t b_launch_resid_stats(const DevPlan &d, const double *r, const double
 // [nb][n] (system-major, caller layout) <-> [n][nbp] (interleaved); padding <- system 0
 cudaError_t b_launch_to_il(const DevPlan &d, const double *src, double *dst, cudaStream_t s);
 cudaError_t b_launch_from_il(const DevPlan &d, const double *src, double *dst, cudaStream_t s);
+cudaError_t b_launch_transpose(const DevPlan &d, const double *src, int64_t count, double *dst,
+                               cudaStream_t s);  // [nb][count] -> [count][nbp]
 cudaError_t b_launch_broadcast(const double *src, int64_t count, int nbp, double *dst, cudaStream_t s);
-cudaError_t b_launch_split_heavy(const DevPlan &d, cudaStream_t s);  // LxH <- Lx (heavy part)
+constexpr int B_HEAVY_SMEM_MAX = 200 * 1024;  // dynamic shared memory of k_b_refactor_heavy
+size_t b_heavy_smem(int xp);
 // FGMRES vector kernels on interleaved [n][nbp] vectors (partials [nbp][nvec][rb])
 cudaError_t b_launch_dots(const DevPlan &d, const double *V, int nvec, const double *w,
                           const int *mask, double *partials, cudaStream_t s);
