@@ -374,6 +374,16 @@ def main():
              "spmv": t_spmv * (max_iters + 3)}
     dom = max(share, key=share.get)
     kd = kern[dom]
+    # DRAM traffic of the dominant kernel family from the committed ncu --set full capture
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r1c_ncu_traffic.json")
+    if os.path.exists(tp):
+        tk = json.load(open(tp))["kernels"]
+        fam = {"refactor": ["k_b_refactor"], "spmv": ["k_b_spmv"],
+               "trisolve_pair": ["k_b_trsv_grid<0>", "k_b_trsv_grid<1>", "k_trsv_blocked<0, 1, 1>",
+                                 "k_trsv_blocked<1, 1, 1>"]}[dom]
+        if all(k in tk for k in fam):
+            traffic = sum(tk[k]["dram_read_bytes"] + tk[k]["dram_write_bytes"] for k in fam)
 
     # ---- single-system latency (B = 1 handle, sequence systems in order) ----
     single = None
@@ -447,7 +457,8 @@ def main():
                     "h2d_bytes_per_step": 8 * B * (nnz_lower + N),
                     "d2h_bytes_per_step": 8 * B * N},
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": kd["GBs"], "peak": peak,
-                         "unit": "GB/s", "frac": kd["GBs"] / peak, "traffic": None,
+                         "unit": "GB/s", "frac": kd["GBs"] / peak, "traffic": traffic,
+                         "algorithmic_bytes": kd["bytes"],
                          "peak_kind": peak_kind,
                          "note": "refactor/trisolve are DAG-latency bound per system; the "
                                  "batch amortises the chain (DESIGN.md §5)"},
