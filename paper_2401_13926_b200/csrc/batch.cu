@@ -225,11 +225,11 @@ struct TaskInfo {
   int j, lgS, sys0, ub, nu, lb, nl, t0, t_end, a0, a1;
 };
 
-__device__ __forceinline__ TaskInfo load_task(const DevPlan &d, int task) {
+__device__ __forceinline__ TaskInfo load_task(const DevPlan &d, const int2 *tasks, int ntask, int task) {
   TaskInfo t;
   t.j = -1;
-  if (task >= d.n_btask) return t;
-  const int2 tk = d.btask[task];
+  if (task >= ntask) return t;
+  const int2 tk = tasks[task];
   t.j = tk.x;
   t.lgS = tk.y & 0xff;
   t.sys0 = tk.y >> 8;
@@ -244,10 +244,10 @@ __device__ __forceinline__ TaskInfo load_task(const DevPlan &d, int task) {
   return t;
 }
 
-__global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
+__global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d, const int2 *__restrict__ tasks,
+                                                           int ntask, int XB, int STG) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
-  const int XB = d.b_xbudget, STG = d.b_stage;
   double *x = smem + (size_t)(threadIdx.x >> 5) * (XB + 3 * STG);
   double *stv0 = x + XB;                                   // [2][STG] staged L values
   int *sts0 = reinterpret_cast<int *>(stv0 + 2 * STG);     // [2][STG] staged slots
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   int ticket = gw;
   if (!d.b_static && lane == 0) ticket = atomicAdd(d.ticket, 1);
-  TaskInfo nt = load_task(d, __shfl_sync(FULL, ticket, 0));
+  TaskInfo nt = load_task(d, tasks, ntask, __shfl_sync(FULL, ticket, 0));
   int cur_task = __shfl_sync(FULL, ticket, 0);
   while (nt.j >= 0) {
     const TaskInfo ti = nt;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
       x[d.a_slot[q] * S + s] = d.A_vals[IL(d, d.a_src[q], sys)];
     __syncwarp();
     cur_task = __shfl_sync(FULL, ticket, 0);
-    nt = load_task(d, cur_task);  // consumed next iteration
+    nt = load_task(d, tasks, ntask, cur_task);  // consumed next iteration
     PROF_MARK(1);
     // for k in so(j) (topological): x[Li(k)] -= Lx(k) * x[k]                  (:324-326)
     while (cur.t0 < t_end) {
@@ -377,11 +377,155 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d) {
     }
     __syncwarp();
     PROF_MARK(5);
-    if (prof && lane == 0 && d.trace_ref && my_task < 2 * d.n)
-      d.trace_ref[my_task] = (unsigned long long)(clock64() - t_task);
+    if (prof && lane == 0 && d.trace_ref && my_task < d.n) {  // {duration, end time}
+      d.trace_ref[2 * my_task] = (unsigned long long)(clock64() - t_task);
+      d.trace_ref[2 * my_task + 1] = globaltimer();
+    }
   }
 }
 
+
+
+// ----------------------------------------------------------------------------
+// Refactor, wide separator columns (j >= J2; second launch): a CTA of 4 warps per
+// (column, SC = 4 systems).  Thread t serves entry lane e = t / SC and system s = t % SC, so
+// a warp access is 8 entries x 4 systems = 8 full 32-byte sectors (the one-system-per-warp
+// replay reads 8 bytes per sector) and a step's entries are spread over 32 entry lanes per
+// system; the steps of so(j) are separated by a 128-thread barrier.  The workspace x[np][SC]
+// and two cp.async stage buffers are shared by the CTA.  Same per-entry order as k_refactor.
+// ----------------------------------------------------------------------------
+constexpr int CT_SC = 4;                 // systems per CTA task
+constexpr int CT_THREADS = 32 * CT_SC;   // 32 entry lanes x SC systems
+constexpr int CT_STAGE = 256;            // update pairs per stage buffer
+
+size_t b_cta_smem(int xp) {
+  return ((size_t)xp * CT_SC + 2 * (size_t)CT_STAGE * CT_SC) * sizeof(double) +
+         2 * (size_t)CT_STAGE * sizeof(int) + 64;
+}
+
+__global__ void __launch_bounds__(CT_THREADS) k_b_refactor_cta(DevPlan d, const int2 *__restrict__ tasks,
+                                                               int ntask) {
+  extern __shared__ double csm[];
+  __shared__ int s_task;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int e = tid / CT_SC, s = tid % CT_SC;
+  double *x = csm;                                          // [xp][SC]
+  double *stv0 = x + (size_t)d.h_xp * CT_SC;                // [2][STAGE][SC]
+  int *sts0 = reinterpret_cast<int *>(stv0 + 2 * CT_STAGE * CT_SC);  // [2][STAGE]
+  while (true) {
+    if (tid == 0) s_task = atomicAdd(d.ticket2, 1);
+    __syncthreads();
+    const int task = s_task;
+    if (task >= ntask) break;
+    const int2 tk = tasks[task];
+    const int j = tk.x, sys0 = tk.y >> 8, sys = sys0 + s;
+    const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
+    const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
+    const int np = nu + 1 + nl;
+    const int t_end = d.so_ptr[j + 1];
+    // first chunk in flight before the A scatter (every warp computes the chunk metadata)
+    Chunk cur = chunk_meta(d, d.so_ptr[j], 0, t_end, CT_STAGE, lane);
+    auto issue = [&](const Chunk &c, int b) {
+      double *stv = stv0 + b * CT_STAGE * CT_SC;
+      int *sts = sts0 + b * CT_STAGE;
+      for (int i = 0; i < c.nsteps; ++i) {
+        const int cnt = __shfl_sync(FULL, c.m.y, i);
+        const int off = __shfl_sync(FULL, c.incl - c.m.y, i);
+        const int lbk = __shfl_sync(FULL, c.m.w, i);
+        for (int f = tid; f < cnt * CT_SC; f += CT_THREADS)
+          cp_async8(&stv[off * CT_SC + f], &d.Lx[IL(d, lbk + f / CT_SC, sys0 + f % CT_SC)]);
+      }
+      const int pair0 = __shfl_sync(FULL, c.m.z, 0);
+      for (int p = tid; p < c.npairs; p += CT_THREADS) cp_async4(&sts[p], &d.upd_slot32[pair0 + p]);
+      cp_async_commit();
+    };
+    issue(cur, 0);
+    int buf = 0;
+    for (int f = tid; f < np * CT_SC; f += CT_THREADS) x[f] = 0.0;
+    __syncthreads();
+    for (int q = d.ap_ptr[j] + e; q < d.ap_ptr[j + 1]; q += 32)
+      x[d.a_slot[q] * CT_SC + s] = d.A_vals[IL(d, d.a_src[q], sys)];
+    while (cur.t0 < t_end) {
+      Chunk nxt;
+      nxt.t0 = cur.next_t0;
+      if (nxt.t0 < t_end) {
+        nxt = chunk_meta(d, cur.next_t0, cur.next_e0, t_end, CT_STAGE, lane);
+        issue(nxt, buf ^ 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();  // staged chunk visible; A scatter / previous step done
+      const double *stv = stv0 + buf * CT_STAGE * CT_SC;
+      const int *sts = sts0 + buf * CT_STAGE;
+      for (int i = 0; i < cur.nsteps; ++i) {
+        const int kslot = __shfl_sync(FULL, cur.m.x, i);
+        const int cnt = __shfl_sync(FULL, cur.m.y, i);
+        const int off = __shfl_sync(FULL, cur.incl - cur.m.y, i);
+        const int lbk = __shfl_sync(FULL, cur.m.w, i);
+        const double xk = x[kslot * CT_SC + s];
+        for (int idx0 = e; idx0 < cnt; idx0 += 4 * 32) {
+          double lv[4], xv[4];
+          int sl[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int idx = idx0 + 32 * q;
+            if (idx < cnt) {
+              lv[q] = stv[(off + idx) * CT_SC + s];
+              sl[q] = sts[off + idx] * CT_SC + s;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (idx0 + 32 * q < cnt) xv[q] = x[sl[q]];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int idx = idx0 + 32 * q;
+            if (idx < cnt) {
+              double l = lv[q];
+              if (is_sentinel(l)) l = wait_value_bo(&d.Lx[IL(d, lbk + idx, sys)], d.poll_ns);
+              x[sl[q]] = __dsub_rn(xv[q], __dmul_rn(l, xk));
+            }
+          }
+        }
+        __syncthreads();  // x[k] of the next step may have been updated in this one
+      }
+      cur = nxt;
+      buf ^= 1;
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj (published first); U(:,j) = x[Ui]  (:327-344)
+    double ujj = x[nu * CT_SC + s];
+    double gm = fabs(ujj);
+    const double eps = patch_floor_b(d, sys);
+    const bool patched = fabs(ujj) < eps;
+    if (patched) ujj = (ujj >= 0.0) ? eps : -eps;
+    for (int i = e; i < nl; i += 32) {
+      const double v = x[(nu + 1 + i) * CT_SC + s];
+      gm = fmax(gm, fabs(v));
+      st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], unsentinel(__ddiv_rn(v, ujj)));
+    }
+    for (int i = e; i < nl; i += 32)
+      d.Lv[IL(d, d.Lmap[lb + i], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + i) * CT_SC + s], ujj));
+    for (int i = e; i < nu; i += 32) {
+      const double v = x[i * CT_SC + s];
+      d.Ux[IL(d, ub + i, sys)] = v;
+      d.Uv[IL(d, d.Umap[ub + i], sys)] = v;
+      gm = fmax(gm, fabs(v));
+    }
+    for (int o = CT_SC; o < 32; o <<= 1) gm = fmax(gm, __shfl_xor_sync(FULL, gm, o));
+    if (lane < CT_SC) {  // one lane per system and warp: warp-level maxima are order-free
+      unsigned long long *sc = d.scal + (size_t)sys * SCAL_STRIDE;
+      if (tid < CT_SC) {
+        d.udiag[IL(d, j, sys)] = ujj;
+        if (patched) atomicAdd(&sc[SC_PATCHED], 1ull);
+      }
+      if (gm > 0.0 && dbits(gm) > __ldcg(&sc[SC_GMAX])) atomicMax(&sc[SC_GMAX], dbits(gm));
+    }
+    __syncthreads();
+  }
+}
 
 // ----------------------------------------------------------------------------
 // Refactor, heavy tail (columns >= J0): one CTA per (column, 32 systems), pull form.
@@ -1019,7 +1163,22 @@ cudaError_t b_launch_expand_norms(const DevPlan &d, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, cudaStream_t s, long long *launches) {
+cudaError_t b_refactor_occupancy(size_t smem, int *blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor, 32 * B_WARPS, smem);
+}
+
+cudaError_t b_cta_configure(size_t smem, int *blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_b_refactor_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_b_refactor_cta, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_cta, CT_THREADS, smem);
+  return e;
+}
+
+cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blocks2, size_t smem2,
+                              cudaStream_t s, long long *launches) {
   if (!d.n) return cudaSuccess;
   // (KKT_NO_RESET=1, diagnostics only: keep the previous factors so no task ever waits)
   static const bool no_reset = std::getenv("KKT_NO_RESET") != nullptr;
@@ -1035,9 +1194,15 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, cudaStr
       ++*launches;
     }
   }
-  if (d.n_btask) {
+  if (d.n_btask1) {
     if (d.prof) cudaMemsetAsync(d.prof, 0, 8 * 8 * (size_t)blocks * B_WARPS, s);
-    k_b_refactor<<<blocks, 32 * B_WARPS, smem, s>>>(d);
+    k_b_refactor<<<blocks, 32 * B_WARPS, smem, s>>>(d, d.btask, d.n_btask1, d.b_xbudget, d.b_stage);
+    ++*launches;
+  }
+  if (d.n_btask > d.n_btask1) {  // the wide separator columns (depend only on earlier ones)
+    cudaError_t e2 = cudaMemsetAsync(d.ticket2, 0, 4, s);
+    if (e2 != cudaSuccess) return e2;
+    k_b_refactor_cta<<<blocks2, CT_THREADS, smem2, s>>>(d, d.btask + d.n_btask1, d.n_btask - d.n_btask1);
     ++*launches;
   }
   if (d.nhc) {  // the heavy tail depends only on earlier columns: a kernel boundary suffices

@@ -59,13 +59,14 @@ static void destroy(Device *dev) {
 // the per-column critical path (lanes over entries): the workspace x[np][S] must fit the
 // per-warp budget, and heavy columns (many update pairs) get more entry lanes.
 // KKT_B_SCHED="lo,mid,hi" overrides the pair thresholds for S <= 8 / 4 / 1.
-static int build_batch_tasks(const HostPlan &h, int nbp, int xbudget, int J0, std::vector<int2> &tasks) {
+static int build_batch_tasks(const HostPlan &h, int nbp, int xbudget, int jlo, int jhi,
+                             std::vector<int2> &tasks) {
   int lo = 1 << 30, mid = 1 << 30, hi = 1 << 30;  // default: S from the workspace only
   if (const char *e = std::getenv("KKT_B_SCHED")) std::sscanf(e, "%d,%d,%d", &lo, &mid, &hi);
   const int start = h.small_lev_ptr[h.n_small_levels];
-  tasks.clear();
   for (int c = start; c < h.n; ++c) {
     const int j = h.col_order[c];
+    if (j < jlo || j >= jhi) continue;
     const int64_t np = (h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j]);
     if (np > xbudget)
       return set_error(KKT_ERR_BAD_SHAPE, "column pattern too large for the batched workspace");
@@ -73,7 +74,6 @@ static int build_batch_tasks(const HostPlan &h, int nbp, int xbudget, int J0, st
     for (int64_t t = h.so_ptr[j]; t < h.so_ptr[j + 1]; ++t) pairs += h.so_meta[4 * t + 1];
     int S = 32;
     while (S > 1 && np * S > xbudget) S >>= 1;
-    if (j >= J0) continue;  // heavy tail: k_b_refactor_heavy
     if (pairs > hi) S = 1;
     else if (pairs > mid) S = std::min(S, 4);
     else if (pairs > lo) S = std::min(S, 8);
@@ -81,7 +81,6 @@ static int build_batch_tasks(const HostPlan &h, int nbp, int xbudget, int J0, st
     while ((1 << lg) < S) ++lg;
     for (int s0 = 0; s0 < nbp; s0 += S) tasks.push_back(make_int2(j, (s0 << 8) | lg));
   }
-  if (tasks.size() >= (size_t)INT32_MAX) return set_error(KKT_ERR_BAD_SHAPE, "too many batched tasks");
   return KKT_OK;
 }
 
@@ -167,9 +166,13 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   HeavyPlan heavy;
   d.b_xbudget = B_XBUDGET;
   d.b_stage = B_STAGE;  // doubles per stage buffer (two buffers per warp)
+  d.b_xbudget2 = B_XBUDGET2;
+  d.b_stage2 = B_STAGE2;
   if (const char *e = std::getenv("KKT_B_SMEM")) std::sscanf(e, "%d,%d", &d.b_xbudget, &d.b_stage);
+  if (const char *e = std::getenv("KKT_B_SMEM2")) std::sscanf(e, "%d,%d", &d.b_xbudget2, &d.b_stage2);
   d.b_static = std::getenv("KKT_B_STATIC") ? std::atoi(std::getenv("KKT_B_STATIC")) : 0;
   d.b_xbudget = std::max(d.b_xbudget, h.maxpat);
+  d.b_xbudget2 = std::max(d.b_xbudget2, h.maxpat);
   if (nb > 1) {
     // heavy tail: from the first column whose pattern exceeds KKT_B_HEAVY_NP slots
     const int heavy_np = std::getenv("KKT_B_HEAVY_NP") ? std::atoi(std::getenv("KKT_B_HEAVY_NP")) : 0;
@@ -184,7 +187,29 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
       d.J0 = h.n;
       rc2 = build_heavy(h, d.J0, heavy);
     }
-    if (rc2 == KKT_OK) rc2 = build_batch_tasks(h, nbp, d.b_xbudget, d.J0, btask);
+    // the replay runs in two launches split at column J2 (first pattern wider than
+    // KKT_B_SPLIT_NP slots): warp tasks before it, 4-warp CTA tasks (k_b_refactor_cta) for the
+    // wide separator columns after it
+    const int split_np = std::getenv("KKT_B_SPLIT_NP") ? std::atoi(std::getenv("KKT_B_SPLIT_NP")) : 128;
+    int J2 = std::min(d.J0, h.n);
+    for (int j = 0; j < J2; ++j)
+      if (split_np > 0 && (h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j]) > split_np) {
+        J2 = j;
+        break;
+      }
+    if (rc2 == KKT_OK) rc2 = build_batch_tasks(h, nbp, d.b_xbudget, 0, J2, btask);
+    d.n_btask1 = (int)btask.size();
+    if (rc2 == KKT_OK) {  // k_b_refactor_cta tasks: (column, B_CT_SC systems)
+      const int start = h.small_lev_ptr[h.n_small_levels];
+      for (int c = start; c < h.n; ++c) {
+        const int j = h.col_order[c];
+        if (j < J2 || j >= d.J0) continue;
+        d.h_xp = std::max<int>(d.h_xp, (int)((h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j])));
+        for (int s0 = 0; s0 < nbp; s0 += B_CT_SC) btask.push_back(make_int2(j, s0 << 8));
+      }
+    }
+    if (rc2 == KKT_OK && btask.size() >= (size_t)INT32_MAX)
+      rc2 = set_error(KKT_ERR_BAD_SHAPE, "too many batched tasks");
     if (rc2 != KKT_OK) {
       delete dev;
       return rc2;
@@ -311,7 +336,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.U_nglev = (int)h.U_glev_ptr.size() - 1;
   d.b_levelsync = std::getenv("KKT_B_LEVELSYNC") ? std::atoi(std::getenv("KKT_B_LEVELSYNC")) : 0;
   d.nhc = (int)heavy.col.size();
-  d.h_xp = heavy.xp;
+  d.h_xp = std::max(d.h_xp, heavy.xp);
   d.hc_col = carve<int>(cur, heavy.col.size());
   d.hc_optr = carve<int>(cur, heavy.optr.size());
   d.h_pp = carve<int>(cur, heavy.pp.size());
@@ -446,7 +471,12 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   if (nbp > 1) {
     int rbps = 0, tbps = 0;
     dev->refactor_smem = b_refactor_smem(d.b_xbudget, d.b_stage);
+    const size_t smem2 = b_cta_smem(std::max(d.h_xp, 1));
+    int rbps2 = 0;
     CUDA_TRY(b_configure(nbp, dev->refactor_smem, &rbps, &tbps));
+    CUDA_TRY(b_cta_configure(smem2, &rbps2));
+    dev->refactor_blocks2 = std::max(1, rbps2) * dev->sm_count;
+    dev->refactor_smem2 = smem2;
     dev->refactor_warps = B_WARPS;
     if (d.trace_step) d.prof = d.trace_step;  // per-warp cycle counters
     dev->refactor_blocks = std::max(1, rbps) * dev->sm_count;
@@ -517,7 +547,8 @@ static int refactor(Device *dev, const double *vals, int layout, int on_device, 
   LAUNCH(launch_reset_scal(d, 1, dev->stream));  // min |u_jj| starts at +inf
   {
     cudaError_t e = d.nbp > 1
-                        ? b_launch_refactor(d, dev->refactor_blocks, dev->refactor_smem, dev->stream,
+                        ? b_launch_refactor(d, dev->refactor_blocks, dev->refactor_smem,
+                                            dev->refactor_blocks2, dev->refactor_smem2, dev->stream,
                                             &dev->launches)
                         : launch_refactor(d, dev->refactor_blocks, dev->refactor_warps,
                                           dev->refactor_smem, dev->stream, &dev->launches);

@@ -39,6 +39,7 @@ struct DevPlan {
   int2 *btask = nullptr;  // batched refactor tasks {column, sys0 << 8 | log2(systems)}
   int n_btask = 0;
   int b_xbudget = 0, b_stage = 0, b_static = 0;
+  int b_xbudget2 = 0, b_stage2 = 0, n_btask1 = 0;  // second replay launch (wide columns)
   // Heavy tail (columns >= J0, the dense separator; batched only): refactorized by a CTA per
   // (column, 32 systems) in "pull" form (k_b_refactor_heavy): every workspace slot sums its
   // own updates in the reference order, the slots spread over the CTA's warps, U slots
@@ -127,7 +128,8 @@ struct Device {
   void *trace_mem = nullptr;
   size_t arena_bytes = 0;
   int sm_count = 0;
-  int refactor_blocks = 0, refactor_warps = 8;
+  int refactor_blocks = 0, refactor_warps = 8, refactor_blocks2 = 0;
+  size_t refactor_smem2 = 0;
   size_t refactor_smem = 0;
   int trsv_blocks = 0;
   long long launches = 0;
@@ -161,11 +163,18 @@ cudaError_t launch_sweep_blocked(const DevPlan &d, bool upper, double *x, cudaSt
 // ---- batched (interleaved, nb > 1) kernels: batch.cu ----
 constexpr int B_XBUDGET = 768;   // default refactor workspace doubles per warp (np * systems)
 constexpr int B_STAGE = 512;     // default stage buffer doubles (pairs * systems), x2 buffers
+constexpr int B_XBUDGET2 = 2304;  // ... for the wide separator columns (second launch)
+constexpr int B_STAGE2 = 768;
 constexpr int B_WARPS = 4;       // warps per refactor CTA
 size_t b_refactor_smem(int xbudget, int stage);
 cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm);
 cudaError_t b_launch_expand_norms(const DevPlan &d, cudaStream_t s);
-cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, cudaStream_t s, long long *launches);
+cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blocks2, size_t smem2,
+                              cudaStream_t s, long long *launches);
+cudaError_t b_refactor_occupancy(size_t smem, int *blocks_per_sm);
+size_t b_cta_smem(int xp);
+cudaError_t b_cta_configure(size_t smem, int *blocks_per_sm);
+constexpr int B_CT_SC = 4;  // systems per k_b_refactor_cta task
 cudaError_t b_launch_diag_stats(const DevPlan &d, cudaStream_t s);
 cudaError_t b_launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,
                           cudaStream_t s, long long *launches);

@@ -14,14 +14,17 @@ from paper_2401_13926_b200 import _native as nat
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("case,nb,heavy", [("acopf_small", 5, None), ("standard_trace", 9, None),
-                                           ("acopf_tiny", 20, None), ("acopf_small", 40, "8"),
-                                           ("standard_trace", 3, "4")])
-def test_batch_refactor_solve_bitwise(case, nb, heavy, monkeypatch):
-    """heavy: KKT_B_HEAVY_NP, forcing the system-major heavy-tail storage on small cases."""
+@pytest.mark.parametrize("case,nb,env", [
+    ("acopf_small", 5, {}), ("standard_trace", 9, {}), ("acopf_tiny", 20, {}),
+    ("acopf_small", 40, {"KKT_B_HEAVY_NP": "8"}), ("standard_trace", 3, {"KKT_B_HEAVY_NP": "4"}),
+    ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8"}), ("standard_trace", 9, {"KKT_B_SPLIT_NP": "4"}),
+    ("acopf_small", 7, {"KKT_B_SPLIT_NP": "8", "KKT_B_HEAVY_NP": "16"})])
+def test_batch_refactor_solve_bitwise(case, nb, env, monkeypatch):
+    """env forces the alternative replay kernels onto small cases: KKT_B_SPLIT_NP (4-warp CTA
+    tasks for the wide columns), KKT_B_HEAVY_NP (pull-form CTA per 32 systems)."""
     import torch
-    if heavy:
-        monkeypatch.setenv("KKT_B_HEAVY_NP", heavy)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     from paper_2401_13926_b200.device import DeviceSystem
     g = golden(case)
     M = g["K_values"].shape[0]

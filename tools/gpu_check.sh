@@ -1,5 +1,5 @@
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1; echo tests=$? >> gpurun_out/gpu_tests.log
-tail -2 gpurun_out/gpu_tests.log
-timeout 120 python tools/probe_kernels.py activsg10k 64 3
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/launches_b64.csv python tools/probe_kernels.py activsg10k 64 1 > /dev/null 2>&1
-python tools/launch_summary.py gpurun_out/launches_b64.csv 2>/dev/null | head -16
+tail -3 gpurun_out/gpu_tests.log
+for SP in 128 64 256 32 0; do
+ echo "split=$SP $(KKT_B_SPLIT_NP=$SP timeout 120 python tools/probe_kernels.py activsg10k 64 3 | cut -c1-90)"
+done
