@@ -387,24 +387,24 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d, const in
 
 
 // ----------------------------------------------------------------------------
-// Refactor, wide separator columns (j >= J2; second launch): a CTA of 4 warps per
-// (column, SC = 4 systems).  Thread t serves entry lane e = t / SC and system s = t % SC, so
+// Refactor, wide separator columns (j >= J2; second launch): a CTA of SC warps per
+// (column, SC systems; KKT_B_CT_SC, default 8).  Thread t serves entry lane e = t / SC and system s = t % SC, so
 // a warp access is 8 entries x 4 systems = 8 full 32-byte sectors (the one-system-per-warp
 // replay reads 8 bytes per sector) and a step's entries are spread over 32 entry lanes per
 // system; the steps of so(j) are separated by a 128-thread barrier.  The workspace x[np][SC]
 // and two cp.async stage buffers are shared by the CTA.  Same per-entry order as k_refactor.
 // ----------------------------------------------------------------------------
-constexpr int CT_SC = 4;                 // systems per CTA task
-constexpr int CT_THREADS = 32 * CT_SC;   // 32 entry lanes x SC systems
 constexpr int CT_STAGE = 256;            // update pairs per stage buffer
 
-size_t b_cta_smem(int xp) {
-  return ((size_t)xp * CT_SC + 2 * (size_t)CT_STAGE * CT_SC) * sizeof(double) +
+size_t b_cta_smem(int xp, int sc) {
+  return ((size_t)xp * sc + 2 * (size_t)CT_STAGE * sc) * sizeof(double) +
          2 * (size_t)CT_STAGE * sizeof(int) + 64;
 }
 
-__global__ void __launch_bounds__(CT_THREADS) k_b_refactor_cta(DevPlan d, const int2 *__restrict__ tasks,
+template <int CT_SC>
+__global__ void __launch_bounds__(32 * CT_SC) k_b_refactor_cta(DevPlan d, const int2 *__restrict__ tasks,
                                                                int ntask) {
+  constexpr int CT_THREADS = 32 * CT_SC;   // 32 entry lanes x SC systems
   extern __shared__ double csm[];
   __shared__ int s_task;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -1167,14 +1167,20 @@ cudaError_t b_refactor_occupancy(size_t smem, int *blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor, 32 * B_WARPS, smem);
 }
 
-cudaError_t b_cta_configure(size_t smem, int *blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_b_refactor_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int SC>
+static cudaError_t cta_conf(size_t smem, int *blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_b_refactor_cta<SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_b_refactor_cta, cudaFuncAttributePreferredSharedMemoryCarveout,
+    e = cudaFuncSetAttribute(k_b_refactor_cta<SC>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_cta, CT_THREADS, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_cta<SC>, 32 * SC, smem);
   return e;
+}
+
+cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm) {
+  return sc == 2 ? cta_conf<2>(smem, blocks_per_sm) : sc == 8 ? cta_conf<8>(smem, blocks_per_sm)
+                                                              : cta_conf<4>(smem, blocks_per_sm);
 }
 
 cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blocks2, size_t smem2,
@@ -1202,7 +1208,11 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blo
   if (d.n_btask > d.n_btask1) {  // the wide separator columns (depend only on earlier ones)
     cudaError_t e2 = cudaMemsetAsync(d.ticket2, 0, 4, s);
     if (e2 != cudaSuccess) return e2;
-    k_b_refactor_cta<<<blocks2, CT_THREADS, smem2, s>>>(d, d.btask + d.n_btask1, d.n_btask - d.n_btask1);
+    const int2 *t2 = d.btask + d.n_btask1;
+    const int n2 = d.n_btask - d.n_btask1;
+    if (d.ct_sc == 2) k_b_refactor_cta<2><<<blocks2, 64, smem2, s>>>(d, t2, n2);
+    else if (d.ct_sc == 8) k_b_refactor_cta<8><<<blocks2, 256, smem2, s>>>(d, t2, n2);
+    else k_b_refactor_cta<4><<<blocks2, 128, smem2, s>>>(d, t2, n2);
     ++*launches;
   }
   if (d.nhc) {  // the heavy tail depends only on earlier columns: a kernel boundary suffices

@@ -190,7 +190,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
     // the replay runs in two launches split at column J2 (first pattern wider than
     // KKT_B_SPLIT_NP slots): warp tasks before it, 4-warp CTA tasks (k_b_refactor_cta) for the
     // wide separator columns after it
-    const int split_np = std::getenv("KKT_B_SPLIT_NP") ? std::atoi(std::getenv("KKT_B_SPLIT_NP")) : 128;
+    const int split_np = std::getenv("KKT_B_SPLIT_NP") ? std::atoi(std::getenv("KKT_B_SPLIT_NP")) : 256;
     int J2 = std::min(d.J0, h.n);
     for (int j = 0; j < J2; ++j)
       if (split_np > 0 && (h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j]) > split_np) {
@@ -199,13 +199,15 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
       }
     if (rc2 == KKT_OK) rc2 = build_batch_tasks(h, nbp, d.b_xbudget, 0, J2, btask);
     d.n_btask1 = (int)btask.size();
-    if (rc2 == KKT_OK) {  // k_b_refactor_cta tasks: (column, B_CT_SC systems)
+    d.ct_sc = std::getenv("KKT_B_CT_SC") ? std::atoi(std::getenv("KKT_B_CT_SC")) : 8;
+    if (d.ct_sc != 2 && d.ct_sc != 8) d.ct_sc = 4;
+    if (rc2 == KKT_OK) {  // k_b_refactor_cta tasks: (column, ct_sc systems)
       const int start = h.small_lev_ptr[h.n_small_levels];
       for (int c = start; c < h.n; ++c) {
         const int j = h.col_order[c];
         if (j < J2 || j >= d.J0) continue;
         d.h_xp = std::max<int>(d.h_xp, (int)((h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j])));
-        for (int s0 = 0; s0 < nbp; s0 += B_CT_SC) btask.push_back(make_int2(j, s0 << 8));
+        for (int s0 = 0; s0 < nbp; s0 += d.ct_sc) btask.push_back(make_int2(j, s0 << 8));
       }
     }
     if (rc2 == KKT_OK && btask.size() >= (size_t)INT32_MAX)
@@ -471,10 +473,10 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   if (nbp > 1) {
     int rbps = 0, tbps = 0;
     dev->refactor_smem = b_refactor_smem(d.b_xbudget, d.b_stage);
-    const size_t smem2 = b_cta_smem(std::max(d.h_xp, 1));
+    const size_t smem2 = b_cta_smem(std::max(d.h_xp, 1), d.ct_sc);
     int rbps2 = 0;
     CUDA_TRY(b_configure(nbp, dev->refactor_smem, &rbps, &tbps));
-    CUDA_TRY(b_cta_configure(smem2, &rbps2));
+    CUDA_TRY(b_cta_configure(d.ct_sc, smem2, &rbps2));
     dev->refactor_blocks2 = std::max(1, rbps2) * dev->sm_count;
     dev->refactor_smem2 = smem2;
     dev->refactor_warps = B_WARPS;

@@ -40,6 +40,7 @@ struct DevPlan {
   int n_btask = 0;
   int b_xbudget = 0, b_stage = 0, b_static = 0;
   int b_xbudget2 = 0, b_stage2 = 0, n_btask1 = 0;  // second replay launch (wide columns)
+  int ct_sc = 4;  // systems per k_b_refactor_cta task (KKT_B_CT_SC = 2 | 4 | 8)
   // Heavy tail (columns >= J0, the dense separator; batched only): refactorized by a CTA per
   // (column, 32 systems) in "pull" form (k_b_refactor_heavy): every workspace slot sums its
   // own updates in the reference order, the slots spread over the CTA's warps, U slots
@@ -172,9 +173,8 @@ cudaError_t b_launch_expand_norms(const DevPlan &d, cudaStream_t s);
 cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blocks2, size_t smem2,
                               cudaStream_t s, long long *launches);
 cudaError_t b_refactor_occupancy(size_t smem, int *blocks_per_sm);
-size_t b_cta_smem(int xp);
-cudaError_t b_cta_configure(size_t smem, int *blocks_per_sm);
-constexpr int B_CT_SC = 4;  // systems per k_b_refactor_cta task
+size_t b_cta_smem(int xp, int sc);
+cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm);
 cudaError_t b_launch_diag_stats(const DevPlan &d, cudaStream_t s);
 cudaError_t b_launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,
                           cudaStream_t s, long long *launches);
