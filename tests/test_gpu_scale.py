@@ -1,0 +1,114 @@
+"""Parity at the BASELINE.json sizes (configs[0..4]): the device path against the C oracle
+(oracle/kkt_oracle.c, the restatement of direct_lu.refactorize / lu_solve and
+refine.refine_fgmres, pinned to the reference's golden vectors by test_oracle.py) on the
+same ACOPF-shaped sequences the bench uses.
+
+* refactorize: factor values bitwise equal to the oracle's (late, ill-conditioned system);
+* lu_solve: bitwise;
+* refine_fgmres: trigger equal, iterations within +-1, final relative residual within
+  max(1.5 x oracle, 4 eps) (SURVEY.md §7 hard part 5) — checked with the oracle's SpMV;
+* batch of 4 systems (interleaved handle): every system bitwise equal to its single-system
+  factors / solution (and so to the oracle).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = [("activsg200", 19), ("activsg2000", 19), ("activsg10k", 19),
+           pytest.param("activsg70k", 12, marks=pytest.mark.slow)]
+
+
+def _setup(config):
+    from paper_2401_13926_b200 import factorize, to_general
+    from paper_2401_13926_b200.acopf import ACOPF_CONFIGS, build_pattern, system_values
+    pat = build_pattern(ACOPF_CONFIGS[config], 0)
+    K0 = pat.K.with_values(system_values(pat, 0, 0))
+    f, _ = factorize(to_general(K0))
+    return pat, K0, f
+
+
+def _oracle(f, K0):
+    from oracle import oracle
+    from paper_2401_13926_b200.sparse import expand_pattern
+    ex = expand_pattern(K0)
+    arrays = dict(row_perm=f.row_perm.perm, col_perm=f.col_perm.perm, Lp=f._Lp, Li=f._Li,
+                  Lx=f._Lx, Up=f._Up, Ui=f._Ui, Ux=f._Ux, Udiag=f._Udiag, so_ptr=f._so_ptr,
+                  so_data=f._so_data, ap_ptr=f._ap_ptr, a_src=f._a_src, a_tgt=f._a_tgt)
+    return oracle.OracleFactors(arrays, ex.general.row_ptr), ex
+
+
+@pytest.mark.parametrize("config,k", CONFIGS)
+def test_full_size_against_oracle(config, k):
+    import torch
+    from oracle import oracle
+    import paper_2401_13926_b200._native as nat
+    from paper_2401_13926_b200.acopf import MU_STEP, system_rhs, system_values
+    from paper_2401_13926_b200.refine import BarrierTiedTolerance
+    pat, K0, f = _setup(config)
+    of, ex = _oracle(f, K0)
+    vals = system_values(pat, k, 0)
+    r = system_rhs(pat, k, 0)
+    delta = BarrierTiedTolerance()(10.0 ** (-MU_STEP * k))
+    # oracle
+    of.refactorize(vals[ex.src])
+    ox0 = of.lu_solve(r)
+    ox, orep = of.refine_fgmres(pat.K.row_ptr, pat.K.col_idx, vals, r, ox0, delta)
+    # device, single system
+    dev = f.device(restart_m=10)
+    LOWER = nat.LAYOUT_SYMMETRIC_LOWER
+    with torch.cuda.stream(dev.stream):
+        tv = torch.from_numpy(vals).to(dev.device)
+        tr = torch.from_numpy(r).to(dev.device)
+        tx = torch.empty_like(tr)
+    dev.refactor_device(tv, LOWER)
+    Lx, Ux, Ud = dev.download_factors()
+    assert np.array_equal(Lx, of.a["Lx"]) and np.array_equal(Ux, of.a["Ux"])
+    assert np.array_equal(Ud, of.a["Udiag"])
+    dev.solve_device(tr, tx)
+    x0 = dev.d2h(tx)
+    assert np.array_equal(x0, ox0)
+    rep = dev.step(tv, LOWER, tr, tx, True, 10, 10, delta)
+    x = dev.d2h(tx)
+    assert bool(rep.triggered) == orep["triggered"]
+    assert abs(rep.iterations - orep["iterations"]) <= 1, (rep.iterations, orep["iterations"])
+    nr = np.linalg.norm(r)
+    rr = np.linalg.norm(r - oracle.spmv(pat.K.row_ptr, pat.K.col_idx, vals, x)) / nr
+    rr_o = np.linalg.norm(r - oracle.spmv(pat.K.row_ptr, pat.K.col_idx, vals, ox)) / nr
+    assert rr <= max(1.5 * rr_o, 4 * np.finfo(float).eps), (rr, rr_o)
+
+
+@pytest.mark.parametrize("config", ["activsg200", "activsg10k"])
+def test_full_size_batch_equals_single(config):
+    """The interleaved batch reproduces each system's single-system factors and solve."""
+    import torch
+    import paper_2401_13926_b200._native as nat
+    from paper_2401_13926_b200.acopf import system_rhs, system_values
+    from paper_2401_13926_b200.device import DeviceSystem
+    pat, K0, f = _setup(config)
+    ks = [3, 11, 17, 19]
+    vals = np.stack([system_values(pat, k, q) for q, k in enumerate(ks)])
+    rhs = np.stack([system_rhs(pat, k, q) for q, k in enumerate(ks)])
+    LOWER = nat.LAYOUT_SYMMETRIC_LOWER
+    devb = DeviceSystem(f, batch=len(ks))
+    with torch.cuda.stream(devb.stream):
+        tv = torch.from_numpy(vals).to(devb.device)
+        tr = torch.from_numpy(rhs).to(devb.device)
+        tx = torch.empty_like(tr)
+    devb.refactor_batch(tv, LOWER)
+    Lb, Ub, Db = devb.download_factors_batch()
+    devb.solve_device(tr, tx)
+    xb = devb.d2h(tx)
+    dev1 = f.device(restart_m=10)
+    for q in range(len(ks)):
+        with torch.cuda.stream(dev1.stream):
+            v1 = torch.from_numpy(vals[q]).to(dev1.device)
+            r1 = torch.from_numpy(rhs[q]).to(dev1.device)
+            x1 = torch.empty_like(r1)
+        dev1.refactor_device(v1, LOWER)
+        L1, U1, D1 = dev1.download_factors()
+        assert np.array_equal(Lb[q], L1) and np.array_equal(Ub[q], U1) and np.array_equal(Db[q], D1)
+        dev1.solve_device(r1, x1)
+        assert np.array_equal(xb[q], dev1.d2h(x1))
+    devb.close()

@@ -1,4 +1,2 @@
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1; echo tests=$? >> gpurun_out/gpu_tests.log
-tail -2 gpurun_out/gpu_tests.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?
-tail -1 gpurun_out/bench.log | cut -c1-400
+timeout 1500 python -m pytest tests/test_gpu_scale.py -x -q -m gpu --durations=10 > gpurun_out/gpu_scale.log 2>&1; echo scale=$? >> gpurun_out/gpu_scale.log
+tail -20 gpurun_out/gpu_scale.log
