@@ -897,20 +897,37 @@ cudaError_t b_launch_trsv(const DevPlan &d, const double *b, double *x, int grid
 // ----------------------------------------------------------------------------
 // SpMV and residual statistics (sparsecore.spmv order; refine.py:62-92)
 // ----------------------------------------------------------------------------
+// Row i of K x for one system (lane), in the reference's order.  The row's products are
+// formed from loads issued 8 entries at a time (all independent), then summed in order.
 __device__ __forceinline__ double row_dot_b(const DevPlan &d, const double *__restrict__ x, int i,
                                             int sys) {
   const int b = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
+  const double *__restrict__ av = d.A_vals;
+  const int *__restrict__ ci = d.A_ci;
   double s1 = 0.0, s2 = 0.0;
-  if (d.sym_lower) {
-    for (int p = b; p < s; ++p)
-      s1 = __dadd_rn(s1, __dmul_rn(d.A_vals[IL(d, p, sys)], x[IL(d, d.A_ci[p], sys)]));
-    for (int p = s; p < e; ++p)
-      s2 = __dadd_rn(s2, __dmul_rn(d.A_vals[IL(d, p, sys)], x[IL(d, d.A_ci[p], sys)]));
-    return __dadd_rn(s1, s2);
+  for (int p0 = b; p0 < e; p0 += 8) {
+    int c[8];
+    double v[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (p0 + u < e) {
+        c[u] = ci[p0 + u];
+        v[u] = av[IL(d, p0 + u, sys)];
+      }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (p0 + u < e) xv[u] = x[IL(d, c[u], sys)];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (p0 + u < e) {
+        const double t = __dmul_rn(v[u], xv[u]);
+        // symmetric-lower operators sum the stored and the mirrored halves apart
+        // (sparsecore.py:296-302); general ones in one pass
+        if (d.sym_lower && p0 + u >= s) s2 = __dadd_rn(s2, t);
+        else s1 = __dadd_rn(s1, t);
+      }
   }
-  for (int p = b; p < e; ++p)
-    s1 = __dadd_rn(s1, __dmul_rn(d.A_vals[IL(d, p, sys)], x[IL(d, d.A_ci[p], sys)]));
-  return s1;
+  return d.sym_lower ? __dadd_rn(s1, s2) : s1;
 }
 
 __global__ void __launch_bounds__(256) k_b_spmv(DevPlan d, const double *__restrict__ x,

@@ -17,14 +17,29 @@ namespace kkt {
 __device__ __forceinline__ double row_dot(const DevPlan &d, const double *__restrict__ av,
                                           const double *__restrict__ x, int i) {
   const int b = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
+  const int *__restrict__ ci = d.A_ci;
   double s1 = 0.0, s2 = 0.0;
-  if (d.sym_lower) {
-    for (int p = b; p < s; ++p) s1 = __dadd_rn(s1, __dmul_rn(av[p], x[d.A_ci[p]]));
-    for (int p = s; p < e; ++p) s2 = __dadd_rn(s2, __dmul_rn(av[p], x[d.A_ci[p]]));
-    return __dadd_rn(s1, s2);
+  for (int p0 = b; p0 < e; p0 += 8) {  // 8 independent loads in flight, then the ordered sum
+    int c[8];
+    double v[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (p0 + u < e) {
+        c[u] = ci[p0 + u];
+        v[u] = av[p0 + u];
+      }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (p0 + u < e) xv[u] = x[c[u]];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (p0 + u < e) {
+        const double t = __dmul_rn(v[u], xv[u]);
+        if (d.sym_lower && p0 + u >= s) s2 = __dadd_rn(s2, t);
+        else s1 = __dadd_rn(s1, t);
+      }
   }
-  for (int p = b; p < e; ++p) s1 = __dadd_rn(s1, __dmul_rn(av[p], x[d.A_ci[p]]));
-  return s1;
+  return d.sym_lower ? __dadd_rn(s1, s2) : s1;
 }
 
 // out = K x, or out = bsub - K x; optional ||out||^2 block partials [nb][rb].
