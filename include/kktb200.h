@@ -210,7 +210,10 @@ int kkt_dev_info(kkt_device *d, int64_t info[16]);
  * refactor_out[2n] = {dispatch ns, done ns} per column, trisolve_out[2n] = publish ns per
  * row of the L then the U sweep (grid phase rows).  Profiling aid. */
 int kkt_dev_trace(kkt_device *d, uint64_t *refactor_out, uint64_t *trisolve_out);
-/* Per replay step (so entry) of the last refactor: ns when applied (bit 0: it was late). */
+/* Secondary trace buffer, max(n_so, 4n) entries: single system — ns when each replay step
+ * (so entry) of the last refactor was applied (bit 0: it was late); batch — per-warp cycle
+ * counters of k_b_refactor and {start, critical-dependency ready} ns per grid-phase row of
+ * the last solve (system 0; L rows at 2r, U rows at 2(n+r)).  Profiling aid. */
 int kkt_dev_trace_steps(kkt_device *d, uint64_t *steps_out);
 
 /* Kernel launches issued by this handle since creation (evidence counter). */

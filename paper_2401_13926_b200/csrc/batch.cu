@@ -665,10 +665,11 @@ __global__ void __launch_bounds__(256) k_b_diag_stats(DevPlan d) {
 // order.  Each warp prefetches its NEXT task's static data (row pointers, the first chunk's
 // column indices and values, the initial value and pivot) while the current task waits on
 // its dependency, so a task's critical path is the dependency's y values only.
+constexpr int RC = 6;  // entries of a row prefetched with the task
 struct RowTask {
   int r, cr, beg, end;
-  int cols[4];
-  double vs[4], acc, piv;
+  int cols[RC];
+  double vs[RC], ys[RC], acc, piv;
 };
 
 template <bool IS_U>
@@ -683,11 +684,11 @@ __device__ __forceinline__ void row_prefetch(const DevPlan &d, const double *__r
   t.beg = rp[t.r];
   t.end = rp[t.r + 1];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < RC; ++q)
     if (t.beg + q < t.end) t.cols[q] = ci[t.beg + q];
   if (act) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < RC; ++q)
       if (t.beg + q < t.end) t.vs[q] = vals[IL(d, t.beg + q, sys)];
     t.acc = IS_U ? ldcg(&d.yL[IL(d, t.r, sys)]) : b[IL(d, d.row_perm[t.r], sys)];
     t.piv = IS_U ? d.udiag[IL(d, t.r, sys)] : 1.0;
@@ -697,7 +698,7 @@ __device__ __forceinline__ void row_prefetch(const DevPlan &d, const double *__r
 template <bool IS_U>
 __global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__restrict__ b,
                                                      double *__restrict__ xout) {
-  constexpr int C = 4;  // entries per chunk
+  constexpr int C = RC;  // entries per chunk
   const int lane = threadIdx.x & 31;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -709,67 +710,80 @@ __global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__
   const int ngroups = d.nbp >> 5;
   const int ntask = nrows * ngroups;
   const int gstart = IS_U ? 0 : d.L_sync_ptr[d.L_nsync];  // leading levels ran row-parallel
-  int task = gstart * ngroups + gwarp;
-  RowTask nt;
-  if (task < ntask) {
-    const int sys = (task % ngroups) * 32 + lane;
-    row_prefetch<IS_U>(d, b, task / ngroups, sys, sys_active(d, sys), nt);
-  }
-  for (; task < ntask; task += nwarps) {
-    const int sys = (task % ngroups) * 32 + lane;
-    const bool act = sys_active(d, sys);
-    RowTask t = nt;
-    const int nxt = task + nwarps;
-    if (nxt < ntask) {
-      const int nsys = (nxt % ngroups) * 32 + lane;
-      row_prefetch<IS_U>(d, b, nxt / ngroups, nsys, sys_active(d, nsys), nt);  // used next round
-    }
-    const unsigned amask = __ballot_sync(FULL, act);
-    if (!amask) continue;
-    // speculative y loads of the first chunk (the non-critical dependencies are normally
-    // published already), then one lane waits (back-off) on the critical dependency
-    double ys[C];
+  // speculative y loads of a prefetched task's first chunk (the non-critical dependencies
+  // are normally published already; sentinels are re-read after the critical wait)
+  auto load_ys = [&](RowTask &t, int sys, bool act) {
     if (act) {
 #pragma unroll
       for (int q = 0; q < C; ++q)
-        if (t.beg + q < t.end) ys[q] = ld_relaxed_f64(&ysrc[IL(d, t.cols[q], sys)]);
+        if (t.beg + q < t.end) t.ys[q] = ld_relaxed_f64(&ysrc[IL(d, t.cols[q], sys)]);
     }
-    if (t.cr >= 0 && lane == 31 - __clz(amask)) wait_value_bo(&ysrc[IL(d, t.cr, sys)], d.poll_ns);
-    __syncwarp();
-    if (!act) continue;  // per lane from here: systems are independent
-    double acc = t.acc;
-    for (int c0 = t.beg; c0 < t.end; c0 += C) {
-      int ncols[C];
-      double nvs[C];
+  };
+  // one row: wait for its critical dependency, sum in the reference order, publish; the
+  // next row's static data is prefetched into `n` first and its y loads issued at the end
+  auto run_row = [&](int task, RowTask &t, RowTask &n) {
+    const int sys = (task % ngroups) * 32 + lane;
+    const bool act = sys_active(d, sys);
+    const int nxt = task + nwarps;
+    const int nsys = (nxt % ngroups) * 32 + lane;
+    const bool nact = nxt < ntask && sys_active(d, nsys);
+    if (nxt < ntask) row_prefetch<IS_U>(d, b, nxt / ngroups, nsys, nact, n);
+    const unsigned amask = __ballot_sync(FULL, act);
+    if (amask) {
+      const bool tr = d.trace_step && sys == 0;  // timeline of system 0: {start, crit ready}
+      if (tr) d.trace_step[2 * ((IS_U ? d.n : 0) + t.r)] = globaltimer();
+      // one lane waits (back-off) on the critical dependency of one system
+      if (t.cr >= 0 && lane == 31 - __clz(amask)) wait_value_bo(&ysrc[IL(d, t.cr, sys)], d.poll_ns);
+      __syncwarp();
+      if (tr) d.trace_step[2 * ((IS_U ? d.n : 0) + t.r) + 1] = globaltimer();
+      if (act) {  // per lane from here: systems are independent
+        double acc = t.acc;
+        for (int c0 = t.beg; c0 < t.end; c0 += C) {
 #pragma unroll
-      for (int q = 0; q < C; ++q)
-        if (c0 + C + q < t.end) {
-          ncols[q] = ci[c0 + C + q];
-          nvs[q] = vals[IL(d, c0 + C + q, sys)];
-        }
+          for (int q = 0; q < C; ++q)
+            if (c0 + q < t.end) {
+              double y = t.ys[q];
+              if (is_sentinel(y)) y = wait_value_bo(&ysrc[IL(d, t.cols[q], sys)], d.poll_ns);
+              acc = __dsub_rn(acc, __dmul_rn(t.vs[q], y));
+            }
+          if (c0 + C < t.end) {  // long rows: the next chunk (one round trip each)
 #pragma unroll
-      for (int q = 0; q < C; ++q)
-        if (c0 + q < t.end) {
-          double y = ys[q];
-          if (is_sentinel(y)) y = wait_value_bo(&ysrc[IL(d, t.cols[q], sys)], d.poll_ns);
-          acc = __dsub_rn(acc, __dmul_rn(t.vs[q], y));
-        }
+            for (int q = 0; q < C; ++q)
+              if (c0 + C + q < t.end) {
+                t.cols[q] = ci[c0 + C + q];
+                t.vs[q] = vals[IL(d, c0 + C + q, sys)];
+              }
 #pragma unroll
-      for (int q = 0; q < C; ++q)
-        if (c0 + C + q < t.end) {
-          t.cols[q] = ncols[q];
-          t.vs[q] = nvs[q];
-          ys[q] = ld_relaxed_f64(&ysrc[IL(d, t.cols[q], sys)]);
+            for (int q = 0; q < C; ++q)
+              if (c0 + C + q < t.end) t.ys[q] = ld_relaxed_f64(&ysrc[IL(d, t.cols[q], sys)]);
+          }
         }
+        const double w = IS_U ? __ddiv_rn(acc, t.piv) : acc;
+        st_relaxed_f64(&ysrc[IL(d, t.r, sys)], unsentinel(w));  // publish first
+        if (d.trace_trsv && sys == 0) d.trace_trsv[(IS_U ? d.n : 0) + t.r] = globaltimer();
+        st_relaxed_f64(&yres[IL(d, t.r, sys)], sentinel_value());
+        if (IS_U) {
+          xout[IL(d, d.col_perm[t.r], sys)] = w;
+          if (!isfinite(w)) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
+        }
+      }
     }
-    const double w = IS_U ? __ddiv_rn(acc, t.piv) : acc;
-    st_relaxed_f64(&ysrc[IL(d, t.r, sys)], unsentinel(w));  // publish first
-    if (d.trace_trsv && sys == 0) d.trace_trsv[(IS_U ? d.n : 0) + t.r] = globaltimer();
-    st_relaxed_f64(&yres[IL(d, t.r, sys)], sentinel_value());
-    if (IS_U) {
-      xout[IL(d, d.col_perm[t.r], sys)] = w;
-      if (!isfinite(w)) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
-    }
+    if (nxt < ntask) load_ys(n, nsys, nact);  // the next row's columns have arrived by now
+  };
+  // two task buffers used alternately (no register copy of a whole task)
+  int task = gstart * ngroups + gwarp;
+  RowTask ta, tb;
+  if (task < ntask) {
+    const int sys = (task % ngroups) * 32 + lane;
+    row_prefetch<IS_U>(d, b, task / ngroups, sys, sys_active(d, sys), ta);
+    load_ys(ta, sys, sys_active(d, sys));
+  }
+  while (task < ntask) {
+    run_row(task, ta, tb);
+    task += nwarps;
+    if (task >= ntask) break;
+    run_row(task, tb, ta);
+    task += nwarps;
   }
 }
 

@@ -364,7 +364,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   }
   d.trace_ref = d.trace_trsv = d.trace_step = nullptr;
   if (std::getenv("KKT_TRACE") && std::atoi(std::getenv("KKT_TRACE")) > 0) {
-    const size_t tb = 4 * 8 * n + 8 * (size_t)d.n_so;
+    const size_t tb = 4 * 8 * n + 8 * std::max<size_t>((size_t)d.n_so, 4 * n);
     ce = cudaMalloc(&dev->trace_mem, tb + 64);
     if (ce == cudaSuccess) {
       d.trace_ref = (unsigned long long *)dev->trace_mem;
@@ -1068,7 +1068,8 @@ int kkt_dev_trace_steps(kkt_device *dd, uint64_t *steps_out) {
   cudaSetDevice(dev->device);
   cudaError_t e = cudaStreamSynchronize(dev->stream);
   if (e == cudaSuccess)
-    e = cudaMemcpy(steps_out, dev->d.trace_step, 8 * (size_t)dev->d.n_so, cudaMemcpyDeviceToHost);
+    e = cudaMemcpy(steps_out, dev->d.trace_step,
+                   8 * std::max<size_t>((size_t)dev->d.n_so, 4 * (size_t)dev->d.n), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
   return KKT_OK;
 }

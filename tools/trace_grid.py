@@ -33,6 +33,9 @@ ref = np.zeros(2 * n, dtype=np.uint64)
 tri = np.zeros(2 * n, dtype=np.uint64)
 nat.check(dev.lib.kkt_dev_trace(dev.h, ref.ctypes.data_as(C.c_void_p), tri.ctypes.data_as(C.c_void_p)))
 t = tri.astype(np.int64)
+steps = np.zeros(max(int(f._so_data.size), 4 * n), dtype=np.uint64)
+nat.check(dev.lib.kkt_dev_trace_steps(dev.h, steps.ctypes.data_as(C.c_void_p)))
+stt = steps.astype(np.int64)
 # dependencies: L row r <- columns of L(r, :) ; U row r <- columns of U(r, :)
 Lp, Li = f._Lp, f._Li
 Up, Ui = f._Up, f._Ui
@@ -70,3 +73,18 @@ for name, off, p, colp, rowi in (("L", 0, pL, Lp, Li), ("U", n, pU, Up, Ui)):
     hops = -np.diff(tt[path])
     print(f"   critical chain {len(path)} rows, mean hop {hops.mean():.0f} ns, chain start at "
           f"{(tt[path[-1]] - t0) / 1e3:.1f} us")
+    if B > 1:
+        st0 = stt[2 * off // 1 + 0: 2 * (off + p): 2] if False else stt[2 * off:2 * (off + p):2]
+        stc = stt[2 * off + 1:2 * (off + p):2]
+        ok = (st0 > 0) & has
+        if ok.any():
+            q = (st0 - last)[ok]   # start after the last dependency was published (queueing)
+            w = (stc - st0)[ok]    # critical-dependency wait
+            k = (tt - stc)[ok]     # work after the dependency: reloads, sum, publish
+            pth = [r for r in path if ok[r]]
+            print(f"   rows: start-after-deps median {np.median(q):.0f} ns (p90 {np.percentile(q, 90):.0f}), "
+                  f"crit wait median {np.median(w):.0f}, work median {np.median(k):.0f} ns")
+            if pth:
+                pq = (st0 - last)[pth]; pw = (stc - st0)[pth]; pk = (tt - stc)[pth]
+                print(f"   on the critical chain: start-after-deps mean {pq.mean():.0f} ns, crit wait "
+                      f"{pw.mean():.0f}, work {pk.mean():.0f} ns")
