@@ -136,6 +136,26 @@ def step_k(s: int, M: int) -> int:
     return 1 + (7 * s) % (M - 1)
 
 
+def rank_seed_base(rank: int) -> int:
+    """value streams of rank r: 1000 r + q, q < B — ranks never share a system"""
+    return 1000 * rank
+
+
+def rank_systems(rank: int, B: int, ks) -> list:
+    """the (barrier step, value stream) of every system rank `rank` processes, in order"""
+    return [(k, rank_seed_base(rank) + q) for k in ks for q in range(B)]
+
+
+def reduce_max(value: float, dist, device) -> float:
+    """max over ranks (the job's time is its slowest rank's)"""
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def make_batch(pat, B: int, k: int, seed_base: int):
     """B independent systems (value streams seed_base + q) at barrier step k."""
     from paper_2401_13926_b200.acopf import MU_STEP, system_rhs, system_values
@@ -259,7 +279,7 @@ def main():
     ks = [step_k(s, M) for s in range(K)]
     wks = [step_k(s, M) for s in range(W)]
     t0 = time.perf_counter()
-    host = {k: make_batch(pat, B, k, seed_base=1000 * rank) for k in sorted(set(ks + wks))}
+    host = {k: make_batch(pat, B, k, seed_base=rank_seed_base(rank)) for k in sorted(set(ks + wks))}
     gen_s += time.perf_counter() - t0
     t0 = time.perf_counter()
     dev = DeviceSystem(f, restart_m=10, device=local, batch=B)
@@ -303,11 +323,7 @@ def main():
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     launches = dev.launch_count() - launches0
-    total_ms = float(np.sum(step_ms))
-    if dist:
-        t = torch.tensor([total_ms], device=dev.device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = reduce_max(float(np.sum(step_ms)), dist, dev.device)
     value = total_ms / (K * B * world)
 
     # ---- e2e through the public API from pinned host buffers (copies overlapped) ----
@@ -320,11 +336,7 @@ def main():
     t0 = time.perf_counter()
     pipe.run([(hp[k][0], hp[k][1], hx[s], policy(host[k][2])) for s, k in enumerate(ks)])
     torch.cuda.synchronize()
-    e2e_total = (time.perf_counter() - t0) * 1e3
-    if dist:
-        t = torch.tensor([e2e_total], device=dev.device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
+    e2e_total = reduce_max((time.perf_counter() - t0) * 1e3, dist, dev.device)
     e2e_value = e2e_total / (K * B * world)
     vals, rhs, _ = host[ks[-1]]
 
