@@ -21,6 +21,8 @@
  *   kkt_dev_residual_norms <- refine.nsr / nrbe / needs_refinement       refine.py:62-92
  *   kkt_dev_fgmres         <- krylov.fgmres(K, M=lu_solve, b, x0, cfg)   krylov.py:117
  *   kkt_dev_refine_fgmres  <- refine.refine_fgmres(K, f, x0, r, cfg)     refine.py:103
+ *   kkt_dev_residual       <- rho = r - spmv(K, x); ||rho||_2            refine.py:158,167-168
+ *   kkt_dev_axpy           <- x += d  (Richardson update)                refine.py:166
  */
 #ifndef KKTB200_H
 #define KKTB200_H
@@ -142,6 +144,14 @@ int kkt_dev_spmv(kkt_device *d, const double *x_dev, double *y_dev);
  * out[batch][6] = {||r-Kx||_2, ||r-Kx||_inf, ||x||_2, ||x||_inf, ||r||_2, ||K||_inf}. */
 int kkt_dev_residual_norms(kkt_device *d, const double *r_dev, const double *x_dev,
                            double *out_host);
+
+/* rho = r - K x (the reference's spmv order, then the subtraction) and norms_host[batch] =
+ * ||rho||_2 per system: the Richardson residual (refine.py:158,167-168).  Device vectors. */
+int kkt_dev_residual(kkt_device *d, const double *r_dev, const double *x_dev, double *rho_dev,
+                     double *norms_host);
+
+/* x += y elementwise over the handle's n * batch entries (refine.py:166).  Device vectors. */
+int kkt_dev_axpy(kkt_device *d, double *x_dev, const double *y_dev);
 
 typedef struct {
   int m;                  /* restart length                  (krylov.py:61) */

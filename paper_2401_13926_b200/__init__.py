@@ -13,7 +13,8 @@ from .direct_lu import (PATCH_RELATIVE_FLOOR, LuDiagnostics, LuFactors, PatternM
 from .krylov import (CGS2, MGS, KrylovConfig, KrylovResult, LinearOperator, NotSpdOperatorError,
                      OperatorOutputError, fgmres, lu_preconditioner)
 from .refine import (BarrierTiedTolerance, FixedTolerance, RefinementConfig, RefinementReport,
-                     config_for_mu, needs_refinement, nrbe, nsr, refine_fgmres)
+                     config_for_mu, needs_refinement, nrbe, nsr, refine_fgmres,
+                     refine_richardson)
 from .sparse_ops import inf_norm, spmv
 
 __all__ = [name for name in dir() if not name.startswith("_")]

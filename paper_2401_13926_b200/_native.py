@@ -69,6 +69,8 @@ SIGNATURES = [
     ("kkt_dev_solve", C.c_int, [vp, vp, vp]),
     ("kkt_dev_spmv", C.c_int, [vp, vp, vp]),
     ("kkt_dev_residual_norms", C.c_int, [vp, vp, vp, f64p]),
+    ("kkt_dev_residual", C.c_int, [vp, vp, vp, vp, f64p]),
+    ("kkt_dev_axpy", C.c_int, [vp, vp, vp]),
     ("kkt_dev_fgmres", C.c_int, [vp, vp, vp, vp, C.POINTER(KrylovCfg), C.POINTER(KrylovReport),
                                  f64p, C.c_int]),
     ("kkt_dev_refine_fgmres", C.c_int, [vp, vp, vp, vp, C.POINTER(KrylovCfg),

@@ -842,6 +842,47 @@ int kkt_dev_spmv(kkt_device *d, const double *x_dev, double *y_dev) {
   return kkt::dev_spmv(dev, x_dev, y_dev, nullptr, nullptr);
 }
 
+int kkt_dev_residual(kkt_device *d, const double *r_dev, const double *x_dev, double *rho_dev,
+                     double *norms_host) {
+  Device *dev = reinterpret_cast<Device *>(d);
+  if (!dev || !r_dev || !x_dev || !rho_dev || !norms_host)
+    return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
+  cudaSetDevice(dev->device);
+  kkt::DevPlan &p = dev->d;
+  const double *r = r_dev, *x = x_dev;
+  double *rho = rho_dev;
+  if (p.nbp > 1) {  // interleave through the staging vectors
+    IL_IN(r_dev, dev->kry->sr);
+    IL_IN(x_dev, dev->kry->sx0);
+    r = dev->kry->sr;
+    x = dev->kry->sx0;
+    rho = dev->kry->sx;
+  }
+  int rc = kkt::dev_spmv(dev, x, rho, r, p.partials);  // rho = r - K x, ||rho||^2 partials
+  if (rc) return rc;
+  {
+    cudaError_t e = kkt::launch_reduce_partials(p, p.partials, 1, dev->kry->nrm, 1, 1, dev->stream);
+    dev->launches++;
+    if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
+  }
+  if (p.nbp > 1) IL_OUT(rho, rho_dev);
+  cudaError_t e = cudaMemcpyAsync(norms_host, dev->kry->nrm, 8 * (size_t)p.nb, cudaMemcpyDeviceToHost,
+                                  dev->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(dev->stream);
+  if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
+  return KKT_OK;
+}
+
+int kkt_dev_axpy(kkt_device *d, double *x_dev, const double *y_dev) {
+  Device *dev = reinterpret_cast<Device *>(d);
+  if (!dev || !x_dev || !y_dev) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
+  cudaSetDevice(dev->device);
+  cudaError_t e = kkt::launch_add_inplace(x_dev, y_dev, (int64_t)dev->d.n * dev->d.nb, dev->stream);
+  dev->launches++;
+  if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
+  return KKT_OK;
+}
+
 int kkt_dev_residual_norms(kkt_device *d, const double *r_dev, const double *x_dev, double *out_host) {
   Device *dev = reinterpret_cast<Device *>(d);
   if (!dev || !r_dev || !x_dev || !out_host) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");

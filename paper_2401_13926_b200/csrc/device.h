@@ -157,6 +157,7 @@ cudaError_t launch_L_front(const DevPlan &d, const double *b, double *x, int gri
                            long long *launches);
 cudaError_t b_launch_grid_L(const DevPlan &d, const double *b, double *x, int grid_blocks, cudaStream_t s);
 cudaError_t launch_fill_sentinel(double *p, int64_t n, cudaStream_t s);
+cudaError_t launch_add_inplace(double *x, const double *y, int64_t n, cudaStream_t s);
 // blocked sweep of the trailing block (sweep.cu), single and batched handles
 cudaError_t sweep_configure();
 cudaError_t launch_sweep_blocked(const DevPlan &d, bool upper, double *x, cudaStream_t s);

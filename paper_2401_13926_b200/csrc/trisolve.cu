@@ -180,6 +180,17 @@ cudaError_t launch_L_front(const DevPlan &d, const double *b, double *x, int gri
   return e;
 }
 
+// x += y (numpy's elementwise add, one rounding)
+__global__ void k_add_inplace(double *__restrict__ x, const double *__restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = __dadd_rn(x[i], y[i]);
+}
+
+cudaError_t launch_add_inplace(double *x, const double *y, int64_t n, cudaStream_t s) {
+  if (n > 0) k_add_inplace<<<(unsigned)std::min<int64_t>((n + 255) / 256, 8 * 148), 256, 0, s>>>(x, y, n);
+  return cudaGetLastError();
+}
+
 __global__ void k_fill_sentinel(double *p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)

@@ -182,6 +182,17 @@ class DeviceSystem:
     def spmv_device(self, x_t, y_t):
         nat.check(self.lib.kkt_dev_spmv(self.h, _vp(x_t), _vp(y_t)), "kkt_dev_spmv")
 
+    def residual_device(self, r_t, x_t, rho_t):
+        """rho = r - K x (reference spmv order) and ||rho||_2 per system (kkt_dev_residual)."""
+        out = (C.c_double * self.nb)()
+        nat.check(self.lib.kkt_dev_residual(self.h, _vp(r_t), _vp(x_t), _vp(rho_t), out),
+                  "kkt_dev_residual")
+        return out[0] if self.nb == 1 else list(out)
+
+    def axpy_device(self, x_t, y_t):
+        """x += y on the device (kkt_dev_axpy)."""
+        nat.check(self.lib.kkt_dev_axpy(self.h, _vp(x_t), _vp(y_t)), "kkt_dev_axpy")
+
     def residual_stats_device(self, r_t, x_t) -> ResidualStats:
         out = (C.c_double * 6)()
         nat.check(self.lib.kkt_dev_residual_norms(self.h, _vp(r_t), _vp(x_t), out))

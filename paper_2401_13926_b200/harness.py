@@ -22,7 +22,8 @@ import numpy as np
 
 from . import _native as nat
 from .direct_lu import factorize, lu_solve, refactorize
-from .refine import FixedTolerance, RefinementConfig, config_for_mu, refine_fgmres
+from .refine import (FixedTolerance, RefinementConfig, config_for_mu, refine_fgmres,
+                     refine_richardson)
 from .sparse import SYMMETRIC_LOWER, CsMatrix, to_general
 
 
@@ -44,9 +45,16 @@ class RowMetrics:
 
 
 def run_refactor_ir(matrices, rhss, cfg: RefinementConfig | None = None, mus=None,
-                    tolerance=None, mode: str = "device", refresh_after: int = 1):
-    """Run the refactor_ir_fgmres strategy over a sequence; returns (rows, factors)."""
+                    tolerance=None, mode: str = "device", refresh_after: int = 1,
+                    method: str = "fgmres"):
+    """Run the refactor_ir_fgmres (``method="fgmres"``) or refactor_ir_richardson
+    (``"richardson"``, refine.py:135; drop-in mode) strategy; returns (rows, factors)."""
     cfg = cfg or RefinementConfig()
+    if method not in ("fgmres", "richardson"):
+        raise ValueError(f"unknown refinement method {method!r}")
+    refine = refine_fgmres if method == "fgmres" else refine_richardson
+    if method == "richardson":
+        mode = "dropin"
     policy = tolerance or FixedTolerance(cfg.delta_tol)
     rows: list[RowMetrics] = []
     factors = None
@@ -65,7 +73,7 @@ def run_refactor_ir(matrices, rhss, cfg: RefinementConfig | None = None, mus=Non
             x0 = lu_solve(factors, r)
             t_solve = time.perf_counter() - t0
             t0 = time.perf_counter()
-            x, rep = refine_fgmres(K, factors, x0, r, rc)
+            x, rep = refine(K, factors, x0, r, rc)
             t_ref = time.perf_counter() - t0
             iters, conv = rep.ir_iterations, rep.converged
             nsr_b, nsr_a = rep.nsr_before, rep.nsr_after
@@ -79,7 +87,7 @@ def run_refactor_ir(matrices, rhss, cfg: RefinementConfig | None = None, mus=Non
             x0 = lu_solve(factors, r)
             t_solve = time.perf_counter() - t0
             t0 = time.perf_counter()
-            x, rep = refine_fgmres(K, factors, x0, r, rc)
+            x, rep = refine(K, factors, x0, r, rc)
             t_ref = time.perf_counter() - t0
             iters, conv = rep.ir_iterations, rep.converged
             nsr_b, nsr_a = rep.nsr_before, rep.nsr_after

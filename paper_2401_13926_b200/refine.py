@@ -1,4 +1,4 @@
-"""Drop-in for ``kktsolve.refine``: FGMRES iterative refinement on the B200.
+"""Drop-in for ``kktsolve.refine``: FGMRES and Richardson iterative refinement on the B200.
 
 ``refine_fgmres`` follows refine.py:103-132 step for step — trigger, NSR before, FGMRES
 with the (stale) LU factors as right preconditioner and ``tol = delta_tol``, NSR/NRBE after —
@@ -145,3 +145,78 @@ def refine_fgmres(K, factors, x0, r, cfg: RefinementConfig):
         triangular_solves_used=factors.triangular_solve_count - count0,
         nsr_before=s0.nsr(), nsr_after=s1.nsr(), rr_final=rr_final, nrbe_final=s1.nrbe(),
         converged=bool(rep.converged))
+
+
+def refine_richardson(K, factors, x0, r, cfg: RefinementConfig):
+    """Richardson iterative refinement (refine.py:135-205) with every vector on the device.
+
+    Per step: d = lu_solve(rho) (device trisolves), x += d (device), rho = r - K x with its
+    2-norm (one fused device pass).  The stopping rules are the reference's: residual
+    tolerance or NSR stagnation, the step budget, divergence after two consecutive residual
+    increases (then the best iterate is returned).  The host reads one norm per step.
+    """
+    x0 = np.asarray(x0, dtype=np.float64)
+    r = np.asarray(r, dtype=np.float64)
+    dev = factors.device(restart_m=cfg.krylov.m)
+    torch = dev.torch
+    dev.set_operator(K)
+    dev.h2d(dev.r, r)
+    dev.h2d(dev.x0, x0)
+    s0 = dev.residual_stats_device(dev.r, dev.x0)
+    if not (s0.err2 > cfg.delta_tol * s0.r2):                      # :147-148
+        q = s0.nsr()
+        return x0.copy(), RefinementReport(
+            triggered=False, method="none", ir_iterations=0, triangular_solves_used=0,
+            nsr_before=q, nsr_after=q, rr_final=1.0, nrbe_final=s0.nrbe(), converged=True)
+    count0 = factors.triangular_solve_count
+    nsr_before = s0.nsr()
+    r_norm = s0.r2
+    with torch.cuda.stream(dev.stream):
+        x = dev.x0.clone()
+        rho = torch.empty_like(x)
+        dvec = torch.empty_like(x)
+        best_x = x.clone()
+    rho_norm = dev.residual_device(dev.r, x, rho)                  # :158
+    rho0_norm = rho_norm
+    nsr_old = nsr_before
+    best_rho = rho_norm
+    steps, converged, diverged, growth = 0, False, False, 0
+    while steps < cfg.richardson_max_steps:
+        if cfg.richardson_stop == TOLERANCE and rho_norm <= cfg.delta_tol * r_norm:
+            converged = True
+            break
+        dev.solve_device(rho, dvec)                                # :166  d = lu_solve(rho)
+        factors.triangular_solve_count += 1
+        dev.axpy_device(x, dvec)                                   #       x += d
+        steps += 1
+        new_norm = dev.residual_device(dev.r, x, rho)              # :168
+        if new_norm < best_rho:
+            with torch.cuda.stream(dev.stream):
+                best_x.copy_(x)
+            best_rho = new_norm
+        if new_norm > rho_norm:
+            growth += 1
+            if growth >= 2:
+                diverged = True
+                break
+        else:
+            growth = 0
+        rho_norm = new_norm
+        if cfg.richardson_stop == NSR_RATIO:
+            nsr_new = dev.residual_stats_device(dev.r, x).nsr()
+            if nsr_old > 0 and nsr_new / nsr_old > cfg.nsr_ratio_floor:
+                converged = True
+                break
+            nsr_old = nsr_new
+    else:
+        converged = cfg.richardson_stop == TOLERANCE and rho_norm <= cfg.delta_tol * r_norm
+    if diverged:
+        x, rho_norm = best_x, best_rho
+    s1 = dev.residual_stats_device(dev.r, x)
+    xh = dev.d2h(x)
+    return xh, RefinementReport(
+        triggered=True, method="richardson", ir_iterations=steps,
+        triangular_solves_used=factors.triangular_solve_count - count0,
+        nsr_before=nsr_before, nsr_after=s1.nsr(),
+        rr_final=(rho_norm / rho0_norm) if rho0_norm > 0 else 0.0,
+        nrbe_final=s1.nrbe(), converged=converged, diverged=diverged)

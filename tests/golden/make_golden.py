@@ -28,7 +28,7 @@ from kktsolve import sparsecore as R_sc  # noqa: E402
 from kktsolve.harness import (MatrixSequence, SequenceItem, StrategySpec,  # noqa: E402
                               run_strategy, sequence_from_trace)
 from kktsolve.krylov import KrylovConfig  # noqa: E402
-from kktsolve.refine import RefinementConfig, refine_fgmres  # noqa: E402
+from kktsolve.refine import RefinementConfig, refine_fgmres, refine_richardson  # noqa: E402
 from kktsolve.seqgen import standard_trace  # noqa: E402
 from conftest import random_sparse  # noqa: E402  (reference test generator)
 
@@ -97,6 +97,20 @@ def sequence_case(name, Ks, rhss, deltas=(1e-10, 1e-14), keep_factor_vals=None):
         out[f"harness_{tag}"] = np.array([[r.nsr_before, r.nsr_after, r.nrbe, r.rr,
                                            r.ir_iterations, r.triangular_solves]
                                           for r in rows])
+    # Richardson IR (refine.py:135-205): tolerance stop at two deltas, NSR-ratio stop
+    for tag, rcfg in (("1e-10", dict(delta_tol=1e-10)), ("1e-14", dict(delta_tol=1e-14)),
+                      ("nsr", dict(delta_tol=1e-10, richardson_stop="nsr_ratio"))):
+        xs, reps = [], []
+        for i, (K, r) in enumerate(zip(Ks, rhss)):
+            R_lu.refactorize(f, R_sc.to_general(K))
+            x0 = R_lu.lu_solve(f, r)
+            x, rep = refine_richardson(K, f, x0, r, RefinementConfig(**rcfg))
+            xs.append(x)
+            reps.append([rep.triggered, rep.ir_iterations, rep.triangular_solves_used,
+                         rep.nsr_before, rep.nsr_after, rep.rr_final, rep.nrbe_final,
+                         rep.converged, rep.diverged])
+        out[f"richardson_{tag}_x"] = np.stack(xs)
+        out[f"richardson_{tag}_report"] = np.array(reps, dtype=np.float64)
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
     print(name, "N", K0.n_rows, "nnzL", f._Li.size, "iters",
           out["refine_1e-10_report"][:, 1].astype(int).tolist())
