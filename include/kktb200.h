@@ -23,6 +23,9 @@
  *   kkt_dev_refine_fgmres  <- refine.refine_fgmres(K, f, x0, r, cfg)     refine.py:103
  *   kkt_dev_residual       <- rho = r - spmv(K, x); ||rho||_2            refine.py:158,167-168
  *   kkt_dev_axpy           <- x += d  (Richardson update)                refine.py:166
+ *   kkt_assemble_values    <- kkt.assemble_kkt values (frozen pattern)   kkt.py:88-124
+ *   kkt_assemble_rhs       <- kkt.assemble_rhs                           kkt.py:127-137
+ *   kkt_recover_dz         <- kkt.recover_dz                             kkt.py:140-144
  */
 #ifndef KKTB200_H
 #define KKTB200_H
@@ -149,6 +152,21 @@ int kkt_dev_residual_norms(kkt_device *d, const double *r_dev, const double *x_d
  * ||rho||_2 per system: the Richardson residual (refine.py:158,167-168).  Device vectors. */
 int kkt_dev_residual(kkt_device *d, const double *r_dev, const double *x_dev, double *rho_dev,
                      double *norms_host);
+
+/* Interior-point bookkeeping on the device (kkt.py:88-144), nb systems, system-major
+ * device arrays, run on `stream` (a cudaStream_t, may be NULL).
+ * kkt_assemble_values: K[nb][nnz_K] of the frozen symmetric-lower pattern; position p sums
+ *   its sources src[p][0..1] (int32 pairs, -1 = none) in order: ids 0..nH-1 = H values,
+ *   nH..nH+n-1 = D_x = z/x diagonal, nH+n.. = J values (np.add.at order, kkt.py:104-107).
+ * kkt_assemble_rhs: rhs[nb][n+m] = [r~_x + (z - mu/x); r_lambda], mu[nb] on the device.
+ * kkt_recover_dz: dz[nb][n] = (r_z - z*dx)/x, dx of system s at dx + s*dx_stride. */
+int kkt_assemble_values(int64_t nnz_K, int64_t n, int64_t nH, int64_t nJ, int nb,
+                        const int32_t *src_dev, const double *H_dev, const double *J_dev,
+                        const double *x_dev, const double *z_dev, double *K_dev, void *stream);
+int kkt_assemble_rhs(int64_t n, int64_t m, int nb, const double *r_tilde_x, const double *r_lambda,
+                     const double *x, const double *z, const double *mu_dev, double *rhs, void *stream);
+int kkt_recover_dz(int64_t n, int nb, int64_t dx_stride, const double *r_z, const double *z,
+                   const double *dx, const double *x, double *dz, void *stream);
 
 /* x += y elementwise over the handle's n * batch entries (refine.py:166).  Device vectors. */
 int kkt_dev_axpy(kkt_device *d, double *x_dev, const double *y_dev);

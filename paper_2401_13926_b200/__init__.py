@@ -16,6 +16,8 @@ from .refine import (BarrierTiedTolerance, FixedTolerance, RefinementConfig, Ref
                      config_for_mu, needs_refinement, nrbe, nsr, refine_fgmres,
                      refine_richardson)
 from .sparse_ops import inf_norm, spmv
+from .kkt import (DeviceKktAssembler, KktBlocks, KktRhs, KktSystem, assemble_kkt, assemble_rhs,
+                  recover_dz)
 
 __all__ = [name for name in dir() if not name.startswith("_")]
 __version__ = "0.1.0"

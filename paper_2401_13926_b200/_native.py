@@ -71,6 +71,9 @@ SIGNATURES = [
     ("kkt_dev_residual_norms", C.c_int, [vp, vp, vp, f64p]),
     ("kkt_dev_residual", C.c_int, [vp, vp, vp, vp, f64p]),
     ("kkt_dev_axpy", C.c_int, [vp, vp, vp]),
+    ("kkt_assemble_values", C.c_int, [i64, i64, i64, i64, C.c_int, vp, vp, vp, vp, vp, vp, vp]),
+    ("kkt_assemble_rhs", C.c_int, [i64, i64, C.c_int, vp, vp, vp, vp, vp, vp, vp]),
+    ("kkt_recover_dz", C.c_int, [i64, C.c_int, i64, vp, vp, vp, vp, vp, vp]),
     ("kkt_dev_fgmres", C.c_int, [vp, vp, vp, vp, C.POINTER(KrylovCfg), C.POINTER(KrylovReport),
                                  f64p, C.c_int]),
     ("kkt_dev_refine_fgmres", C.c_int, [vp, vp, vp, vp, C.POINTER(KrylovCfg),

@@ -185,6 +185,40 @@ def edge_cases():
     np.savez_compressed(os.path.join(HERE, "edge_cases.npz"), **out)
 
 
+def kkt_case():
+    """Reference kkt.py (assemble_kkt / assemble_rhs / recover_dz) on the standard trace."""
+    from kktsolve.kkt import assemble_kkt, assemble_rhs, recover_dz
+    from kktsolve.seqgen import qp_residuals
+    tr = standard_trace()
+    out = {}
+    ks0 = tr.systems[0][0]
+    H, J = ks0.blocks.H, ks0.blocks.J
+    out.update(H_row_ptr=H.row_ptr, H_col_idx=H.col_idx, H_values=H.values, J_row_ptr=J.row_ptr,
+               J_col_idx=J.col_idx, J_values=J.values, n=np.array([H.n_rows, J.n_rows]))
+    rng = np.random.default_rng(7)
+    xs, zs, mus, Kv, Kd, rts, rls, rzs, rxs, dxs, dzs = ([] for _ in range(11))
+    donor = None
+    for ks, rhs, mu, _c in tr.systems:
+        b = ks.blocks
+        k2 = assemble_kkt(b, pattern_from=donor)
+        if donor is None:
+            k_fresh = assemble_kkt(b)
+            assert np.array_equal(k_fresh.K.values, k2.K.values)
+        donor = k2
+        rt = rhs.r_tilde_x
+        r2 = assemble_rhs(b, rt, rhs.r_lambda, rhs.r_z)
+        dx = rng.standard_normal(b.n)
+        xs.append(b.x); zs.append(b.z); mus.append(b.mu); Kv.append(k2.K.values)
+        Kd.append(k2.dx_diag); rts.append(rt); rls.append(rhs.r_lambda); rzs.append(rhs.r_z)
+        rxs.append(r2.r_x); dxs.append(dx); dzs.append(recover_dz(b, rhs.r_z, dx))
+    out.update(K_row_ptr=donor.K.row_ptr, K_col_idx=donor.K.col_idx, x=np.stack(xs), z=np.stack(zs),
+               mu=np.array(mus), K_values=np.stack(Kv), dx_diag=np.stack(Kd), r_tilde_x=np.stack(rts),
+               r_lambda=np.stack(rls), r_z=np.stack(rzs), r_x=np.stack(rxs), dx=np.stack(dxs),
+               dz=np.stack(dzs))
+    np.savez_compressed(os.path.join(HERE, "kkt_assembly.npz"), **out)
+    print("kkt_assembly", len(xs), "systems, nnz(K)", donor.K.nnz)
+
+
 def main():
     meta = {"reference": "/root/reference/pkg (kktsolve 0.1.0)", "numpy": np.__version__}
     standard()
@@ -192,6 +226,7 @@ def main():
     acopf_case("acopf_small", acopf.ACOPF_CONFIGS["small"], 20)
     random_cases()
     edge_cases()
+    kkt_case()
     with open(os.path.join(HERE, "MANIFEST.json"), "w") as fh:
         json.dump(meta, fh, indent=2)
 

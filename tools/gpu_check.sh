@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1; echo tests=$? >> gpurun_out/gpu_tests.log
-tail -25 gpurun_out/gpu_tests.log
+tail -15 gpurun_out/gpu_tests.log
