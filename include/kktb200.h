@@ -26,6 +26,8 @@
  *   kkt_assemble_values    <- kkt.assemble_kkt values (frozen pattern)   kkt.py:88-124
  *   kkt_assemble_rhs       <- kkt.assemble_rhs                           kkt.py:127-137
  *   kkt_recover_dz         <- kkt.recover_dz                             kkt.py:140-144
+ *   kkt_mm_info / kkt_mm_read_coo / kkt_mm_read_array
+ *                          <- mmio.load_matrix_market / load_vector      mmio.py:36-130
  */
 #ifndef KKTB200_H
 #define KKTB200_H
@@ -152,6 +154,14 @@ int kkt_dev_residual_norms(kkt_device *d, const double *r_dev, const double *x_d
  * ||rho||_2 per system: the Richardson residual (refine.py:158,167-168).  Device vectors. */
 int kkt_dev_residual(kkt_device *d, const double *r_dev, const double *x_dev, double *rho_dev,
                      double *norms_host);
+
+/* Matrix Market ingestion (host, C++; mmio.py:36-130).  kkt_mm_info: info[5] = {format
+ * (0 coordinate, 1 array), symmetric, rows, cols, nnz (array: rows)}.  kkt_mm_read_coo: the
+ * coordinate entries, 0-based, in file order (triplets; symmetric files: lower triangle).
+ * kkt_mm_read_array: an n x 1 array file.  Errors carry "path:line: message". */
+int kkt_mm_info(const char *path, int64_t *info);
+int kkt_mm_read_coo(const char *path, int64_t nnz, int64_t *rows, int64_t *cols, double *vals);
+int kkt_mm_read_array(const char *path, int64_t n, double *out);
 
 /* Interior-point bookkeeping on the device (kkt.py:88-144), nb systems, system-major
  * device arrays, run on `stream` (a cudaStream_t, may be NULL).

@@ -74,6 +74,9 @@ SIGNATURES = [
     ("kkt_assemble_values", C.c_int, [i64, i64, i64, i64, C.c_int, vp, vp, vp, vp, vp, vp, vp]),
     ("kkt_assemble_rhs", C.c_int, [i64, i64, C.c_int, vp, vp, vp, vp, vp, vp, vp]),
     ("kkt_recover_dz", C.c_int, [i64, C.c_int, i64, vp, vp, vp, vp, vp, vp]),
+    ("kkt_mm_info", C.c_int, [C.c_char_p, i64p]),
+    ("kkt_mm_read_coo", C.c_int, [C.c_char_p, i64, i64p, i64p, f64p]),
+    ("kkt_mm_read_array", C.c_int, [C.c_char_p, i64, f64p]),
     ("kkt_dev_fgmres", C.c_int, [vp, vp, vp, vp, C.POINTER(KrylovCfg), C.POINTER(KrylovReport),
                                  f64p, C.c_int]),
     ("kkt_dev_refine_fgmres", C.c_int, [vp, vp, vp, vp, C.POINTER(KrylovCfg),

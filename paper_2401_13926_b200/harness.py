@@ -15,8 +15,10 @@ The optional ``tolerance`` policy maps each system's mu to delta_tol (barrier-ti
 
 from __future__ import annotations
 
+import json
+import os
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -25,6 +27,61 @@ from .direct_lu import factorize, lu_solve, refactorize
 from .refine import (FixedTolerance, RefinementConfig, config_for_mu, refine_fgmres,
                      refine_richardson)
 from .sparse import SYMMETRIC_LOWER, CsMatrix, to_general
+
+
+class SequenceError(ValueError):
+    """Invalid sequence manifest or pattern drift (harness.py SequenceError)."""
+
+
+@dataclass
+class SequenceItem:
+    K: CsMatrix
+    rhs: np.ndarray
+    matrix_path: str | None = None
+    rhs_path: str | None = None
+
+
+@dataclass
+class MatrixSequence:
+    name: str
+    items: list
+    metadata: dict = field(default_factory=dict)
+
+
+def _lower_nnz(K: CsMatrix) -> int:
+    if K.symmetry == SYMMETRIC_LOWER:
+        return K.nnz
+    rows = np.repeat(np.arange(K.n_rows), np.diff(K.row_ptr))
+    return int(np.count_nonzero(rows >= K.col_idx))
+
+
+def load_sequence(manifest_path: str) -> MatrixSequence:
+    """A manifest's systems through the C++ Matrix Market reader, validating the shared
+    pattern (harness.load_sequence, harness.py:118-146)."""
+    from .mmio import load_matrix_market, load_vector
+    with open(manifest_path, "r") as fh:
+        manifest = json.load(fh)
+    systems = manifest.get("systems", [])
+    if not systems:
+        raise SequenceError("sequence must contain at least one system")
+    base = os.path.dirname(os.path.abspath(manifest_path))
+    items: list[SequenceItem] = []
+    for i, entry in enumerate(systems):
+        mpath = os.path.join(base, entry["matrix"])
+        rpath = os.path.join(base, entry["rhs"])
+        K = load_matrix_market(mpath)
+        rhs = load_vector(rpath)
+        if rhs.size != K.n_rows:
+            raise SequenceError(f"system {i}: rhs length {rhs.size} does not "
+                                f"match matrix dimension {K.n_rows}")
+        if items and not K.same_pattern(items[0].K):
+            raise SequenceError(f"system {i}: sparsity pattern differs from system 0")
+        items.append(SequenceItem(K=K, rhs=rhs, matrix_path=mpath, rhs_path=rpath))
+    metadata = {"N": items[0].K.n_rows, "nnz": _lower_nnz(items[0].K)}
+    for key in ("n", "m", "mu"):
+        if key in manifest:
+            metadata[key] = manifest[key]
+    return MatrixSequence(name=manifest.get("name", "sequence"), items=items, metadata=metadata)
 
 
 @dataclass

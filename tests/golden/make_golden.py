@@ -219,6 +219,49 @@ def kkt_case():
     print("kkt_assembly", len(xs), "systems, nnz(K)", donor.K.nnz)
 
 
+def mm_case():
+    """Reference mmio on files written by the reference: parsed arrays + error messages."""
+    from kktsolve import mmio as R_mm
+    d = os.path.join(HERE, "mm")
+    os.makedirs(d, exist_ok=True)
+    tr = standard_trace()
+    K = tr.systems[3][0].K
+    R_mm.write_matrix_market(os.path.join(d, "K_sym.mtx"), K)
+    R_mm.write_matrix_market(os.path.join(d, "K_gen.mtx"), R_sc.to_general(K))
+    R_mm.write_vector(os.path.join(d, "r.mtx"), tr.systems[3][1].r_x)
+    bad = {
+        "bad_header.mtx": "%%MatrixMarket vector coordinate real general\n1 1 1\n1 1 1.0\n",
+        "bad_field.mtx": "%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1.0\n",
+        "bad_size.mtx": "%%MatrixMarket matrix coordinate real general\n% c\n2 2\n",
+        "bad_entry.mtx": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n2 x 3.0\n",
+        "bad_range.mtx": "%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n",
+        "bad_upper.mtx": "%%MatrixMarket matrix coordinate real symmetric\n2 2 1\n1 2 1.0\n",
+        "bad_count.mtx": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n",
+        "bad_extra.mtx": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 1.0\n2 2 2.0\n",
+    }
+    msgs = {}
+    for name, text in bad.items():
+        path = os.path.join(d, name)
+        with open(path, "w") as fh:
+            fh.write(text)
+        try:
+            R_mm.load_matrix_market(path)
+            msgs[name] = None
+        except R_mm.MatrixMarketError as exc:
+            msgs[name] = str(exc).replace(d, "<dir>")
+    out = {}
+    for name in ("K_sym.mtx", "K_gen.mtx"):
+        A = R_mm.load_matrix_market(os.path.join(d, name))
+        tag = name.split(".")[0]
+        out[f"{tag}_row_ptr"], out[f"{tag}_col_idx"], out[f"{tag}_values"] = A.row_ptr, A.col_idx, A.values
+        out[f"{tag}_sym"] = np.array([A.symmetry == R_sc.SYMMETRIC_LOWER])
+    out["r"] = R_mm.load_vector(os.path.join(d, "r.mtx"))
+    np.savez_compressed(os.path.join(d, "expected.npz"), **out)
+    with open(os.path.join(d, "errors.json"), "w") as fh:
+        json.dump(msgs, fh, indent=1)
+    print("mm files", sorted(msgs))
+
+
 def main():
     meta = {"reference": "/root/reference/pkg (kktsolve 0.1.0)", "numpy": np.__version__}
     standard()
@@ -227,6 +270,7 @@ def main():
     random_cases()
     edge_cases()
     kkt_case()
+    mm_case()
     with open(os.path.join(HERE, "MANIFEST.json"), "w") as fh:
         json.dump(meta, fh, indent=2)
 
