@@ -1215,7 +1215,8 @@ cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm) {
 }
 
 cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blocks2, size_t smem2,
-                              cudaStream_t s, long long *launches) {
+                              cudaStream_t s, long long *launches, cudaStream_t s2, cudaEvent_t ev_a,
+                              cudaEvent_t ev_b, int blocks_ov) {
   if (!d.n) return cudaSuccess;
   // (KKT_NO_RESET=1, diagnostics only: keep the previous factors so no task ever waits)
   static const bool no_reset = std::getenv("KKT_NO_RESET") != nullptr;
@@ -1231,20 +1232,42 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blo
       ++*launches;
     }
   }
-  if (d.n_btask1) {
-    if (d.prof) cudaMemsetAsync(d.prof, 0, 8 * 8 * (size_t)blocks * B_WARPS, s);
-    k_b_refactor<<<blocks, 32 * B_WARPS, smem, s>>>(d, d.btask, d.n_btask1, d.b_xbudget, d.b_stage);
-    ++*launches;
-  }
-  if (d.n_btask > d.n_btask1) {  // the wide separator columns (depend only on earlier ones)
+  const bool two = d.n_btask > d.n_btask1;
+  // Overlap (s2 != null): the wide-column replay runs on s2 next to the warp replay, its
+  // tasks waiting on the published L columns of the first launch (one-way dependency, both
+  // launches deadlock-free on their own, and both fit on the SMs together: the first one
+  // is launched with blocks_ov CTAs).  Otherwise the wide columns follow a kernel boundary.
+  const bool ov = two && d.n_btask1 && s2 && ev_a && ev_b && blocks_ov > 0;
+  if (two) {
     cudaError_t e2 = cudaMemsetAsync(d.ticket2, 0, 4, s);
     if (e2 != cudaSuccess) return e2;
+  }
+  auto launch_wide = [&](cudaStream_t st) {
     const int2 *t2 = d.btask + d.n_btask1;
     const int n2 = d.n_btask - d.n_btask1;
-    if (d.ct_sc == 2) k_b_refactor_cta<2><<<blocks2, 64, smem2, s>>>(d, t2, n2);
-    else if (d.ct_sc == 8) k_b_refactor_cta<8><<<blocks2, 256, smem2, s>>>(d, t2, n2);
-    else k_b_refactor_cta<4><<<blocks2, 128, smem2, s>>>(d, t2, n2);
+    if (d.ct_sc == 2) k_b_refactor_cta<2><<<blocks2, 64, smem2, st>>>(d, t2, n2);
+    else if (d.ct_sc == 8) k_b_refactor_cta<8><<<blocks2, 256, smem2, st>>>(d, t2, n2);
+    else k_b_refactor_cta<4><<<blocks2, 128, smem2, st>>>(d, t2, n2);
     ++*launches;
+  };
+  if (ov) {
+    cudaError_t e2 = cudaEventRecord(ev_a, s);
+    if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(s2, ev_a, 0);
+    if (e2 != cudaSuccess) return e2;
+  }
+  if (d.n_btask1) {
+    if (d.prof) cudaMemsetAsync(d.prof, 0, 8 * 8 * (size_t)blocks * B_WARPS, s);
+    k_b_refactor<<<ov ? blocks_ov : blocks, 32 * B_WARPS, smem, s>>>(d, d.btask, d.n_btask1, d.b_xbudget,
+                                                                      d.b_stage);
+    ++*launches;
+  }
+  if (ov) {
+    launch_wide(s2);
+    cudaError_t e2 = cudaEventRecord(ev_b, s2);
+    if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(s, ev_b, 0);
+    if (e2 != cudaSuccess) return e2;
+  } else if (two) {
+    launch_wide(s);
   }
   if (d.nhc) {  // the heavy tail depends only on earlier columns: a kernel boundary suffices
     cudaError_t e2 = cudaMemsetAsync(d.ticket2, 0, 4, s);

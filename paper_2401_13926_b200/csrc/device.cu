@@ -51,6 +51,9 @@ static void destroy(Device *dev) {
   if (dev->trace_mem) cudaFree(dev->trace_mem);
   if (dev->pinned) cudaFreeHost(dev->pinned);
   if (dev->stream) cudaStreamDestroy(dev->stream);
+  if (dev->stream2) cudaStreamDestroy(dev->stream2);
+  if (dev->ev_a) cudaEventDestroy(dev->ev_a);
+  if (dev->ev_b) cudaEventDestroy(dev->ev_b);
   delete dev;
 }
 
@@ -479,6 +482,23 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
     CUDA_TRY(b_cta_configure(d.ct_sc, smem2, &rbps2));
     dev->refactor_blocks2 = std::max(1, rbps2) * dev->sm_count;
     dev->refactor_smem2 = smem2;
+    // overlapped launches (KKT_B_OVERLAP=1; measured slower): one wide-column CTA per SM next to
+    // as many warp-replay CTAs as still fit
+    const int ov = std::getenv("KKT_B_OVERLAP") ? std::atoi(std::getenv("KKT_B_OVERLAP")) : 0;
+    if (ov && rbps2 >= 1) {
+      cudaDeviceProp prop;
+      CUDA_TRY(cudaGetDeviceProperties(&prop, dev->device));
+      const size_t sm_left = prop.sharedMemPerMultiprocessor - smem2 - prop.reservedSharedMemPerBlock;
+      const int fit = (int)(sm_left / (dev->refactor_smem + prop.reservedSharedMemPerBlock));
+      const int b1 = std::min(std::max(rbps, 1), fit);
+      if (b1 >= 1) {
+        dev->refactor_blocks_ov = b1 * dev->sm_count;
+        dev->refactor_blocks2 = dev->sm_count;  // one wide-column CTA per SM
+        CUDA_TRY(cudaStreamCreateWithFlags(&dev->stream2, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&dev->ev_a, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&dev->ev_b, cudaEventDisableTiming));
+      }
+    }
     dev->refactor_warps = B_WARPS;
     if (d.trace_step) d.prof = d.trace_step;  // per-warp cycle counters
     dev->refactor_blocks = std::max(1, rbps) * dev->sm_count;
@@ -551,7 +571,8 @@ static int refactor(Device *dev, const double *vals, int layout, int on_device, 
     cudaError_t e = d.nbp > 1
                         ? b_launch_refactor(d, dev->refactor_blocks, dev->refactor_smem,
                                             dev->refactor_blocks2, dev->refactor_smem2, dev->stream,
-                                            &dev->launches)
+                                            &dev->launches, dev->stream2, dev->ev_a, dev->ev_b,
+                                            dev->refactor_blocks_ov)
                         : launch_refactor(d, dev->refactor_blocks, dev->refactor_warps,
                                           dev->refactor_smem, dev->stream, &dev->launches);
     if (e != cudaSuccess) return set_error(KKT_ERR_CUDA, std::string("refactor: ") + cudaGetErrorString(e));

@@ -123,13 +123,15 @@ struct Krylov;  // FGMRES workspace (krylov.cu)
 struct Device {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;          // batched: the wide-column replay, run alongside
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   DevPlan d;
   HostPlan h;
   void *arena = nullptr;
   void *trace_mem = nullptr;
   size_t arena_bytes = 0;
   int sm_count = 0;
-  int refactor_blocks = 0, refactor_warps = 8, refactor_blocks2 = 0;
+  int refactor_blocks = 0, refactor_warps = 8, refactor_blocks2 = 0, refactor_blocks_ov = 0;
   size_t refactor_smem2 = 0;
   size_t refactor_smem = 0;
   int trsv_blocks = 0;
@@ -172,7 +174,8 @@ size_t b_refactor_smem(int xbudget, int stage);
 cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm);
 cudaError_t b_launch_expand_norms(const DevPlan &d, cudaStream_t s);
 cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blocks2, size_t smem2,
-                              cudaStream_t s, long long *launches);
+                              cudaStream_t s, long long *launches, cudaStream_t s2 = nullptr,
+                              cudaEvent_t ev_a = nullptr, cudaEvent_t ev_b = nullptr, int blocks_ov = 0);
 cudaError_t b_refactor_occupancy(size_t smem, int *blocks_per_sm);
 size_t b_cta_smem(int xp, int sc);
 cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm);
