@@ -1073,6 +1073,61 @@ __global__ void __launch_bounds__(256) k_b_cgs(DevPlan d, const double *__restri
   }
 }
 
+// CGS2 pass 2 fused (the minimal 3-pass schedule): w_out = w_in - V h and,
+// from the same V loads, the block partials of V^T w_out — the second pass's dots.
+template <int NV>
+__global__ void __launch_bounds__(256) k_b_cgs_dots(DevPlan d, const double *__restrict__ V, int nvec,
+                                                    const double *__restrict__ w_in,
+                                                    const double *__restrict__ h, int hstride,
+                                                    double *__restrict__ w_out, const int *__restrict__ mask,
+                                                    double *__restrict__ partials) {
+  __shared__ double sh[BY][32];
+  __shared__ double hs[NV][32];
+  const int sys = blockIdx.y * 32 + threadIdx.x;
+  const bool act = mask[sys] != 0;
+  if (!__syncthreads_or(act)) return;
+  for (int q = threadIdx.y; q < nvec; q += BY) hs[q][threadIdx.x] = act ? h[(size_t)sys * hstride + q] : 0.0;
+  __syncthreads();
+  const size_t vstride = (size_t)d.n * d.nbp;
+  double acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  if (act)
+    for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
+      double v[NV];
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+        if (q < nvec) {
+          v[q] = V[(size_t)q * vstride + IL(d, i, sys)];
+          t += v[q] * hs[q][threadIdx.x];
+        }
+      const double o = w_in[IL(d, i, sys)] - t;
+      w_out[IL(d, i, sys)] = o;
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+        if (q < nvec) acc[q] += v[q] * o;
+    }
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    if (q < nvec) {
+      const double tq = reduce_y<false>(acc[q], sh);
+      if (threadIdx.y == 0 && act) partials[((size_t)sys * nvec + q) * gridDim.x + blockIdx.x] = tq;
+    }
+  }
+}
+
+cudaError_t b_launch_cgs_dots(const DevPlan &d, const double *V, int nvec, const double *w_in,
+                              const double *h, int hstride, double *w_out, const int *mask,
+                              double *partials, cudaStream_t s) {
+  const dim3 g(d.rb, d.nbp >> 5);
+  if (nvec <= 4) k_b_cgs_dots<4><<<g, dim3(32, BY), 0, s>>>(d, V, nvec, w_in, h, hstride, w_out, mask, partials);
+  else if (nvec <= 8) k_b_cgs_dots<8><<<g, dim3(32, BY), 0, s>>>(d, V, nvec, w_in, h, hstride, w_out, mask, partials);
+  else if (nvec <= 16) k_b_cgs_dots<16><<<g, dim3(32, BY), 0, s>>>(d, V, nvec, w_in, h, hstride, w_out, mask, partials);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(256) k_b_scale(DevPlan d, const double *__restrict__ in,
                                                  double *__restrict__ out, const double *__restrict__ den,
                                                  int dstride, const int *__restrict__ mask) {

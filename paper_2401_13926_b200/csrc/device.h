@@ -200,6 +200,9 @@ cudaError_t b_launch_dots(const DevPlan &d, const double *V, int nvec, const dou
 cudaError_t b_launch_cgs(const DevPlan &d, const double *V, int nvec, const double *w_in,
                          const double *h, int hstride, double *w_out, int mode, const int *mask,
                          double *partials, cudaStream_t s);
+cudaError_t b_launch_cgs_dots(const DevPlan &d, const double *V, int nvec, const double *w_in,
+                              const double *h, int hstride, double *w_out, const int *mask,
+                              double *partials, cudaStream_t s);  // nvec <= 16
 cudaError_t b_launch_scale(const DevPlan &d, const double *in, double *out, const double *den,
                            int dstride, const int *mask, cudaStream_t s);
 cudaError_t b_launch_update_x(const DevPlan &d, double *x, const double *Z, const double *y,

@@ -347,7 +347,13 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout,
       d.sys_mask = nullptr;
       const int nv = j + 1;
       // cgs2_step (:93-105): h1 = V^T w; w1 = w - V h1; h2 = V^T w1; w2 = w1 - V h2
-      if (il) {
+      if (il && nv <= 16) {  // 3 passes: h1 = V^T w | w1 = w - V h1 with h2 = V^T w1 | w - V h2, ||.||
+        LAUNCH(b_launch_dots(d, K.V, nv, K.w, K.mask, K.partials, s));
+        LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h1, M + 1, 0, s));
+        LAUNCH(b_launch_cgs_dots(d, K.V, nv, K.w, K.h1, M + 1, K.w1, K.mask, K.partials, s));
+        LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h2, M + 1, 0, s));
+        LAUNCH(b_launch_cgs(d, K.V, nv, K.w1, K.h2, M + 1, K.w, 1, K.mask, K.partials, s));
+      } else if (il) {
         LAUNCH(b_launch_dots(d, K.V, nv, K.w, K.mask, K.partials, s));
         LAUNCH(launch_reduce_partials(d, K.partials, nv, K.h1, M + 1, 0, s));
         LAUNCH(b_launch_cgs(d, K.V, nv, K.w, K.h1, M + 1, K.w1, 0, K.mask, nullptr, s));
