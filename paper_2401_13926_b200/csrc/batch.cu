@@ -1253,9 +1253,133 @@ cudaError_t b_refactor_occupancy(size_t smem, int *blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor, 32 * B_WARPS, smem);
 }
 
+// Variant (KKT_B_CT_MODE=1): warp w replays system sys0 + w alone (32 entry lanes, a
+// __syncwarp per step, no CTA barrier per step), the chunk staged once for the CTA's systems
+// with per-system rows in shared memory (conflict-free replay reads).
+template <int SC>
+__global__ void __launch_bounds__(32 * SC) k_b_refactor_ctaw(DevPlan d, const int2 *__restrict__ tasks,
+                                                            int ntask) {
+  constexpr int NT = 32 * SC;
+  extern __shared__ double csm[];
+  __shared__ int s_task;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  double *xw = csm + (size_t)w * d.h_xp;                     // this warp's workspace [np]
+  double *stv0 = csm + (size_t)d.h_xp * SC;                  // [2][SC][STAGE] (per-system rows)
+  int *sts0 = reinterpret_cast<int *>(stv0 + 2 * CT_STAGE * SC);  // [2][STAGE]
+  while (true) {
+    if (tid == 0) s_task = atomicAdd(d.ticket2, 1);
+    __syncthreads();
+    const int task = s_task;
+    if (task >= ntask) break;
+    const int2 tk = tasks[task];
+    const int j = tk.x, sys0 = tk.y >> 8, sys = sys0 + w;
+    const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
+    const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
+    const int np = nu + 1 + nl;
+    const int t_end = d.so_ptr[j + 1];
+    Chunk cur = chunk_meta(d, d.so_ptr[j], 0, t_end, CT_STAGE, lane);  // every warp alike
+    auto issue = [&](const Chunk &c, int b) {
+      double *stv = stv0 + b * CT_STAGE * SC;
+      int *sts = sts0 + b * CT_STAGE;
+      for (int i = 0; i < c.nsteps; ++i) {
+        const int cnt = __shfl_sync(FULL, c.m.y, i);
+        const int off = __shfl_sync(FULL, c.incl - c.m.y, i);
+        const int lbk = __shfl_sync(FULL, c.m.w, i);
+        for (int f = tid; f < cnt * SC; f += NT)  // global side coalesced (entry-major)
+          cp_async8(&stv[(f % SC) * CT_STAGE + off + f / SC], &d.Lx[IL(d, lbk + f / SC, sys0 + f % SC)]);
+      }
+      const int pair0 = __shfl_sync(FULL, c.m.z, 0);
+      for (int p = tid; p < c.npairs; p += NT) cp_async4(&sts[p], &d.upd_slot32[pair0 + p]);
+      cp_async_commit();
+    };
+    issue(cur, 0);
+    int buf = 0;
+    for (int f = lane; f < np; f += 32) xw[f] = 0.0;
+    __syncwarp();
+    for (int q = d.ap_ptr[j] + lane; q < d.ap_ptr[j + 1]; q += 32)
+      xw[d.a_slot[q]] = d.A_vals[IL(d, d.a_src[q], sys)];
+    while (cur.t0 < t_end) {
+      cp_async_wait<0>();
+      __syncthreads();  // chunk `cur` staged by all threads; the other buffer is free
+      Chunk nxt;
+      nxt.t0 = cur.next_t0;
+      if (nxt.t0 < t_end) {
+        nxt = chunk_meta(d, cur.next_t0, cur.next_e0, t_end, CT_STAGE, lane);
+        issue(nxt, buf ^ 1);  // in flight during this chunk's replay
+      }
+      const double *stv = stv0 + buf * CT_STAGE * SC + w * CT_STAGE;  // this warp's system
+      const int *sts = sts0 + buf * CT_STAGE;
+      for (int i = 0; i < cur.nsteps; ++i) {
+        const int kslot = __shfl_sync(FULL, cur.m.x, i);
+        const int cnt = __shfl_sync(FULL, cur.m.y, i);
+        const int off = __shfl_sync(FULL, cur.incl - cur.m.y, i);
+        const int lbk = __shfl_sync(FULL, cur.m.w, i);
+        const double xk = xw[kslot];
+        for (int e0 = lane; e0 < cnt; e0 += 128) {
+          double lv[4], xv[4];
+          int sl[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (e0 + 32 * q < cnt) {
+              lv[q] = stv[off + e0 + 32 * q];
+              sl[q] = sts[off + e0 + 32 * q];
+            }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (e0 + 32 * q < cnt) xv[q] = xw[sl[q]];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (e0 + 32 * q < cnt) {
+              double l = lv[q];
+              if (is_sentinel(l)) l = wait_value_bo(&d.Lx[IL(d, lbk + e0 + 32 * q, sys)], d.poll_ns);
+              xw[sl[q]] = __dsub_rn(xv[q], __dmul_rn(l, xk));
+            }
+        }
+        __syncwarp();
+      }
+      cur = nxt;
+      buf ^= 1;
+    }
+    cp_async_wait<0>();
+    // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj (published first); U(:,j) = x[Ui]  (:327-344)
+    double ujj = xw[nu];
+    double gm = fabs(ujj);
+    const double eps = patch_floor_b(d, sys);
+    const bool patched = fabs(ujj) < eps;
+    if (patched) ujj = (ujj >= 0.0) ? eps : -eps;
+    for (int i = lane; i < nl; i += 32) {
+      const double v = xw[nu + 1 + i];
+      gm = fmax(gm, fabs(v));
+      st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], unsentinel(__ddiv_rn(v, ujj)));
+    }
+    for (int i = lane; i < nl; i += 32)
+      d.Lv[IL(d, d.Lmap[lb + i], sys)] = unsentinel(__ddiv_rn(xw[nu + 1 + i], ujj));
+    for (int i = lane; i < nu; i += 32) {
+      const double v = xw[i];
+      d.Ux[IL(d, ub + i, sys)] = v;
+      d.Uv[IL(d, d.Umap[ub + i], sys)] = v;
+      gm = fmax(gm, fabs(v));
+    }
+    gm = warp_max(gm);
+    if (lane == 0) {
+      unsigned long long *sc = d.scal + (size_t)sys * SCAL_STRIDE;
+      d.udiag[IL(d, j, sys)] = ujj;
+      if (patched) atomicAdd(&sc[SC_PATCHED], 1ull);
+      if (gm > 0.0 && dbits(gm) > __ldcg(&sc[SC_GMAX])) atomicMax(&sc[SC_GMAX], dbits(gm));
+    }
+    __syncthreads();  // workspaces and stage buffers are reused by the next task
+  }
+}
+
+
 template <int SC>
 static cudaError_t cta_conf(size_t smem, int *blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_b_refactor_cta<SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_b_refactor_ctaw<SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_b_refactor_ctaw<SC>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_b_refactor_cta<SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_b_refactor_cta<SC>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
@@ -1300,9 +1424,15 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blo
   auto launch_wide = [&](cudaStream_t st) {
     const int2 *t2 = d.btask + d.n_btask1;
     const int n2 = d.n_btask - d.n_btask1;
-    if (d.ct_sc == 2) k_b_refactor_cta<2><<<blocks2, 64, smem2, st>>>(d, t2, n2);
-    else if (d.ct_sc == 8) k_b_refactor_cta<8><<<blocks2, 256, smem2, st>>>(d, t2, n2);
-    else k_b_refactor_cta<4><<<blocks2, 128, smem2, st>>>(d, t2, n2);
+    if (d.ct_mode == 1) {
+      if (d.ct_sc == 2) k_b_refactor_ctaw<2><<<blocks2, 64, smem2, st>>>(d, t2, n2);
+      else if (d.ct_sc == 8) k_b_refactor_ctaw<8><<<blocks2, 256, smem2, st>>>(d, t2, n2);
+      else k_b_refactor_ctaw<4><<<blocks2, 128, smem2, st>>>(d, t2, n2);
+    } else {
+      if (d.ct_sc == 2) k_b_refactor_cta<2><<<blocks2, 64, smem2, st>>>(d, t2, n2);
+      else if (d.ct_sc == 8) k_b_refactor_cta<8><<<blocks2, 256, smem2, st>>>(d, t2, n2);
+      else k_b_refactor_cta<4><<<blocks2, 128, smem2, st>>>(d, t2, n2);
+    }
     ++*launches;
   };
   if (ov) {

@@ -204,6 +204,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
     d.n_btask1 = (int)btask.size();
     d.ct_sc = std::getenv("KKT_B_CT_SC") ? std::atoi(std::getenv("KKT_B_CT_SC")) : 8;
     if (d.ct_sc != 2 && d.ct_sc != 8) d.ct_sc = 4;
+    d.ct_mode = std::getenv("KKT_B_CT_MODE") ? std::atoi(std::getenv("KKT_B_CT_MODE")) : 0;
     if (rc2 == KKT_OK) {  // k_b_refactor_cta tasks: (column, ct_sc systems)
       const int start = h.small_lev_ptr[h.n_small_levels];
       for (int c = start; c < h.n; ++c) {

@@ -41,6 +41,7 @@ struct DevPlan {
   int b_xbudget = 0, b_stage = 0, b_static = 0;
   int b_xbudget2 = 0, b_stage2 = 0, n_btask1 = 0;  // second replay launch (wide columns)
   int ct_sc = 4;  // systems per k_b_refactor_cta task (KKT_B_CT_SC = 2 | 4 | 8)
+  int ct_mode = 0;  // 0: entry x system lanes + CTA barrier per step; 1: warp per system
   // Heavy tail (columns >= J0, the dense separator; batched only): refactorized by a CTA per
   // (column, 32 systems) in "pull" form (k_b_refactor_heavy): every workspace slot sums its
   // own updates in the reference order, the slots spread over the CTA's warps, U slots
