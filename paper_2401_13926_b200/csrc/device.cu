@@ -235,7 +235,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.n_small_levels = h.n_small_levels;
   for (int l = 0; l <= h.n_small_levels; ++l) d.lev_ptr[l] = h.small_lev_ptr[l];
   d.ref_start = h.small_lev_ptr[h.n_small_levels];
-  d.poll_ns = std::getenv("KKT_POLL_NS") ? std::atoi(std::getenv("KKT_POLL_NS")) : (nbp > 1 ? 256 : 0);
+  d.poll_ns = std::getenv("KKT_POLL_NS") ? std::atoi(std::getenv("KKT_POLL_NS")) : (nbp > 1 ? 64 : 0);
   d.pL = h.pL;
   d.pU = h.pU;
   d.nLg = (int)h.L_grid_order.size();

@@ -166,8 +166,8 @@ cudaError_t sweep_configure();
 cudaError_t launch_sweep_blocked(const DevPlan &d, bool upper, double *x, cudaStream_t s);
 
 // ---- batched (interleaved, nb > 1) kernels: batch.cu ----
-constexpr int B_XBUDGET = 768;   // default refactor workspace doubles per warp (np * systems)
-constexpr int B_STAGE = 512;     // default stage buffer doubles (pairs * systems), x2 buffers
+constexpr int B_XBUDGET = 576;   // default refactor workspace doubles per warp (np * systems)
+constexpr int B_STAGE = 256;     // default stage buffer doubles (pairs * systems), x2 buffers
 constexpr int B_XBUDGET2 = 2304;  // ... for the wide separator columns (second launch)
 constexpr int B_STAGE2 = 768;
 constexpr int B_WARPS = 4;       // warps per refactor CTA
