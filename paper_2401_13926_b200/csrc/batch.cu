@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "device.h"
@@ -401,10 +402,10 @@ size_t b_cta_smem(int xp, int sc) {
          2 * (size_t)CT_STAGE * sizeof(int) + 64;
 }
 
-template <int CT_SC>
-__global__ void __launch_bounds__(32 * CT_SC) k_b_refactor_cta(DevPlan d, const int2 *__restrict__ tasks,
+template <int CT_SC, int CT_E>
+__global__ void __launch_bounds__(CT_E * CT_SC, CT_E == 64 ? 2 : 3) k_b_refactor_cta(DevPlan d, const int2 *__restrict__ tasks,
                                                                int ntask) {
-  constexpr int CT_THREADS = 32 * CT_SC;   // 32 entry lanes x SC systems
+  constexpr int CT_THREADS = CT_E * CT_SC;  // CT_E entry lanes x SC systems
   extern __shared__ double csm[];
   __shared__ int s_task;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -419,6 +420,10 @@ __global__ void __launch_bounds__(32 * CT_SC) k_b_refactor_cta(DevPlan d, const 
     if (task >= ntask) break;
     const int2 tk = tasks[task];
     const int j = tk.x, sys0 = tk.y >> 8, sys = sys0 + s;
+    if (d.trace_trsv && tid == 0 && 4 * task + 3 < 2 * d.n) {  // KKT_TRACE: {start, end, column}
+      d.trace_trsv[4 * task] = globaltimer();
+      d.trace_trsv[4 * task + 2] = j;
+    }
     const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
     const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
     const int np = nu + 1 + nl;
@@ -443,7 +448,7 @@ __global__ void __launch_bounds__(32 * CT_SC) k_b_refactor_cta(DevPlan d, const 
     int buf = 0;
     for (int f = tid; f < np * CT_SC; f += CT_THREADS) x[f] = 0.0;
     __syncthreads();
-    for (int q = d.ap_ptr[j] + e; q < d.ap_ptr[j + 1]; q += 32)
+    for (int q = d.ap_ptr[j] + e; q < d.ap_ptr[j + 1]; q += CT_E)
       x[d.a_slot[q] * CT_SC + s] = d.A_vals[IL(d, d.a_src[q], sys)];
     while (cur.t0 < t_end) {
       Chunk nxt;
@@ -458,18 +463,44 @@ __global__ void __launch_bounds__(32 * CT_SC) k_b_refactor_cta(DevPlan d, const 
       __syncthreads();  // staged chunk visible; A scatter / previous step done
       const double *stv = stv0 + buf * CT_STAGE * CT_SC;
       const int *sts = sts0 + buf * CT_STAGE;
+      // Step i's static operands (metadata, its staged L value and target slot for this
+      // thread's entry) are fetched while step i-1 is still in flight, so after each
+      // barrier only x[k], x[target], one multiply-subtract and the store remain.
+      int kslot_n = __shfl_sync(FULL, cur.m.x, 0), cnt_n = __shfl_sync(FULL, cur.m.y, 0);
+      int off_n = __shfl_sync(FULL, cur.incl - cur.m.y, 0), lbk_n = __shfl_sync(FULL, cur.m.w, 0);
+      double lv_n = 0.0;
+      int sl_n = 0;
+      if (e < cnt_n) {
+        lv_n = stv[(off_n + e) * CT_SC + s];
+        sl_n = sts[off_n + e] * CT_SC + s;
+      }
       for (int i = 0; i < cur.nsteps; ++i) {
-        const int kslot = __shfl_sync(FULL, cur.m.x, i);
-        const int cnt = __shfl_sync(FULL, cur.m.y, i);
-        const int off = __shfl_sync(FULL, cur.incl - cur.m.y, i);
-        const int lbk = __shfl_sync(FULL, cur.m.w, i);
+        const int kslot = kslot_n, cnt = cnt_n, off = off_n, lbk = lbk_n;
+        const double lv0 = lv_n;
+        const int sl0 = sl_n;
         const double xk = x[kslot * CT_SC + s];
-        for (int idx0 = e; idx0 < cnt; idx0 += 4 * 32) {
+        const double xv0 = e < cnt ? x[sl0] : 0.0;
+        if (i + 1 < cur.nsteps) {
+          kslot_n = __shfl_sync(FULL, cur.m.x, i + 1);
+          cnt_n = __shfl_sync(FULL, cur.m.y, i + 1);
+          off_n = __shfl_sync(FULL, cur.incl - cur.m.y, i + 1);
+          lbk_n = __shfl_sync(FULL, cur.m.w, i + 1);
+          if (e < cnt_n) {
+            lv_n = stv[(off_n + e) * CT_SC + s];
+            sl_n = sts[off_n + e] * CT_SC + s;
+          }
+        }
+        if (e < cnt) {  // this thread's first entry of the step
+          double l = lv0;
+          if (is_sentinel(l)) l = wait_value_bo(&d.Lx[IL(d, lbk + e, sys)], d.poll_ns);
+          x[sl0] = __dsub_rn(xv0, __dmul_rn(l, xk));
+        }
+        for (int idx0 = e + CT_E; idx0 < cnt; idx0 += 4 * CT_E) {  // wide steps: the rest
           double lv[4], xv[4];
           int sl[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int idx = idx0 + 32 * q;
+            const int idx = idx0 + CT_E * q;
             if (idx < cnt) {
               lv[q] = stv[(off + idx) * CT_SC + s];
               sl[q] = sts[off + idx] * CT_SC + s;
@@ -477,10 +508,10 @@ __global__ void __launch_bounds__(32 * CT_SC) k_b_refactor_cta(DevPlan d, const 
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (idx0 + 32 * q < cnt) xv[q] = x[sl[q]];
+            if (idx0 + CT_E * q < cnt) xv[q] = x[sl[q]];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int idx = idx0 + 32 * q;
+            const int idx = idx0 + CT_E * q;
             if (idx < cnt) {
               double l = lv[q];
               if (is_sentinel(l)) l = wait_value_bo(&d.Lx[IL(d, lbk + idx, sys)], d.poll_ns);
@@ -501,14 +532,14 @@ __global__ void __launch_bounds__(32 * CT_SC) k_b_refactor_cta(DevPlan d, const 
     const double eps = patch_floor_b(d, sys);
     const bool patched = fabs(ujj) < eps;
     if (patched) ujj = (ujj >= 0.0) ? eps : -eps;
-    for (int i = e; i < nl; i += 32) {
+    for (int i = e; i < nl; i += CT_E) {
       const double v = x[(nu + 1 + i) * CT_SC + s];
       gm = fmax(gm, fabs(v));
       st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], unsentinel(__ddiv_rn(v, ujj)));
     }
-    for (int i = e; i < nl; i += 32)
+    for (int i = e; i < nl; i += CT_E)
       d.Lv[IL(d, d.Lmap[lb + i], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + i) * CT_SC + s], ujj));
-    for (int i = e; i < nu; i += 32) {
+    for (int i = e; i < nu; i += CT_E) {
       const double v = x[i * CT_SC + s];
       d.Ux[IL(d, ub + i, sys)] = v;
       d.Uv[IL(d, d.Umap[ub + i], sys)] = v;
@@ -517,6 +548,7 @@ __global__ void __launch_bounds__(32 * CT_SC) k_b_refactor_cta(DevPlan d, const 
     for (int o = CT_SC; o < 32; o <<= 1) gm = fmax(gm, __shfl_xor_sync(FULL, gm, o));
     if (lane < CT_SC) {  // one lane per system and warp: warp-level maxima are order-free
       unsigned long long *sc = d.scal + (size_t)sys * SCAL_STRIDE;
+      if (d.trace_trsv && tid == 0 && 4 * task + 3 < 2 * d.n) d.trace_trsv[4 * task + 1] = globaltimer();
       if (tid < CT_SC) {
         d.udiag[IL(d, j, sys)] = ujj;
         if (patched) atomicAdd(&sc[SC_PATCHED], 1ull);
@@ -525,6 +557,373 @@ __global__ void __launch_bounds__(32 * CT_SC) k_b_refactor_cta(DevPlan d, const 
     }
     __syncthreads();
   }
+}
+
+// ----------------------------------------------------------------------------
+// Refactor, wide columns through a TMA / mbarrier pipeline (ct_mode 3, default).  A CTA is
+// one producer warp + 8 consumer warps; a task is (column j >= J2, 8 systems).  The replay
+// arithmetic and per-entry order are k_b_refactor_cta's (direct_lu.py:324-344).
+//  producer: cuts so(j) into chunks (steps, or pieces of a step, whose rows rounded up to
+//   the 8-row box fit TS_STG), waits for the stage to drain, waits for the done flag of
+//   every wide column k the chunk reads (its L(:,k) values for these systems are final),
+//   writes the step metadata, arms the stage's full barrier with the byte count and issues
+//   the copies: L rows by 2-D TMA (boxes 128 / 32 / 8 rows x 8 systems over [nnz_L][nbp]),
+//   update slots by a 1-D bulk copy of a 16-byte-aligned superset.
+//  consumers: wait full -> replay the steps (one named barrier per step, no sentinel checks,
+//   no polling) -> release the stage -> after the last chunk u_jj, L(:,j), U(:,j) as in
+//   k_b_refactor_cta, then raise the column's flag (per-thread fence, barrier, release).
+// ----------------------------------------------------------------------------
+// stages x rows per stage (KKT_B_TMA=ns,rows): 2 x 256 (default), 3 x 160, 4 x 128
+constexpr int TS_SC = 8;                         // systems per task
+constexpr int TS_THREADS = 32 + 32 * TS_SC;      // producer warp + consumers
+__host__ __device__ constexpr int ts_slots(int stg) { return stg + 6 * 32 + 8; }  // + alignment slack
+
+size_t b_tma_smem_ns(int xp, int ns, int stg) {
+  return (size_t)ns * stg * TS_SC * 8 + (size_t)ns * ts_slots(stg) * 4 + (size_t)ns * 33 * 16 + 2 * ns * 8 +
+         (size_t)xp * TS_SC * 8 + 64;
+}
+void b_tma_shape(int *ns, int *stg) {  // KKT_B_TMA=ns,rows among the instantiated shapes
+  int a = 2, b = 256;
+  if (const char *e = std::getenv("KKT_B_TMA")) std::sscanf(e, "%d,%d", &a, &b);
+  if (!((a == 2 && b == 256) || (a == 3 && b == 160) || (a == 4 && b == 128) || (a == 3 && b == 256) ||
+        (a == 2 && b == 384))) {
+    a = 2;
+    b = 256;
+  }
+  *ns = a;
+  *stg = b;
+}
+size_t b_tma_smem(int xp, int ns, int stg) { return b_tma_smem_ns(xp, ns, stg); }
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, unsigned tx) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_rows(void *dst, const CUtensorMap *m, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"((unsigned long long)m), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ int ld_acquire_i32(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_i32(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * TS_SC) : "memory"); }
+
+template <int TS_NS, int TS_STG>
+__global__ void __launch_bounds__(TS_THREADS, 3)
+    k_b_refactor_tma(const __grid_constant__ DevPlan d, const int2 *__restrict__ tasks, int ntask) {
+  constexpr int TS_SLOTS = ts_slots(TS_STG);
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  __shared__ int s_task;
+  double *stv0 = reinterpret_cast<double *>(tsm);                                    // [NS][STG][8]
+  int *sts0 = reinterpret_cast<int *>(tsm + (size_t)TS_NS * TS_STG * TS_SC * 8);     // [NS][SLOTS]
+  int4 *meta0 = reinterpret_cast<int4 *>(sts0 + TS_NS * TS_SLOTS);                   // [NS][32]
+  int4 *hdr = meta0 + TS_NS * 32;                                                    // [NS]
+  uint64_t *full = reinterpret_cast<uint64_t *>(hdr + TS_NS);
+  uint64_t *empty = full + TS_NS;
+  double *x = reinterpret_cast<double *>(empty + TS_NS);                             // [xp][8]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < TS_NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int G = d.nbp / TS_SC;
+  int stage = 0;
+  unsigned phase = 0;  // ring position: producer and consumers walk the same chunk sequence
+  while (true) {
+    if (tid == 0) s_task = atomicAdd(d.ticket2, 1);
+    __syncthreads();
+    const int task = s_task;
+    if (task >= ntask) break;
+    const int2 tk = tasks[task];
+    const int j = tk.x, sys0 = tk.y >> 8, g = sys0 / TS_SC;
+    const int t_begin = d.so_ptr[j], t_end = d.so_ptr[j + 1];
+    unsigned long long *trc = (d.trace_trsv && 8 * task + 7 < 2 * d.n) ? d.trace_trsv + 8 * task : nullptr;
+    if (trc && tid == 0) {  // KKT_TRACE: {start, end, column, last flag seen, last chunk, steps done, fenced}
+      trc[0] = globaltimer();
+      trc[2] = j;
+    }
+    if (warp == 0) {
+      // ---------------- producer ----------------
+      // The so_meta / so_dep window of the next chunk is fetched while this one is staged,
+      // and its dependency flags are read at the end of the iteration, so a chunk normally
+      // starts with everything in registers (a flag still down is then polled).
+      int t0 = t_begin, e0 = 0;
+      int4 pm = make_int4(0, 0, 0, 0);
+      int pdep = -1, pfl = 1;
+      if (t0 + lane < t_end) {
+        pm = d.so_meta[t0 + lane];
+        pdep = d.so_dep[t0 + lane - d.so_dep0];
+        if (pdep >= 0) pfl = ld_acquire_i32(d.cflag + (size_t)pdep * G + g);
+      }
+      while (t0 < t_end) {
+        const int t = t0 + lane;
+        int4 m = pm;  // {slot of k, |L(:,k)|, first pair, first L index}
+        const int dep = pdep, fl = pfl;
+        if (lane == 0) {  // resume inside step t0
+          m.y -= e0;
+          m.z += e0;
+          m.w += e0;
+        }
+        int r = (m.y + 7) & ~7;  // staged rows: whole 8-row boxes
+        int incl = r;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += v;
+        }
+        int nsteps = __popc(__ballot_sync(FULL, t < t_end && incl <= TS_STG));
+        // end the chunk before the first step whose column was not yet published when its
+        // flag was read: the steps ahead of it need not wait for it
+        const unsigned late = __ballot_sync(FULL, t < t_end && dep >= 0 && fl == 0) & ~1u;
+        if (late) nsteps = min(nsteps, __ffs(late) - 1);
+        int nt0, ne0;
+        if (nsteps == 0) {  // step t0 alone exceeds the stage: a piece of TS_STG rows
+          if (lane == 0) {
+            m.y = TS_STG;
+            r = TS_STG;
+            incl = TS_STG;
+          }
+          nsteps = 1;
+          nt0 = t0;
+          ne0 = e0 + TS_STG;
+        } else {
+          nt0 = t0 + nsteps;
+          ne0 = 0;
+          pm = make_int4(0, 0, 0, 0);
+          pdep = -1;
+          pfl = 1;
+          if (nt0 + lane < t_end) {
+            pm = d.so_meta[nt0 + lane];
+            pdep = d.so_dep[nt0 + lane - d.so_dep0];
+          }
+        }
+        const bool mine = lane < nsteps;
+        const int mis = m.z & 3;
+        const int sw = (mine && m.y > 0) ? ((mis + m.y + 3) & ~3) : 0;  // slot ints copied
+        int sincl = sw;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(FULL, sincl, o);
+          if (lane >= o) sincl += v;
+        }
+        // Only the chunk's first step can still be unpublished (the cut above).  Its rows are
+        // then not staged: the consumers read them from L2 once the flag is seen (one round
+        // trip instead of flag -> TMA -> barrier on the critical chain); everything else of
+        // the chunk is in flight before the flag wait.
+        const bool late0 = __shfl_sync(FULL, dep >= 0 && fl == 0, 0);
+        const bool direct = late0 && d.tma_direct;
+        if (late0 && !direct && lane == 0) {  // (KKT_B_TMA_DIRECT=0: stage it after the flag)
+          const int *f = d.cflag + (size_t)dep * G + g;
+          unsigned ns = 32;
+          while (ld_acquire_i32(f) == 0) {
+            __nanosleep(ns);
+            ns = ns < 64 ? 2 * ns : 64;
+          }
+        }
+        if (mine && dep >= 0 && !(direct && lane == 0)) asm volatile("fence.proxy.async.global;" ::: "memory");
+        mbar_wait(&empty[stage], phase ^ 1);
+        int4 *meta = meta0 + stage * 32;
+        if (mine) meta[lane] = make_int4(m.x, m.y, (direct && lane == 0) ? -(m.w + 1) : incl - r, sincl - sw + mis);
+        const int rows = __shfl_sync(FULL, incl, nsteps - 1) - (direct ? __shfl_sync(FULL, r, 0) : 0);
+        const int ints = __shfl_sync(FULL, sincl, nsteps - 1);
+        if (lane == 0) hdr[stage] = make_int4(nsteps, nt0 >= t_end ? 1 : 0, 0, 0);
+        __syncwarp();
+        if (lane == 0) mbar_expect_tx(&full[stage], (unsigned)(rows * TS_SC * 8 + ints * 4));
+        __syncwarp();
+        if (mine && !(direct && lane == 0)) {
+          double *dst = stv0 + ((size_t)stage * TS_STG + (incl - r)) * TS_SC;
+          int row = m.w, left = r;
+          for (; left >= 128; left -= 128, row += 128, dst += 128 * TS_SC) tma_rows(dst, &d.tmL[0], sys0, row, &full[stage]);
+          for (; left >= 32; left -= 32, row += 32, dst += 32 * TS_SC) tma_rows(dst, &d.tmL[1], sys0, row, &full[stage]);
+          for (; left >= 8; left -= 8, row += 8, dst += 8 * TS_SC) tma_rows(dst, &d.tmL[2], sys0, row, &full[stage]);
+        }
+        if (mine && sw > 0)
+          bulk_copy(sts0 + stage * TS_SLOTS + (sincl - sw), d.upd_slot32 + (m.z - mis), (unsigned)sw * 4,
+                    &full[stage]);
+        if (direct && lane == 0) {  // wait until the wide column k's L values are published
+          const int *f = d.cflag + (size_t)dep * G + g;
+          unsigned ns = 32;
+          while (ld_acquire_i32(f) == 0) {
+            __nanosleep(ns);
+            ns = ns < 64 ? 2 * ns : 64;
+          }
+          if (trc) trc[3] = globaltimer();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (++stage == TS_NS) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (nt0 != t0 && pdep >= 0) pfl = ld_acquire_i32(d.cflag + (size_t)pdep * G + g);
+        else if (nt0 == t0) pfl = lane == 0 ? 1 : fl;  // next piece of step t0 (flag seen): same window
+        t0 = nt0;
+        e0 = ne0;
+      }
+    } else {
+      // ---------------- consumers ----------------
+      const int ct = tid - 32, e = ct / TS_SC, s = ct % TS_SC, sys = sys0 + s;
+      const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
+      const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
+      const int np = nu + 1 + nl;
+      for (int f = ct; f < np * TS_SC; f += 32 * TS_SC) x[f] = 0.0;
+      consumer_bar();
+      for (int q = d.ap_ptr[j] + e; q < d.ap_ptr[j + 1]; q += 32)
+        x[d.a_slot[q] * TS_SC + s] = d.A_vals[IL(d, d.a_src[q], sys)];
+      consumer_bar();
+      if (t_begin < t_end) {
+        while (true) {
+          mbar_wait(&full[stage], phase);
+          const int4 h = hdr[stage];
+          if (trc && ct == 0 && h.y) trc[4] = globaltimer();
+          const double *stv = stv0 + (size_t)stage * TS_STG * TS_SC;
+          const int *sts = sts0 + stage * TS_SLOTS;
+          const int4 *meta = meta0 + stage * 32;
+          for (int i = 0; i < h.x; ++i) {
+            const int4 m = meta[i];  // {slot of k, entries, first staged row, first staged slot}
+            const double xk = x[m.x * TS_SC + s];
+            for (int idx0 = e; idx0 < m.y; idx0 += 4 * 32) {
+              double lv[4], xv[4];
+              int sl[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int idx = idx0 + 32 * q;
+                if (idx < m.y) {
+                  lv[q] = m.z >= 0 ? stv[(m.z + idx) * TS_SC + s] : ld_relaxed_f64(&d.Lx[IL(d, -m.z - 1 + idx, sys)]);
+                  sl[q] = sts[m.w + idx] * TS_SC + s;
+                }
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (idx0 + 32 * q < m.y) xv[q] = x[sl[q]];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (idx0 + 32 * q < m.y) x[sl[q]] = __dsub_rn(xv[q], __dmul_rn(lv[q], xk));
+            }
+            consumer_bar();  // x[k] of the next step may have been updated in this one
+          }
+          if (ct == 0) mbar_arrive(&empty[stage]);
+          const bool last = h.y != 0;
+          if (++stage == TS_NS) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (last) break;
+        }
+      }
+      // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj; U(:,j) = x[Ui]  (direct_lu.py:327-344)
+      if (trc && ct == 0) trc[5] = globaltimer();
+      double ujj = x[nu * TS_SC + s];
+      double gm = fabs(ujj);
+      const double eps = patch_floor_b(d, sys);
+      const bool patched = fabs(ujj) < eps;
+      if (patched) ujj = (ujj >= 0.0) ? eps : -eps;
+      for (int i = e; i < nl; i += 32) {
+        const double v = x[(nu + 1 + i) * TS_SC + s];
+        gm = fmax(gm, fabs(v));
+        d.Lx[IL(d, lb + i, sys)] = unsentinel(__ddiv_rn(v, ujj));
+      }
+      if (d.poll_ns < 0) __threadfence();  // (diagnostic: per-thread fences)
+      consumer_bar();  // every L(:,j) store of the CTA precedes the release below
+      if (trc && ct == 0) trc[6] = globaltimer();
+      if (ct == 0) st_release_i32(&d.cflag[(size_t)(j - d.J2) * G + g], 1);
+      if (trc && ct == 0) trc[1] = globaltimer();
+      for (int i = e; i < nl; i += 32)
+        d.Lv[IL(d, d.Lmap[lb + i], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + i) * TS_SC + s], ujj));
+      for (int i = e; i < nu; i += 32) {
+        const double v = x[i * TS_SC + s];
+        d.Ux[IL(d, ub + i, sys)] = v;
+        d.Uv[IL(d, d.Umap[ub + i], sys)] = v;
+        gm = fmax(gm, fabs(v));
+      }
+      for (int o = TS_SC; o < 32; o <<= 1) gm = fmax(gm, __shfl_xor_sync(FULL, gm, o));
+      if (lane < TS_SC) {  // one lane per system and warp: warp-level maxima are order-free
+        unsigned long long *sc = d.scal + (size_t)sys * SCAL_STRIDE;
+        if (ct < TS_SC) {
+          d.udiag[IL(d, j, sys)] = ujj;
+          if (patched) atomicAdd(&sc[SC_PATCHED], 1ull);
+        }
+        if (gm > 0.0 && dbits(gm) > __ldcg(&sc[SC_GMAX])) atomicMax(&sc[SC_GMAX], dbits(gm));
+      }
+    }
+    __syncthreads();  // workspace reused by the next task
+  }
+}
+
+cudaError_t b_tma_maps(DevPlan &d) {
+  typedef CUresult (*Encode)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess) return e;
+  if (!fn || q != cudaDriverEntryPointSuccess) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {(cuuint64_t)d.nbp, (cuuint64_t)std::max<int64_t>(d.nnz_L, 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)d.nbp * 8};
+  const cuuint32_t rows[3] = {128, 32, 8}, es[2] = {1, 1};
+  for (int i = 0; i < 3; ++i) {
+    const cuuint32_t box[2] = {(cuuint32_t)TS_SC, rows[i]};
+    const CUresult r = ((Encode)fn)(&d.tmL[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, d.Lx, dims, strides, box, es,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
+}
+
+template <int NS, int STG>
+static cudaError_t tma_conf(size_t smem, int *blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_b_refactor_tma<NS, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_b_refactor_tma<NS, STG>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_tma<NS, STG>, TS_THREADS, smem);
+  return e;
+}
+cudaError_t b_tma_configure(int ns, int stg, size_t smem, int *blocks_per_sm) {
+  if (ns == 3 && stg == 256) return tma_conf<3, 256>(smem, blocks_per_sm);
+  if (ns == 2 && stg == 384) return tma_conf<2, 384>(smem, blocks_per_sm);
+  return ns == 4 ? tma_conf<4, 128>(smem, blocks_per_sm)
+                 : ns == 3 ? tma_conf<3, 160>(smem, blocks_per_sm) : tma_conf<2, 256>(smem, blocks_per_sm);
 }
 
 // ----------------------------------------------------------------------------
@@ -1373,24 +1772,30 @@ __global__ void __launch_bounds__(32 * SC) k_b_refactor_ctaw(DevPlan d, const in
 
 
 template <int SC>
-static cudaError_t cta_conf(size_t smem, int *blocks_per_sm) {
+static cudaError_t cta_conf(size_t smem, int *blocks_per_sm, bool wide) {
   cudaError_t e = cudaFuncSetAttribute(k_b_refactor_ctaw<SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_b_refactor_ctaw<SC>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_b_refactor_cta<SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(k_b_refactor_cta<SC, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_b_refactor_cta<SC>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    e = cudaFuncSetAttribute(k_b_refactor_cta<SC, 32>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess && SC == 8)
+    e = cudaFuncSetAttribute(k_b_refactor_cta<8, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess && SC == 8)
+    e = cudaFuncSetAttribute(k_b_refactor_cta<8, 64>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_cta<SC>, 32 * SC, smem);
+    e = wide ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_cta<8, 64>, 512, smem)
+             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_cta<SC, 32>, 32 * SC, smem);
   return e;
 }
 
-cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm) {
-  return sc == 2 ? cta_conf<2>(smem, blocks_per_sm) : sc == 8 ? cta_conf<8>(smem, blocks_per_sm)
-                                                              : cta_conf<4>(smem, blocks_per_sm);
+cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm, bool wide) {
+  return sc == 2 ? cta_conf<2>(smem, blocks_per_sm, false) : sc == 8 ? cta_conf<8>(smem, blocks_per_sm, wide)
+                                                                     : cta_conf<4>(smem, blocks_per_sm, false);
 }
 
 cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blocks2, size_t smem2,
@@ -1419,19 +1824,28 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blo
   const bool ov = two && d.n_btask1 && s2 && ev_a && ev_b && blocks_ov > 0;
   if (two) {
     cudaError_t e2 = cudaMemsetAsync(d.ticket2, 0, 4, s);
+    if (e2 == cudaSuccess && d.ct_mode == 3)
+      e2 = cudaMemsetAsync(d.cflag, 0, 4 * (size_t)(d.n - d.J2) * (d.nbp / TS_SC), s);
     if (e2 != cudaSuccess) return e2;
   }
   auto launch_wide = [&](cudaStream_t st) {
     const int2 *t2 = d.btask + d.n_btask1;
     const int n2 = d.n_btask - d.n_btask1;
-    if (d.ct_mode == 1) {
+    if (d.ct_mode == 3) {
+      if (d.tma_ns == 3 && d.tma_stg == 256) k_b_refactor_tma<3, 256><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else if (d.tma_ns == 2 && d.tma_stg == 384) k_b_refactor_tma<2, 384><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else if (d.tma_ns == 4) k_b_refactor_tma<4, 128><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else if (d.tma_ns == 3) k_b_refactor_tma<3, 160><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else k_b_refactor_tma<2, 256><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+    } else if (d.ct_mode == 1) {
       if (d.ct_sc == 2) k_b_refactor_ctaw<2><<<blocks2, 64, smem2, st>>>(d, t2, n2);
       else if (d.ct_sc == 8) k_b_refactor_ctaw<8><<<blocks2, 256, smem2, st>>>(d, t2, n2);
       else k_b_refactor_ctaw<4><<<blocks2, 128, smem2, st>>>(d, t2, n2);
     } else {
-      if (d.ct_sc == 2) k_b_refactor_cta<2><<<blocks2, 64, smem2, st>>>(d, t2, n2);
-      else if (d.ct_sc == 8) k_b_refactor_cta<8><<<blocks2, 256, smem2, st>>>(d, t2, n2);
-      else k_b_refactor_cta<4><<<blocks2, 128, smem2, st>>>(d, t2, n2);
+      if (d.ct_sc == 2) k_b_refactor_cta<2, 32><<<blocks2, 64, smem2, st>>>(d, t2, n2);
+      else if (d.ct_sc == 8 && d.ct_mode == 2) k_b_refactor_cta<8, 64><<<blocks2, 512, smem2, st>>>(d, t2, n2);
+      else if (d.ct_sc == 8) k_b_refactor_cta<8, 32><<<blocks2, 256, smem2, st>>>(d, t2, n2);
+      else k_b_refactor_cta<4, 32><<<blocks2, 128, smem2, st>>>(d, t2, n2);
     }
     ++*launches;
   };

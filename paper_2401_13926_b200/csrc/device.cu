@@ -166,6 +166,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   // the SMs several times over whatever the number of 32-system groups
   d.rb = nb == 1 ? RED_BLOCKS : std::max(64, 8 * 148 / (nbp / 32));
   std::vector<int2> btask;
+  std::vector<int> so_dep;  // wide-column steps: k - J2 for a wide k, else -1 (ct_mode 3)
   HeavyPlan heavy;
   d.b_xbudget = B_XBUDGET;
   d.b_stage = B_STAGE;  // doubles per stage buffer (two buffers per warp)
@@ -201,10 +202,21 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
         break;
       }
     if (rc2 == KKT_OK) rc2 = build_batch_tasks(h, nbp, d.b_xbudget, 0, J2, btask);
+    if (J2 < h.n) {
+      d.J2 = J2;
+      d.so_dep0 = (int)h.so_ptr[J2];
+      so_dep.resize(h.so_data.size() - (size_t)h.so_ptr[J2]);
+      for (size_t t = 0; t < so_dep.size(); ++t) {
+        const int64_t k = h.so_data[d.so_dep0 + t];
+        so_dep[t] = (k >= J2 && k < d.J0) ? (int)(k - J2) : -1;
+      }
+    }
     d.n_btask1 = (int)btask.size();
     d.ct_sc = std::getenv("KKT_B_CT_SC") ? std::atoi(std::getenv("KKT_B_CT_SC")) : 8;
     if (d.ct_sc != 2 && d.ct_sc != 8) d.ct_sc = 4;
-    d.ct_mode = std::getenv("KKT_B_CT_MODE") ? std::atoi(std::getenv("KKT_B_CT_MODE")) : 0;
+    d.ct_mode = std::getenv("KKT_B_CT_MODE") ? std::atoi(std::getenv("KKT_B_CT_MODE")) : 3;
+    if (d.ct_mode == 3 && (d.ct_sc != 8 || (nbp & 7))) d.ct_mode = 0;  // the TMA pipeline serves 8 systems
+    d.tma_direct = std::getenv("KKT_B_TMA_DIRECT") ? std::atoi(std::getenv("KKT_B_TMA_DIRECT")) : 1;
     if (rc2 == KKT_OK) {  // k_b_refactor_cta tasks: (column, ct_sc systems)
       const int start = h.small_lev_ptr[h.n_small_levels];
       for (int c = start; c < h.n; ++c) {
@@ -276,6 +288,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   acc(4 * h.L_glev_ptr.size()); acc(4 * h.U_glev_ptr.size()); acc(64);     // levels, barrier
   acc(4 * heavy.col.size()); acc(4 * heavy.optr.size()); acc(4 * heavy.pp.size());
   acc(2 * heavy.ord.size()); acc(8 * heavy.pairs.size()); acc(64);          // heavy tail
+  const size_t ncflag = d.J2 < n ? (size_t)(n - d.J2) * (size_t)(nbp / 8 + 1) : 0;
+  acc(4 * so_dep.size()); acc(4 * ncflag);                                 // wide-column flags
   for (const HostSweep *hs : {&h.swL, &h.swU}) {
     acc(4 * hs->dptr.size()); acc(4 * hs->dsrc.size()); acc(2 * hs->ddst.size());
     acc(4 * hs->dmask.size()); acc(4 * hs->bptr.size()); acc(4 * hs->brow.size());
@@ -349,6 +363,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   d.h_ord = carve<uint16_t>(cur, heavy.ord.size());
   d.h_pairs = carve<int2>(cur, heavy.pairs.size());
   d.ticket2 = carve<int>(cur, 16);
+  d.so_dep = carve<int>(cur, so_dep.size());
+  d.cflag = carve<int>(cur, ncflag);
   {
     const HostSweep *hs[2] = {&h.swL, &h.swU};
     SweepDev *sd[2] = {&d.swL, &d.swU};
@@ -417,6 +433,7 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   UP(d.Ui, h.Ui32);
   UP(d.Ltail_split, h.Ltail_split);
   UP(d.btask, btask);
+  UP(d.so_dep, so_dep);
   UP(d.hc_col, heavy.col);
   UP(d.hc_optr, heavy.optr);
   UP(d.h_pp, heavy.pp);
@@ -477,16 +494,23 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   if (nbp > 1) {
     int rbps = 0, tbps = 0;
     dev->refactor_smem = b_refactor_smem(d.b_xbudget, d.b_stage);
-    const size_t smem2 = b_cta_smem(std::max(d.h_xp, 1), d.ct_sc);
+    if (d.ct_mode == 3) b_tma_shape(&d.tma_ns, &d.tma_stg);
+    const size_t smem2 = d.ct_mode == 3 ? b_tma_smem(std::max(d.h_xp, 1), d.tma_ns, d.tma_stg)
+                                        : b_cta_smem(std::max(d.h_xp, 1), d.ct_sc);
     int rbps2 = 0;
     CUDA_TRY(b_configure(nbp, dev->refactor_smem, &rbps, &tbps));
-    CUDA_TRY(b_cta_configure(d.ct_sc, smem2, &rbps2));
+    if (d.ct_mode == 3) {
+      CUDA_TRY(b_tma_configure(d.tma_ns, d.tma_stg, smem2, &rbps2));
+      CUDA_TRY(b_tma_maps(d));
+    } else {
+      CUDA_TRY(b_cta_configure(d.ct_sc, smem2, &rbps2, d.ct_mode == 2));
+    }
     dev->refactor_blocks2 = std::max(1, rbps2) * dev->sm_count;
     dev->refactor_smem2 = smem2;
     // overlapped launches (KKT_B_OVERLAP=1; measured slower): one wide-column CTA per SM next to
     // as many warp-replay CTAs as still fit
     const int ov = std::getenv("KKT_B_OVERLAP") ? std::atoi(std::getenv("KKT_B_OVERLAP")) : 0;
-    if (ov && rbps2 >= 1) {
+    if (ov && rbps2 >= 1 && d.ct_mode != 3) {  // (the TMA pipeline needs phase 1 complete)
       cudaDeviceProp prop;
       CUDA_TRY(cudaGetDeviceProperties(&prop, dev->device));
       const size_t sm_left = prop.sharedMemPerMultiprocessor - smem2 - prop.reservedSharedMemPerBlock;

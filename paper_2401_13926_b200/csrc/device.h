@@ -6,6 +6,7 @@
 // (task, system) pairs dispatched in dependency (level) order, so the dependency chains of
 // all systems advance together in one launch (the batched path).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "plan.h"
@@ -41,7 +42,8 @@ struct DevPlan {
   int b_xbudget = 0, b_stage = 0, b_static = 0;
   int b_xbudget2 = 0, b_stage2 = 0, n_btask1 = 0;  // second replay launch (wide columns)
   int ct_sc = 4;  // systems per k_b_refactor_cta task (KKT_B_CT_SC = 2 | 4 | 8)
-  int ct_mode = 0;  // 0: entry x system lanes + CTA barrier per step; 1: warp per system
+  int ct_mode = 3;  // 3 (default): TMA pipeline; 0: entry x system lanes + CTA barrier per step;
+                  // 1: warp per system; 2: 64 entry lanes (KKT_B_CT_MODE)
   // Heavy tail (columns >= J0, the dense separator; batched only): refactorized by a CTA per
   // (column, 32 systems) in "pull" form (k_b_refactor_heavy): every workspace slot sums its
   // own updates in the reference order, the slots spread over the CTA's warps, U slots
@@ -52,6 +54,17 @@ struct DevPlan {
   uint16_t *h_ord = nullptr;               // per heavy column: slots in pull order
   int2 *h_pairs = nullptr;                 // {source slot, L index}, slot-major, step order
   int *ticket2 = nullptr;
+  // Wide columns through the TMA pipeline (k_b_refactor_tma, ct_mode 3): a producer warp
+  // stages each chunk's L(:,k) rows (2-D tensor maps over Lx viewed as [nnz_L][nbp], boxes of
+  // 128 / 32 / 8 rows x 8 systems) and update slots (1-D bulk copies) into an mbarrier ring
+  // once the dependency column's done flag is up; the consumer warps only replay.
+  int J2 = 0x7fffffff;                     // first wide column
+  int so_dep0 = 0;                         // so index of the first wide column's first step
+  int *so_dep = nullptr;                   // per wide-column step: k - J2 (wide k) or -1
+  int *cflag = nullptr;                    // [(j - J2) * nbp / 8 + group]: L(:,j) published
+  int tma_ns = 2, tma_stg = 256;           // stages x rows (KKT_B_TMA)
+  int tma_direct = 1;                      // late step read from L2 after the flag (KKT_B_TMA_DIRECT)
+  CUtensorMap tmL[3];                      // Lx boxes of 128, 32, 8 rows x 8 systems
   unsigned long long *prof = nullptr;  // optional per-warp cycle counters (KKT_TRACE, batched)
   int rb = RED_BLOCKS;  // reduction blocks per system
   int64_t nnz_a = 0, in_nnz = 0, in_cap = 0, nnz_L = 0, nnz_U = 0, n_so = 0, n_upd = 0, n_ap = 0;
@@ -179,7 +192,11 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blo
                               cudaEvent_t ev_a = nullptr, cudaEvent_t ev_b = nullptr, int blocks_ov = 0);
 cudaError_t b_refactor_occupancy(size_t smem, int *blocks_per_sm);
 size_t b_cta_smem(int xp, int sc);
-cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm);
+void b_tma_shape(int *ns, int *stg);
+size_t b_tma_smem(int xp, int ns, int stg);
+cudaError_t b_tma_configure(int ns, int stg, size_t smem, int *blocks_per_sm);
+cudaError_t b_tma_maps(DevPlan &d);  // encode d.tmL over d.Lx
+cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm, bool wide);
 cudaError_t b_launch_diag_stats(const DevPlan &d, cudaStream_t s);
 cudaError_t b_launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,
                           cudaStream_t s, long long *launches);

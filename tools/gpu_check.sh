@@ -1,3 +1,3 @@
-for st in 256 512 1024; do cp tools/libs_tmp/lib_rs$st.so paper_2401_13926_b200/libkktb200.so; touch paper_2401_13926_b200/libkktb200.so
-echo "stage=$st $(timeout 120 python tools/probe_kernels.py activsg10k 1 5 | cut -c1-100)"
-done
+timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 600 python bench.py 2>&1 | tail -1
