@@ -268,6 +268,10 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d, const in
     const TaskInfo ti = nt;
     const long long t_task = prof ? clock64() : 0;
     const int my_task = cur_task;
+    if (prof && lane == 0 && 100000 + 2 * (size_t)my_task + 1 < 4 * (size_t)d.n) {  // {start, column}
+      d.prof[100000 + 2 * (size_t)my_task] = globaltimer();
+      d.prof[100000 + 2 * (size_t)my_task + 1] = ti.j;
+    }
     if (d.b_static) ticket += nw;
     else if (lane == 0) ticket = atomicAdd(d.ticket, 1);
     const int j = ti.j, lgS = ti.lgS, sys0 = ti.sys0;
