@@ -388,10 +388,10 @@ def main():
     kd = kern[dom]
     # DRAM traffic of the dominant kernel family from the committed ncu --set full capture
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r1f_ncu_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r1g_ncu_traffic.json")
     if os.path.exists(tp):
         tk = json.load(open(tp))["kernels"]
-        fam = {"refactor": ["k_b_refactor", "k_b_refactor_cta<8>"], "spmv": ["k_b_spmv"],
+        fam = {"refactor": ["k_b_refactor", "k_b_refactor_tma<2, 256>"], "spmv": ["k_b_spmv"],
                "trisolve_pair": ["k_b_trsv_grid<0>", "k_b_trsv_grid<1>", "k_trsv_blocked<0, 1, 1>",
                                  "k_trsv_blocked<1, 1, 1>"]}[dom]
         if all(k in tk for k in fam):
