@@ -79,17 +79,19 @@ def test_full_size_against_oracle(config, k):
     assert rr <= max(1.5 * rr_o, 4 * np.finfo(float).eps), (rr, rr_o)
 
 
-@pytest.mark.parametrize("config", ["activsg200", "activsg10k"])
-def test_full_size_batch_equals_single(config):
-    """The interleaved batch reproduces each system's single-system factors and solve."""
+@pytest.mark.parametrize("config,nb", [("activsg200", 4), ("activsg10k", 4), ("activsg2000", 40)])
+def test_full_size_batch_equals_single(config, nb):
+    """The interleaved batch reproduces each system's single-system factors and solve (nb = 40:
+    8-system groups of the TMA wide-column pipeline, every group's done flags and the
+    padding systems of the last 32-block)."""
     import torch
     import paper_2401_13926_b200._native as nat
     from paper_2401_13926_b200.acopf import system_rhs, system_values
     from paper_2401_13926_b200.device import DeviceSystem
     pat, K0, f = _setup(config)
-    ks = [3, 11, 17, 19]
-    vals = np.stack([system_values(pat, k, q) for q, k in enumerate(ks)])
-    rhs = np.stack([system_rhs(pat, k, q) for q, k in enumerate(ks)])
+    ks = [3, 11, 17, 19] if nb == 4 else [1 + (7 * q) % 19 for q in range(nb)]
+    vals = np.stack([system_values(pat, k, q % 4) for q, k in enumerate(ks)])
+    rhs = np.stack([system_rhs(pat, k, q % 4) for q, k in enumerate(ks)])
     LOWER = nat.LAYOUT_SYMMETRIC_LOWER
     devb = DeviceSystem(f, batch=len(ks))
     with torch.cuda.stream(devb.stream):

@@ -1,3 +1,1 @@
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 600 python bench.py 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_scale.py -x -q -m gpu -k "batch_equals" 2>&1 | tail -3
