@@ -220,6 +220,12 @@ int kkt_dev_step(kkt_device *d, const double *values_in, int layout, const doubl
                  double *x_out, int io_on_device, const kkt_krylov_cfg *cfg,
                  kkt_krylov_report *rep, double *diag_out);
 
+/* The second half of kkt_dev_step for factors already refactorized (kkt_dev_refactor):
+ * x0 = solve(r) -> refine_fgmres -> x.  Lets a caller overlap the rhs upload with the
+ * refactorization (pipeline.BatchPipeline).  r/x on host or device. */
+int kkt_dev_step_solve(kkt_device *d, const double *r_in, double *x_out, int io_on_device,
+                       const kkt_krylov_cfg *cfg, kkt_krylov_report *rep);
+
 /* Download the current factor values in the LuFactors layout (_Lx, _Ux, _Udiag). */
 int kkt_dev_download_factors(kkt_device *d, double *Lx, double *Ux, double *Udiag);
 

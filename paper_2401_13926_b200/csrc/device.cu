@@ -1025,6 +1025,15 @@ int kkt_dev_step(kkt_device *d, const double *values_in, int layout, const doubl
   cudaSetDevice(dev->device);
   int rc = kkt::refactor(dev, values_in, layout, io_on_device, diag_out);
   if (rc) return rc;
+  return kkt_dev_step_solve(d, r_in, x_out, io_on_device, cfg, rep);
+}
+
+int kkt_dev_step_solve(kkt_device *d, const double *r_in, double *x_out, int io_on_device,
+                       const kkt_krylov_cfg *cfg, kkt_krylov_report *rep) {
+  Device *dev = reinterpret_cast<Device *>(d);
+  if (!dev || !r_in || !x_out || !cfg || !rep) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
+  cudaSetDevice(dev->device);
+  int rc = KKT_OK;
   kkt::Krylov &K = *dev->kry;
   const bool il = dev->d.nbp > 1;
   const size_t bytes = 8 * (size_t)dev->d.n * dev->d.nb;  // caller layout [nb][n]

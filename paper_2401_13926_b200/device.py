@@ -240,6 +240,23 @@ class DeviceSystem:
             return rep, np.array(list(dg)).reshape(self.nb, 4)
         return rep
 
+    def step_solve(self, r, x_out, on_device: bool, m: int, max_outer: int, delta_tol):
+        """solve -> refine_fgmres for the factors of the last refactor (kkt_dev_step_solve):
+        the second half of ``step``, so the rhs upload can overlap the refactorization."""
+        dsys = None
+        if np.ndim(delta_tol):
+            dsys = (C.c_double * self.nb)(*[float(v) for v in delta_tol])
+            delta_tol = float(np.max(delta_tol))
+        cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(delta_tol),
+                            delta_tol=float(delta_tol), delta_sys=dsys)
+        reps = (nat.KrylovReport * self.nb)()
+        if on_device:
+            args = (_vp(r), _vp(x_out), 1)
+        else:
+            args = (r.ctypes.data_as(C.c_void_p), x_out.ctypes.data_as(C.c_void_p), 0)
+        nat.check(self.lib.kkt_dev_step_solve(self.h, *args, C.byref(cfg), reps), "kkt_dev_step_solve")
+        return reps[0] if self.nb == 1 else list(reps)
+
     def refactor_batch(self, values_t, layout: int) -> np.ndarray:
         """Refactorize all systems from device values [nb][nnz]; returns diagnostics [nb][4]."""
         dg = (C.c_double * (4 * self.nb))()

@@ -3,10 +3,11 @@ the host traffic overlapped (the harness loop of harness._run_direct_family,
 harness.py:217-269, for a batch of independent systems per barrier step).
 
 Each batch (``values [B][nnz]``, ``rhs [B][n]`` in pinned host memory) goes through
-``kkt_dev_step`` (refactor -> lu_solve -> refine_fgmres) on the handle's stream, while a
-copy stream uploads the NEXT batch's inputs and downloads the PREVIOUS batch's solution.
-Device buffers are double-buffered; events order the copies against the step.  Nothing is
-computed on the host.
+``kkt_dev_refactor`` then ``kkt_dev_step_solve`` (lu_solve -> refine_fgmres) on the handle's
+stream, while a copy stream uploads the NEXT batch's inputs and downloads the PREVIOUS
+batch's solution.  Values and rhs have their own events: the refactorization starts once the
+values have landed, the rhs upload overlaps it.  Device buffers are double-buffered; events
+order the copies against the step.  Nothing is computed on the host.
 """
 
 from __future__ import annotations
@@ -45,6 +46,7 @@ class BatchPipeline:
         if not items:
             return []
         reps = []
+        up_vals = [t.cuda.Event(), t.cuda.Event()]
         up_done = [t.cuda.Event(), t.cuda.Event()]
         down_done = [t.cuda.Event(), t.cuda.Event()]
         step_done = [t.cuda.Event(), t.cuda.Event()]
@@ -56,6 +58,7 @@ class BatchPipeline:
             with t.cuda.stream(self.copy):
                 self.copy.wait_event(step_done[i % 2])  # step i-2 has consumed the buffer
                 v.copy_(items[i][0], non_blocking=True)
+                up_vals[i % 2].record(self.copy)
                 r.copy_(items[i][1], non_blocking=True)
                 up_done[i % 2].record(self.copy)
 
@@ -70,14 +73,16 @@ class BatchPipeline:
         upload(0)
         for i in range(len(items)):
             slot = i % 2
+            v, r, x = self._v[slot], self._r[slot], self._x[slot]
+            dev.stream.wait_event(up_vals[slot])
+            dev.refactor_device(v, self.layout)      # async: overlaps this batch's rhs upload
             dev.stream.wait_event(up_done[slot])
             dev.stream.wait_event(down_done[slot])  # x of batch i-2 is on the host
             if i + 1 < len(items):
                 upload(i + 1)
             if i >= 1:
                 download(i - 1)
-            v, r, x = self._v[slot], self._r[slot], self._x[slot]
-            reps.append(dev.step(v, self.layout, r, x, True, self.m, self.max_outer, items[i][3]))
+            reps.append(dev.step_solve(r, x, True, self.m, self.max_outer, items[i][3]))
             step_done[slot].record(dev.stream)
         download(len(items) - 1)
         self.copy.synchronize()

@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_scale.py -x -q -m gpu -k "batch_equals" 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_pipeline.py -x -q -m gpu 2>&1 | tail -15
