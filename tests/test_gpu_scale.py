@@ -79,7 +79,8 @@ def test_full_size_against_oracle(config, k):
     assert rr <= max(1.5 * rr_o, 4 * np.finfo(float).eps), (rr, rr_o)
 
 
-@pytest.mark.parametrize("config,nb", [("activsg200", 4), ("activsg10k", 4), ("activsg2000", 40)])
+@pytest.mark.parametrize("config,nb", [("activsg200", 4), ("activsg10k", 4), ("activsg2000", 40),
+                                       pytest.param("activsg70k", 8, marks=pytest.mark.slow)])
 def test_full_size_batch_equals_single(config, nb):
     """The interleaved batch reproduces each system's single-system factors and solve (nb = 40:
     8-system groups of the TMA wide-column pipeline, every group's done flags and the
@@ -90,6 +91,8 @@ def test_full_size_batch_equals_single(config, nb):
     from paper_2401_13926_b200.device import DeviceSystem
     pat, K0, f = _setup(config)
     ks = [3, 11, 17, 19] if nb == 4 else [1 + (7 * q) % 19 for q in range(nb)]
+    if config == "activsg70k":
+        ks = [min(k, 12) for k in ks]  # the calibrated range at 70k (CONFIGS above)
     vals = np.stack([system_values(pat, k, q % 4) for q, k in enumerate(ks)])
     rhs = np.stack([system_rhs(pat, k, q % 4) for q, k in enumerate(ks)])
     LOWER = nat.LAYOUT_SYMMETRIC_LOWER
