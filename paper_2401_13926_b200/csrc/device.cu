@@ -194,7 +194,21 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
     // the replay runs in two launches split at column J2 (first pattern wider than
     // KKT_B_SPLIT_NP slots): warp tasks before it, 4-warp CTA tasks (k_b_refactor_cta) for the
     // wide separator columns after it
-    const int split_np = std::getenv("KKT_B_SPLIT_NP") ? std::atoi(std::getenv("KKT_B_SPLIT_NP")) : 256;
+    // Default split: 144 slots when the TMA pipeline (ct_mode 3) keeps 3 CTAs per SM for the
+    // widest pattern (its replay beats the warp replay from ~144 slots on: 10k 7.28 -> 6.71 ms,
+    // 2000 3.13 -> 2.73 ms), else 256 (70k: xp 1351, one CTA per SM, 256 is faster).
+    int split_np = 256;
+    {
+      const int mode = std::getenv("KKT_B_CT_MODE") ? std::atoi(std::getenv("KKT_B_CT_MODE")) : 3;
+      const int sc = std::getenv("KKT_B_CT_SC") ? std::atoi(std::getenv("KKT_B_CT_SC")) : 8;
+      int maxnp = 1;
+      for (int j = 0; j < std::min(d.J0, h.n); ++j)
+        maxnp = std::max<int>(maxnp, (int)((h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j])));
+      int ns = 2, stg = 256;
+      b_tma_shape(&ns, &stg);
+      if (mode == 3 && sc == 8 && b_tma_smem(maxnp, ns, stg) <= 74 * 1024) split_np = 144;
+    }
+    if (std::getenv("KKT_B_SPLIT_NP")) split_np = std::atoi(std::getenv("KKT_B_SPLIT_NP"));
     int J2 = std::min(d.J0, h.n);
     for (int j = 0; j < J2; ++j)
       if (split_np > 0 && (h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j]) > split_np) {
