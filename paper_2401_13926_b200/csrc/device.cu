@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -232,10 +233,54 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
     if (d.ct_mode == 3 && (d.ct_sc != 8 || (nbp & 7))) d.ct_mode = 0;  // the TMA pipeline serves 8 systems
     d.tma_direct = std::getenv("KKT_B_TMA_DIRECT") ? std::atoi(std::getenv("KKT_B_TMA_DIRECT")) : 1;
     if (rc2 == KKT_OK) {  // k_b_refactor_cta tasks: (column, ct_sc systems)
-      const int start = h.small_lev_ptr[h.n_small_levels];
-      for (int c = start; c < h.n; ++c) {
-        const int j = h.col_order[c];
-        if (j < J2 || j >= d.J0) continue;
+      // Dispatch order of the wide columns: any topological order is deadlock-free (a task
+      // only waits on columns of earlier tickets).  0 (default): level order.
+      // KKT_B_TAIL_ORDER=1: critical path first — among the columns whose wide dependencies
+      // are all dispatched, the one with the longest remaining chain of update pairs (upward
+      // rank) goes next (measured: 10k 6.74 -> 6.99 ms, 2000 2.77 -> 2.73 ms, 70k equal).
+      const int lo = std::getenv("KKT_B_TAIL_ORDER") ? std::atoi(std::getenv("KKT_B_TAIL_ORDER")) : 0;
+      std::vector<int> order;
+      const int J1 = std::min(d.J0, h.n);
+      const int start = h.small_lev_ptr[h.n_small_levels];  // columns the small kernel runs
+      if (lo == 1 && J2 < J1) {
+        const int m = J1 - J2;
+        std::vector<char> mine(m, 0);
+        for (int c = start; c < h.n; ++c)
+          if (h.col_order[c] >= J2 && h.col_order[c] < J1) mine[h.col_order[c] - J2] = 1;
+        std::vector<std::vector<int>> succ(m);
+        std::vector<int> indeg(m, 0);
+        std::vector<int64_t> cost(m, 0), rank(m, 0);
+        for (int j = J2; j < J1; ++j) {
+          if (!mine[j - J2]) continue;
+          for (int64_t t = h.so_ptr[j]; t < h.so_ptr[j + 1]; ++t) {
+            const int64_t k = h.so_data[t];
+            cost[j - J2] += h.so_meta[4 * t + 1] + 1;
+            if (k >= J2 && k < J1 && mine[k - J2]) {
+              succ[k - J2].push_back(j - J2);
+              ++indeg[j - J2];
+            }
+          }
+        }
+        for (int i = m - 1; i >= 0; --i) {  // deps point to smaller columns
+          int64_t best = 0;
+          for (int q : succ[i]) best = std::max(best, rank[q]);
+          rank[i] = cost[i] + best;
+        }
+        std::priority_queue<std::pair<int64_t, int>> ready;
+        for (int i = 0; i < m; ++i)
+          if (mine[i] && !indeg[i]) ready.push({rank[i], -i});
+        while (!ready.empty()) {
+          const int i = -ready.top().second;
+          ready.pop();
+          order.push_back(J2 + i);
+          for (int q : succ[i])
+            if (--indeg[q] == 0) ready.push({rank[q], -q});
+        }
+      } else {
+        for (int c = start; c < h.n; ++c)
+          if (h.col_order[c] >= J2 && h.col_order[c] < d.J0) order.push_back(h.col_order[c]);
+      }
+      for (const int j : order) {
         d.h_xp = std::max<int>(d.h_xp, (int)((h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j])));
         for (int s0 = 0; s0 < nbp; s0 += d.ct_sc) btask.push_back(make_int2(j, s0 << 8));
       }
