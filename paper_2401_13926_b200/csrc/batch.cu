@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(TS_THREADS, 3)
         if (mine && sw > 0)
           bulk_copy(sts0 + stage * TS_SLOTS + (sincl - sw), d.upd_slot32 + (m.z - mis), (unsigned)sw * 4,
                     &full[stage]);
-        if (direct && lane == 0) {  // wait until the wide column k's L values are published
+        if (direct && lane == 0 && d.tma_direct == 1) {  // wait until the column's flag is up
           const int *f = d.cflag + (size_t)dep * G + g;
           unsigned ns = 32;
           while (ld_acquire_i32(f) == 0) {
@@ -797,7 +797,8 @@ __global__ void __launch_bounds__(TS_THREADS, 3)
           phase ^= 1;
         }
         if (nt0 != t0 && pdep >= 0) pfl = ld_acquire_i32(d.cflag + (size_t)pdep * G + g);
-        else if (nt0 == t0) pfl = lane == 0 ? 1 : fl;  // next piece of step t0 (flag seen): same window
+        else if (nt0 == t0)  // next piece of step t0, same window (flag seen unless read per value)
+          pfl = (lane == 0 && !(direct && d.tma_direct == 2)) ? 1 : fl;
         t0 = nt0;
         e0 = ne0;
       }
@@ -830,7 +831,13 @@ __global__ void __launch_bounds__(TS_THREADS, 3)
               for (int q = 0; q < 4; ++q) {
                 const int idx = idx0 + 32 * q;
                 if (idx < m.y) {
-                  lv[q] = m.z >= 0 ? stv[(m.z + idx) * TS_SC + s] : ld_relaxed_f64(&d.Lx[IL(d, -m.z - 1 + idx, sys)]);
+                  if (m.z >= 0) {
+                    lv[q] = stv[(m.z + idx) * TS_SC + s];
+                  } else {  // unstaged (late) step: straight from L2, each value its own flag
+                    const double *p = &d.Lx[IL(d, -m.z - 1 + idx, sys)];
+                    lv[q] = ld_relaxed_f64(p);
+                    if (is_sentinel(lv[q])) lv[q] = wait_value_bo(p, 32);
+                  }
                   sl[q] = sts[m.w + idx] * TS_SC + s;
                 }
               }
@@ -862,7 +869,7 @@ __global__ void __launch_bounds__(TS_THREADS, 3)
       for (int i = e; i < nl; i += 32) {
         const double v = x[(nu + 1 + i) * TS_SC + s];
         gm = fmax(gm, fabs(v));
-        d.Lx[IL(d, lb + i, sys)] = unsentinel(__ddiv_rn(v, ujj));
+        st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], unsentinel(__ddiv_rn(v, ujj)));
       }
       if (d.poll_ns < 0) __threadfence();  // (diagnostic: per-thread fences)
       consumer_bar();  // every L(:,j) store of the CTA precedes the release below

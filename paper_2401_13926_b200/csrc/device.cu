@@ -231,7 +231,9 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
     if (d.ct_sc != 2 && d.ct_sc != 8) d.ct_sc = 4;
     d.ct_mode = std::getenv("KKT_B_CT_MODE") ? std::atoi(std::getenv("KKT_B_CT_MODE")) : 3;
     if (d.ct_mode == 3 && (d.ct_sc != 8 || (nbp & 7))) d.ct_mode = 0;  // the TMA pipeline serves 8 systems
-    d.tma_direct = std::getenv("KKT_B_TMA_DIRECT") ? std::atoi(std::getenv("KKT_B_TMA_DIRECT")) : 1;
+    // late steps: 0 staged after the flag; 1 read from L2 after the flag; 2 read from L2 with
+    // every value its own readiness flag (no wait on the column flag's release fence)
+    d.tma_direct = std::getenv("KKT_B_TMA_DIRECT") ? std::atoi(std::getenv("KKT_B_TMA_DIRECT")) : 2;
     if (rc2 == KKT_OK) {  // k_b_refactor_cta tasks: (column, ct_sc systems)
       // Dispatch order of the wide columns: any topological order is deadlock-free (a task
       // only waits on columns of earlier tickets).  0 (default): level order.

@@ -63,7 +63,7 @@ struct DevPlan {
   int *so_dep = nullptr;                   // per wide-column step: k - J2 (wide k) or -1
   int *cflag = nullptr;                    // [(j - J2) * nbp / 8 + group]: L(:,j) published
   int tma_ns = 2, tma_stg = 256;           // stages x rows (KKT_B_TMA)
-  int tma_direct = 1;                      // late step read from L2 after the flag (KKT_B_TMA_DIRECT)
+  int tma_direct = 2;                      // late steps: 2 value-as-flag L2 reads (KKT_B_TMA_DIRECT)
   CUtensorMap tmL[3];                      // Lx boxes of 128, 32, 8 rows x 8 systems
   unsigned long long *prof = nullptr;  // optional per-warp cycle counters (KKT_TRACE, batched)
   int rb = RED_BLOCKS;  // reduction blocks per system
