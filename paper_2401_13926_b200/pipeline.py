@@ -25,6 +25,8 @@ class BatchPipeline:
     def __init__(self, dev: DeviceSystem, layout: int, m: int = 10, max_outer: int = 10):
         torch = dev.torch
         self.dev, self.layout, self.m, self.max_outer = dev, layout, m, max_outer
+        import os
+        self.split = os.environ.get("KKT_PIPE_SPLIT", "1") != "0"  # refactor on values arrival
         self.torch = torch
         self.copy = torch.cuda.Stream(device=dev.device)
         self._v = [None, None]
@@ -74,15 +76,19 @@ class BatchPipeline:
         for i in range(len(items)):
             slot = i % 2
             v, r, x = self._v[slot], self._r[slot], self._x[slot]
-            dev.stream.wait_event(up_vals[slot])
-            dev.refactor_device(v, self.layout)      # async: overlaps this batch's rhs upload
+            if self.split:
+                dev.stream.wait_event(up_vals[slot])
+                dev.refactor_device(v, self.layout)      # async: overlaps this batch's rhs upload
             dev.stream.wait_event(up_done[slot])
             dev.stream.wait_event(down_done[slot])  # x of batch i-2 is on the host
             if i + 1 < len(items):
                 upload(i + 1)
             if i >= 1:
                 download(i - 1)
-            reps.append(dev.step_solve(r, x, True, self.m, self.max_outer, items[i][3]))
+            if self.split:
+                reps.append(dev.step_solve(r, x, True, self.m, self.max_outer, items[i][3]))
+            else:
+                reps.append(dev.step(v, self.layout, r, x, True, self.m, self.max_outer, items[i][3]))
             step_done[slot].record(dev.stream)
         download(len(items) - 1)
         self.copy.synchronize()
