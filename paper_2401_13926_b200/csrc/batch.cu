@@ -579,7 +579,8 @@ __global__ void __launch_bounds__(CT_E * CT_SC, CT_E == 64 ? 2 : 3) k_b_refactor
 // ----------------------------------------------------------------------------
 // stages x rows per stage (KKT_B_TMA=ns,rows): 2 x 256 (default), 3 x 160, 4 x 128
 constexpr int TS_SC = 8;                         // systems per task
-constexpr int TS_THREADS = 32 + 32 * TS_SC;      // producer warp + consumers
+constexpr int TS_THREADS = 32 + 32 * TS_SC;      // producer warp + consumers (32 entry lanes)
+__host__ __device__ constexpr int ts_threads(int e) { return 32 + e * TS_SC; }
 __host__ __device__ constexpr int ts_slots(int stg) { return stg + 6 * 32 + 8; }  // + alignment slack
 
 size_t b_tma_smem_ns(int xp, int ns, int stg) {
@@ -643,10 +644,12 @@ __device__ __forceinline__ int ld_acquire_i32(const int *p) {
 __device__ __forceinline__ void st_release_i32(int *p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * TS_SC) : "memory"); }
+template <int E>
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(E * TS_SC) : "memory"); }
 
-template <int TS_NS, int TS_STG>
-__global__ void __launch_bounds__(TS_THREADS, 3)
+// TS_E entry lanes per system: 32 (3 CTAs/SM) or 64 (the 70k-class tail, one CTA per SM)
+template <int TS_NS, int TS_STG, int TS_E>
+__global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
     k_b_refactor_tma(const __grid_constant__ DevPlan d, const int2 *__restrict__ tasks, int ntask) {
   constexpr int TS_SLOTS = ts_slots(TS_STG);
   extern __shared__ __align__(1024) unsigned char tsm[];
@@ -808,11 +811,11 @@ __global__ void __launch_bounds__(TS_THREADS, 3)
       const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
       const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
       const int np = nu + 1 + nl;
-      for (int f = ct; f < np * TS_SC; f += 32 * TS_SC) x[f] = 0.0;
-      consumer_bar();
-      for (int q = d.ap_ptr[j] + e; q < d.ap_ptr[j + 1]; q += 32)
+      for (int f = ct; f < np * TS_SC; f += TS_E * TS_SC) x[f] = 0.0;
+      consumer_bar<TS_E>();
+      for (int q = d.ap_ptr[j] + e; q < d.ap_ptr[j + 1]; q += TS_E)
         x[d.a_slot[q] * TS_SC + s] = d.A_vals[IL(d, d.a_src[q], sys)];
-      consumer_bar();
+      consumer_bar<TS_E>();
       if (t_begin < t_end) {
         while (true) {
           mbar_wait(&full[stage], phase);
@@ -824,12 +827,12 @@ __global__ void __launch_bounds__(TS_THREADS, 3)
           for (int i = 0; i < h.x; ++i) {
             const int4 m = meta[i];  // {slot of k, entries, first staged row, first staged slot}
             const double xk = x[m.x * TS_SC + s];
-            for (int idx0 = e; idx0 < m.y; idx0 += 4 * 32) {
+            for (int idx0 = e; idx0 < m.y; idx0 += 4 * TS_E) {
               double lv[4], xv[4];
               int sl[4];
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                const int idx = idx0 + 32 * q;
+                const int idx = idx0 + TS_E * q;
                 if (idx < m.y) {
                   if (m.z >= 0) {
                     lv[q] = stv[(m.z + idx) * TS_SC + s];
@@ -843,12 +846,12 @@ __global__ void __launch_bounds__(TS_THREADS, 3)
               }
 #pragma unroll
               for (int q = 0; q < 4; ++q)
-                if (idx0 + 32 * q < m.y) xv[q] = x[sl[q]];
+                if (idx0 + TS_E * q < m.y) xv[q] = x[sl[q]];
 #pragma unroll
               for (int q = 0; q < 4; ++q)
-                if (idx0 + 32 * q < m.y) x[sl[q]] = __dsub_rn(xv[q], __dmul_rn(lv[q], xk));
+                if (idx0 + TS_E * q < m.y) x[sl[q]] = __dsub_rn(xv[q], __dmul_rn(lv[q], xk));
             }
-            consumer_bar();  // x[k] of the next step may have been updated in this one
+            consumer_bar<TS_E>();  // x[k] of the next step may have been updated in this one
           }
           if (ct == 0) mbar_arrive(&empty[stage]);
           const bool last = h.y != 0;
@@ -866,19 +869,19 @@ __global__ void __launch_bounds__(TS_THREADS, 3)
       const double eps = patch_floor_b(d, sys);
       const bool patched = fabs(ujj) < eps;
       if (patched) ujj = (ujj >= 0.0) ? eps : -eps;
-      for (int i = e; i < nl; i += 32) {
+      for (int i = e; i < nl; i += TS_E) {
         const double v = x[(nu + 1 + i) * TS_SC + s];
         gm = fmax(gm, fabs(v));
         st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], unsentinel(__ddiv_rn(v, ujj)));
       }
       if (d.poll_ns < 0) __threadfence();  // (diagnostic: per-thread fences)
-      consumer_bar();  // every L(:,j) store of the CTA precedes the release below
+      consumer_bar<TS_E>();  // every L(:,j) store of the CTA precedes the release below
       if (trc && ct == 0) trc[6] = globaltimer();
       if (ct == 0) st_release_i32(&d.cflag[(size_t)(j - d.J2) * G + g], 1);
       if (trc && ct == 0) trc[1] = globaltimer();
-      for (int i = e; i < nl; i += 32)
+      for (int i = e; i < nl; i += TS_E)
         d.Lv[IL(d, d.Lmap[lb + i], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + i) * TS_SC + s], ujj));
-      for (int i = e; i < nu; i += 32) {
+      for (int i = e; i < nu; i += TS_E) {
         const double v = x[i * TS_SC + s];
         d.Ux[IL(d, ub + i, sys)] = v;
         d.Uv[IL(d, d.Umap[ub + i], sys)] = v;
@@ -920,17 +923,18 @@ cudaError_t b_tma_maps(DevPlan &d) {
   return cudaSuccess;
 }
 
-template <int NS, int STG>
+template <int NS, int STG, int E = 32>
 static cudaError_t tma_conf(size_t smem, int *blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_b_refactor_tma<NS, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_b_refactor_tma<NS, STG, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_b_refactor_tma<NS, STG>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    e = cudaFuncSetAttribute(k_b_refactor_tma<NS, STG, E>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_tma<NS, STG>, TS_THREADS, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_tma<NS, STG, E>, ts_threads(E), smem);
   return e;
 }
-cudaError_t b_tma_configure(int ns, int stg, size_t smem, int *blocks_per_sm) {
+cudaError_t b_tma_configure(int ns, int stg, int e, size_t smem, int *blocks_per_sm) {
+  if (e == 64) return tma_conf<2, 256, 64>(smem, blocks_per_sm);
   if (ns == 3 && stg == 256) return tma_conf<3, 256>(smem, blocks_per_sm);
   if (ns == 2 && stg == 384) return tma_conf<2, 384>(smem, blocks_per_sm);
   return ns == 4 ? tma_conf<4, 128>(smem, blocks_per_sm)
@@ -1843,11 +1847,12 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blo
     const int2 *t2 = d.btask + d.n_btask1;
     const int n2 = d.n_btask - d.n_btask1;
     if (d.ct_mode == 3) {
-      if (d.tma_ns == 3 && d.tma_stg == 256) k_b_refactor_tma<3, 256><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
-      else if (d.tma_ns == 2 && d.tma_stg == 384) k_b_refactor_tma<2, 384><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
-      else if (d.tma_ns == 4) k_b_refactor_tma<4, 128><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
-      else if (d.tma_ns == 3) k_b_refactor_tma<3, 160><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
-      else k_b_refactor_tma<2, 256><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      if (d.tma_e == 64) k_b_refactor_tma<2, 256, 64><<<blocks2, ts_threads(64), smem2, st>>>(d, t2, n2);
+      else if (d.tma_ns == 3 && d.tma_stg == 256) k_b_refactor_tma<3, 256, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else if (d.tma_ns == 2 && d.tma_stg == 384) k_b_refactor_tma<2, 384, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else if (d.tma_ns == 4) k_b_refactor_tma<4, 128, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else if (d.tma_ns == 3) k_b_refactor_tma<3, 160, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else k_b_refactor_tma<2, 256, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
     } else if (d.ct_mode == 1) {
       if (d.ct_sc == 2) k_b_refactor_ctaw<2><<<blocks2, 64, smem2, st>>>(d, t2, n2);
       else if (d.ct_sc == 8) k_b_refactor_ctaw<8><<<blocks2, 256, smem2, st>>>(d, t2, n2);

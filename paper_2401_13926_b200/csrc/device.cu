@@ -555,13 +555,24 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
   if (nbp > 1) {
     int rbps = 0, tbps = 0;
     dev->refactor_smem = b_refactor_smem(d.b_xbudget, d.b_stage);
-    if (d.ct_mode == 3) b_tma_shape(&d.tma_ns, &d.tma_stg);
+    if (d.ct_mode == 3) {
+      b_tma_shape(&d.tma_ns, &d.tma_stg);
+      // KKT_B_TMA_E=64: 16 consumer warps per CTA (measured at 70k, one CTA per SM: 96.6 ->
+      // 98.0 ms, so 32 entry lanes stay the default everywhere)
+      d.tma_e = std::getenv("KKT_B_TMA_E") ? std::atoi(std::getenv("KKT_B_TMA_E")) : 32;
+      if (d.tma_e == 64) {
+        d.tma_ns = 2;
+        d.tma_stg = 256;
+      } else {
+        d.tma_e = 32;
+      }
+    }
     const size_t smem2 = d.ct_mode == 3 ? b_tma_smem(std::max(d.h_xp, 1), d.tma_ns, d.tma_stg)
                                         : b_cta_smem(std::max(d.h_xp, 1), d.ct_sc);
     int rbps2 = 0;
     CUDA_TRY(b_configure(nbp, dev->refactor_smem, &rbps, &tbps));
     if (d.ct_mode == 3) {
-      CUDA_TRY(b_tma_configure(d.tma_ns, d.tma_stg, smem2, &rbps2));
+      CUDA_TRY(b_tma_configure(d.tma_ns, d.tma_stg, d.tma_e, smem2, &rbps2));
       CUDA_TRY(b_tma_maps(d));
     } else {
       CUDA_TRY(b_cta_configure(d.ct_sc, smem2, &rbps2, d.ct_mode == 2));

@@ -63,6 +63,7 @@ struct DevPlan {
   int *so_dep = nullptr;                   // per wide-column step: k - J2 (wide k) or -1
   int *cflag = nullptr;                    // [(j - J2) * nbp / 8 + group]: L(:,j) published
   int tma_ns = 2, tma_stg = 256;           // stages x rows (KKT_B_TMA)
+  int tma_e = 32;                          // entry lanes per system (64: one CTA per SM; KKT_B_TMA_E)
   int tma_direct = 2;                      // late steps: 2 value-as-flag L2 reads (KKT_B_TMA_DIRECT)
   CUtensorMap tmL[3];                      // Lx boxes of 128, 32, 8 rows x 8 systems
   unsigned long long *prof = nullptr;  // optional per-warp cycle counters (KKT_TRACE, batched)
@@ -194,7 +195,7 @@ cudaError_t b_refactor_occupancy(size_t smem, int *blocks_per_sm);
 size_t b_cta_smem(int xp, int sc);
 void b_tma_shape(int *ns, int *stg);
 size_t b_tma_smem(int xp, int ns, int stg);
-cudaError_t b_tma_configure(int ns, int stg, size_t smem, int *blocks_per_sm);
+cudaError_t b_tma_configure(int ns, int stg, int e, size_t smem, int *blocks_per_sm);
 cudaError_t b_tma_maps(DevPlan &d);  // encode d.tmL over d.Lx
 cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm, bool wide);
 cudaError_t b_launch_diag_stats(const DevPlan &d, cudaStream_t s);

@@ -25,7 +25,8 @@ pytestmark = pytest.mark.gpu
     ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_DIRECT": "0", "KKT_B_TMA": "4,128"}),
     ("standard_trace", 9, {"KKT_B_SPLIT_NP": "4", "KKT_B_TMA": "3,160"}),
     ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TAIL_ORDER": "1"}),
-    ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_DIRECT": "1"})])
+    ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_DIRECT": "1"}),
+    ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_E": "64"})])
 def test_batch_refactor_solve_bitwise(case, nb, env, monkeypatch):
     """env forces the alternative replay kernels onto small cases: KKT_B_SPLIT_NP (4-warp CTA
     tasks for the wide columns), KKT_B_HEAVY_NP (pull-form CTA per 32 systems)."""
