@@ -204,7 +204,9 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     }
     P.small_lev_ptr.assign(1, 0);
     int32_t l = 0;
-    while (l < P.refactor_levels && l < 2 && cnt[l] >= 2048 && mp[l] <= 64) {
+    int cap = 2;  // KKT_SMALL_LEVELS (<= 8; 4/6/8 measured slower at 10k, batched and single)
+    if (const char *e = std::getenv("KKT_SMALL_LEVELS")) cap = std::max(0, std::min(8, std::atoi(e)));
+    while (l < P.refactor_levels && l < cap && cnt[l] >= 2048 && mp[l] <= 64) {
       P.small_lev_ptr.push_back(P.small_lev_ptr.back() + (int32_t)cnt[l]);
       ++l;
     }
