@@ -363,10 +363,11 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d, const in
     for (int idx = e; idx < nl; idx += E) {
       const double v = x[(nu + 1 + idx) * S + s];
       gm = fmax(gm, fabs(v));
-      st_relaxed_f64(&d.Lx[IL(d, lb + idx, sys)], unsentinel(__ddiv_rn(v, ujj)));
+      const double l = unsentinel(__ddiv_rn(v, ujj));
+      st_relaxed_f64(&d.Lx[IL(d, lb + idx, sys)], l);
+      x[(nu + 1 + idx) * S + s] = l;  // (each lane rereads only its own entries below)
     }
-    for (int idx = e; idx < nl; idx += E)
-      d.Lv[IL(d, d.Lmap[lb + idx], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + idx) * S + s], ujj));
+    for (int idx = e; idx < nl; idx += E) d.Lv[IL(d, d.Lmap[lb + idx], sys)] = x[(nu + 1 + idx) * S + s];
     for (int idx = e; idx < nu; idx += E) {
       const double v = x[idx * S + s];
       d.Ux[IL(d, ub + idx, sys)] = v;
@@ -539,10 +540,11 @@ __global__ void __launch_bounds__(CT_E * CT_SC, CT_E == 64 ? 2 : 3) k_b_refactor
     for (int i = e; i < nl; i += CT_E) {
       const double v = x[(nu + 1 + i) * CT_SC + s];
       gm = fmax(gm, fabs(v));
-      st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], unsentinel(__ddiv_rn(v, ujj)));
+      const double l = unsentinel(__ddiv_rn(v, ujj));
+      st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], l);
+      x[(nu + 1 + i) * CT_SC + s] = l;
     }
-    for (int i = e; i < nl; i += CT_E)
-      d.Lv[IL(d, d.Lmap[lb + i], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + i) * CT_SC + s], ujj));
+    for (int i = e; i < nl; i += CT_E) d.Lv[IL(d, d.Lmap[lb + i], sys)] = x[(nu + 1 + i) * CT_SC + s];
     for (int i = e; i < nu; i += CT_E) {
       const double v = x[i * CT_SC + s];
       d.Ux[IL(d, ub + i, sys)] = v;
@@ -880,6 +882,8 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
       if (ct == 0) st_release_i32(&d.cflag[(size_t)(j - d.J2) * G + g], 1);
       if (trc && ct == 0) trc[1] = globaltimer();
       for (int i = e; i < nl; i += TS_E)
+        // (recomputed rather than parked in x: a shared-memory write-back on the chain's
+        // publish path measured slower)
         d.Lv[IL(d, d.Lmap[lb + i], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + i) * TS_SC + s], ujj));
       for (int i = e; i < nu; i += TS_E) {
         const double v = x[i * TS_SC + s];
@@ -1031,10 +1035,11 @@ __global__ void __launch_bounds__(32 * HW, 1) k_b_refactor_heavy(DevPlan d) {
     for (int i = warp; i < nl; i += HW) {
       const double v = x[(nu + 1 + i) * 32 + lane];
       gm = fmax(gm, fabs(v));
-      st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], unsentinel(__ddiv_rn(v, ujj)));
+      const double l = unsentinel(__ddiv_rn(v, ujj));
+      st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], l);
+      x[(nu + 1 + i) * 32 + lane] = l;
     }
-    for (int i = warp; i < nl; i += HW)
-      d.Lv[IL(d, d.Lmap[lb + i], sys)] = unsentinel(__ddiv_rn(x[(nu + 1 + i) * 32 + lane], ujj));
+    for (int i = warp; i < nl; i += HW) d.Lv[IL(d, d.Lmap[lb + i], sys)] = x[(nu + 1 + i) * 32 + lane];
     for (int i = warp; i < nu; i += HW) {
       const double v = x[i * 32 + lane];
       d.Ux[IL(d, ub + i, sys)] = v;
@@ -1764,10 +1769,11 @@ __global__ void __launch_bounds__(32 * SC) k_b_refactor_ctaw(DevPlan d, const in
     for (int i = lane; i < nl; i += 32) {
       const double v = xw[nu + 1 + i];
       gm = fmax(gm, fabs(v));
-      st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], unsentinel(__ddiv_rn(v, ujj)));
+      const double l = unsentinel(__ddiv_rn(v, ujj));
+      st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], l);
+      xw[nu + 1 + i] = l;
     }
-    for (int i = lane; i < nl; i += 32)
-      d.Lv[IL(d, d.Lmap[lb + i], sys)] = unsentinel(__ddiv_rn(xw[nu + 1 + i], ujj));
+    for (int i = lane; i < nl; i += 32) d.Lv[IL(d, d.Lmap[lb + i], sys)] = xw[nu + 1 + i];
     for (int i = lane; i < nu; i += 32) {
       const double v = xw[i];
       d.Ux[IL(d, ub + i, sys)] = v;

@@ -218,7 +218,9 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
     for (int s = lane; s < nl; s += 32) {
       const double v = x[nu + 1 + s];
       gm = fmax(gm, fabs(v));
-      st_relaxed_f64(&Lx[lb + s], unsentinel(__ddiv_rn(v, ujj)));  // value == readiness
+      const double l = unsentinel(__ddiv_rn(v, ujj));
+      st_relaxed_f64(&Lx[lb + s], l);  // value == readiness
+      x[nu + 1 + s] = l;               // reused by the CSR copy below (same lane)
     }
     // CSR copies for the solves (scatter through the maps: batch the map loads)
     for (int s0 = 0; s0 < nl; s0 += 128) {
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int s = s0 + 32 * q + lane;
-        if (s < nl) Lv[mp[q]] = unsentinel(__ddiv_rn(x[nu + 1 + s], ujj));
+        if (s < nl) Lv[mp[q]] = x[nu + 1 + s];
       }
     }
     for (int s0 = 0; s0 < nu; s0 += 128) {
