@@ -388,14 +388,16 @@ def main():
     kd = kern[dom]
     # DRAM traffic of the dominant kernel family from the committed ncu --set full capture
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r1i_ncu_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r1j_ncu_traffic.json")
     if os.path.exists(tp):
         tk = json.load(open(tp))["kernels"]
-        fam = {"refactor": ["k_b_refactor", "k_b_refactor_tma<2, 256>"], "spmv": ["k_b_spmv"],
+        fam = {"refactor": ["k_b_refactor", "k_b_refactor_tma<"], "spmv": ["k_b_spmv"],
                "trisolve_pair": ["k_b_trsv_grid<0>", "k_b_trsv_grid<1>", "k_trsv_blocked<0, 1, 1>",
                                  "k_trsv_blocked<1, 1, 1>"]}[dom]
-        if all(k in tk for k in fam):
-            traffic = sum(tk[k]["dram_read_bytes"] + tk[k]["dram_write_bytes"] for k in fam)
+        # a family member ending in "<" matches any instantiation of that template
+        hit = [[k for k in tk if (k.startswith(f) if f.endswith("<") else k == f)] for f in fam]
+        if all(len(h) == 1 for h in hit):
+            traffic = sum(tk[h[0]]["dram_read_bytes"] + tk[h[0]]["dram_write_bytes"] for h in hit)
 
     # ---- single-system latency (B = 1 handle, sequence systems in order) ----
     single = None

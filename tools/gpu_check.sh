@@ -1,1 +1,1 @@
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+timeout 900 python bench.py > gpurun_out/r1j_bench.log 2>&1; echo bench=$?
