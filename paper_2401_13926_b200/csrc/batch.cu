@@ -581,6 +581,10 @@ __global__ void __launch_bounds__(CT_E * CT_SC, CT_E == 64 ? 2 : 3) k_b_refactor
 // ----------------------------------------------------------------------------
 // stages x rows per stage (KKT_B_TMA=ns,rows): 2 x 256 (default), 3 x 160, 4 x 128
 constexpr int TS_SC = 8;                         // systems per task
+// entries per consumer thread in flight per step: 1 (measured at 10k: 1 6.19 ms, 2 6.25,
+// 3 6.38, 4 6.56, 8 spills 9.7; the step's other entries come from the other 7 warps and
+// the co-resident CTAs)
+constexpr int TS_U = 1;
 constexpr int TS_THREADS = 32 + 32 * TS_SC;      // producer warp + consumers (32 entry lanes)
 __host__ __device__ constexpr int ts_threads(int e) { return 32 + e * TS_SC; }
 __host__ __device__ constexpr int ts_slots(int stg) { return stg + 6 * 32 + 8; }  // + alignment slack
@@ -829,11 +833,11 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
           for (int i = 0; i < h.x; ++i) {
             const int4 m = meta[i];  // {slot of k, entries, first staged row, first staged slot}
             const double xk = x[m.x * TS_SC + s];
-            for (int idx0 = e; idx0 < m.y; idx0 += 4 * TS_E) {
-              double lv[4], xv[4];
-              int sl[4];
+            for (int idx0 = e; idx0 < m.y; idx0 += TS_U * TS_E) {
+              double lv[TS_U], xv[TS_U];
+              int sl[TS_U];
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
+              for (int q = 0; q < TS_U; ++q) {
                 const int idx = idx0 + TS_E * q;
                 if (idx < m.y) {
                   if (m.z >= 0) {
@@ -847,10 +851,10 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
                 }
               }
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
+              for (int q = 0; q < TS_U; ++q)
                 if (idx0 + TS_E * q < m.y) xv[q] = x[sl[q]];
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
+              for (int q = 0; q < TS_U; ++q)
                 if (idx0 + TS_E * q < m.y) x[sl[q]] = __dsub_rn(xv[q], __dmul_rn(lv[q], xk));
             }
             consumer_bar<TS_E>();  // x[k] of the next step may have been updated in this one
