@@ -145,6 +145,9 @@ __global__ void __launch_bounds__(256) k_b_refactor_small(DevPlan d, int begin, 
 // Lane = (entry e < E, system s < S), E * S = 32.  Workspace x[np][S] and the staged update
 // pairs live in shared memory.
 // ----------------------------------------------------------------------------
+// entries per lane in flight per replay step (10k: 1 5.96 ms, 2 6.17, 4 6.18)
+constexpr int B_U = 1;
+
 size_t b_refactor_smem(int xbudget, int stage) {
   return (size_t)B_WARPS * (xbudget + 3 * stage) * sizeof(double);
 }
@@ -322,12 +325,12 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d, const in
         const int off = __shfl_sync(FULL, cur.incl - cur.m.y, i);
         const int lbk = __shfl_sync(FULL, cur.m.w, i);  // L(:,k) = Lx[lbk, lbk+cnt)
         const double xk = x[kslot * S + s];
-        // the targets of one step are distinct slots: 4 RMWs per lane in flight
-        for (int idx0 = e; idx0 < cnt; idx0 += 4 * E) {
-          double lv[4], xv[4];
-          int sl[4];
+        // the targets of one step are distinct slots (B_U RMWs per lane in flight)
+        for (int idx0 = e; idx0 < cnt; idx0 += B_U * E) {
+          double lv[B_U], xv[B_U];
+          int sl[B_U];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < B_U; ++q) {
             const int idx = idx0 + q * E;
             if (idx < cnt) {
               lv[q] = stv[((off + idx) << lgS) + s];
@@ -335,10 +338,10 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d, const in
             }
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < B_U; ++q)
             if (idx0 + q * E < cnt) xv[q] = x[sl[q]];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < B_U; ++q) {
             const int idx = idx0 + q * E;
             if (idx < cnt) {
               double l = lv[q];  // staged before L(:,k) was published?  wait for it
