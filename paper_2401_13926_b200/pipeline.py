@@ -4,8 +4,8 @@ harness.py:217-269, for a batch of independent systems per barrier step).
 
 Each batch (``values [B][nnz]``, ``rhs [B][n]`` in pinned host memory) goes through
 ``kkt_dev_refactor`` then ``kkt_dev_step_solve`` (lu_solve -> refine_fgmres) on the handle's
-stream, while a copy stream uploads the NEXT batch's inputs and downloads the PREVIOUS
-batch's solution.  Values and rhs have their own events: the refactorization starts once the
+stream, while one copy stream uploads the NEXT batch's inputs and another downloads the
+PREVIOUS batch's solution (both PCIe directions at once).  Values and rhs have their own events: the refactorization starts once the
 values have landed, the rhs upload overlaps it.  Device buffers are double-buffered; events
 order the copies against the step.  Nothing is computed on the host.
 """
@@ -28,7 +28,8 @@ class BatchPipeline:
         import os
         self.split = os.environ.get("KKT_PIPE_SPLIT", "1") != "0"  # refactor on values arrival
         self.torch = torch
-        self.copy = torch.cuda.Stream(device=dev.device)
+        self.copy = torch.cuda.Stream(device=dev.device)   # host -> device
+        self.copy_out = torch.cuda.Stream(device=dev.device)  # device -> host (PCIe is duplex)
         self._v = [None, None]
         self._r = [None, None]
         self._x = [None, None]
@@ -53,7 +54,7 @@ class BatchPipeline:
         down_done = [t.cuda.Event(), t.cuda.Event()]
         step_done = [t.cuda.Event(), t.cuda.Event()]
         for e in down_done:
-            e.record(self.copy)
+            e.record(self.copy_out)
 
         def upload(i):
             v, r, _ = self._bufs(i % 2, items[i][0], items[i][1])
@@ -65,10 +66,10 @@ class BatchPipeline:
                 up_done[i % 2].record(self.copy)
 
         def download(i):
-            with t.cuda.stream(self.copy):
-                self.copy.wait_event(step_done[i % 2])
+            with t.cuda.stream(self.copy_out):
+                self.copy_out.wait_event(step_done[i % 2])
                 items[i][2].copy_(self._x[i % 2], non_blocking=True)
-                down_done[i % 2].record(self.copy)
+                down_done[i % 2].record(self.copy_out)
 
         for e in step_done:
             e.record(dev.stream)
@@ -92,6 +93,7 @@ class BatchPipeline:
             step_done[slot].record(dev.stream)
         download(len(items) - 1)
         self.copy.synchronize()
+        self.copy_out.synchronize()
         return reps
 
 

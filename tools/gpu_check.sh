@@ -1,2 +1,2 @@
-echo "B1 $(timeout 120 python tools/probe_kernels.py activsg10k 1 5 2>&1 | tail -1 | cut -c1-110)"
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+timeout 600 python -m pytest tests/test_gpu_pipeline.py -x -q -m gpu 2>&1 | tail -1
+for r in 1 2; do echo "$(timeout 600 python bench.py --no-single --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'])")"; done
