@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_pipeline.py -x -q -m gpu 2>&1 | tail -1
-for r in 1 2; do echo "$(timeout 600 python bench.py --no-single --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'])")"; done
+timeout 900 python bench.py > gpurun_out/r1k_bench2.log 2>&1; echo bench=$?
+timeout 900 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
