@@ -388,7 +388,7 @@ def main():
     kd = kern[dom]
     # DRAM traffic of the dominant kernel family from the committed ncu --set full capture
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r1k_ncu_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r1l_ncu_traffic.json")
     if os.path.exists(tp):
         tk = json.load(open(tp))["kernels"]
         fam = {"refactor": ["k_b_refactor", "k_b_refactor_tma<"], "spmv": ["k_b_spmv"],
