@@ -1,2 +1,2 @@
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-for r in 1 2; do timeout 600 python bench.py --no-single --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['kernels']['spmv']['ms'])"; done
+for v in 1 2 4; do echo "S=$v $(KKT_SWEEP_S=$v timeout 120 python tools/probe_kernels.py activsg10k 64 5 2>&1 | tail -1 | cut -c1-110)"; done
+echo "nostage $(KKT_SWEEP_NOSTAGE=1 timeout 120 python tools/probe_kernels.py activsg10k 64 5 2>&1 | tail -1 | cut -c1-110)"
