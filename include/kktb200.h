@@ -20,6 +20,8 @@
  *   kkt_dev_spmv           <- sparsecore.spmv(K, x)                      sparsecore.py:284
  *   kkt_dev_residual_norms <- refine.nsr / nrbe / needs_refinement       refine.py:62-92
  *   kkt_dev_fgmres         <- krylov.fgmres(K, M=lu_solve, b, x0, cfg)   krylov.py:117
+ *   kkt_dev_fgmres_ops     <- krylov.fgmres(K, M, b, x0, cfg) for any LinearOperator pair
+ *                             (matrix / identity / LU / host callback)   krylov.py:36-54,117
  *   kkt_dev_refine_fgmres  <- refine.refine_fgmres(K, f, x0, r, cfg)     refine.py:103
  *   kkt_dev_residual       <- rho = r - spmv(K, x); ||rho||_2            refine.py:158,167-168
  *   kkt_dev_axpy           <- x += d  (Richardson update)                refine.py:166
@@ -47,7 +49,8 @@ enum {
   KKT_ERR_NONFINITE = 4,        /* OperatorOutputError        krylov.py:28     */
   KKT_ERR_CUDA = 5,             /* CUDA runtime failure                        */
   KKT_ERR_OOM = 6,              /* allocation failure                          */
-  KKT_ERR_BAD_ARG = 7           /* ValueError (config validation)              */
+  KKT_ERR_BAD_ARG = 7,          /* ValueError (config validation)              */
+  KKT_ERR_CALLBACK = 8          /* a host operator callback reported failure   */
 };
 
 const char *kkt_last_error(void);
@@ -110,7 +113,7 @@ typedef struct {
   int device;             /* CUDA ordinal                                  */
   int batch;              /* number of same-pattern systems held (>=1)     */
   int restart_m;          /* FGMRES restart length the workspace is sized for */
-  int trisolve_mode;      /* 0 = ordered (bitwise with lu_solve), 1 = fast */
+  int reserved;           /* 0 (the solves are always bitwise with lu_solve) */
   int flags;              /* reserved, 0                                   */
 } kkt_device_opts;
 
@@ -188,7 +191,17 @@ typedef struct {
   double delta_tol;       /* refinement trigger (refine only; refine.py:35) */
   const double *delta_sys; /* optional per-system delta_tol (and tol) [batch], or NULL:
                               each system of a batch may carry its own barrier parameter */
+  int flags;              /* KKT_FG_* below                                  */
 } kkt_krylov_cfg;
+
+enum {
+  KKT_FG_STATS_AFTER = 1, /* refine: also compute the residual statistics of the result   */
+  KKT_FG_HOST_LOOP = 2,   /* drive the restart/iteration control from the host (reads the
+                             device control words per iteration) instead of one CUDA graph
+                             with conditional nodes; same kernels, same results          */
+  KKT_FG_MGS = 4          /* modified Gram-Schmidt (KrylovConfig.ortho = "mgs") instead of
+                             CGS2                                                        */
+};
 
 typedef struct {
   int iterations;         /* KrylovResult.iterations          */
@@ -199,7 +212,11 @@ typedef struct {
   double est_final;       /* est_residual_history[-1]          */
   double true_final;      /* KrylovResult.true_final_residual  */
   int triggered;          /* refine only                       */
-  int nonfinite;          /* a NaN/Inf was produced            */
+  int nonfinite;          /* a NaN/Inf was produced: this system failed (OperatorOutputError) */
+  double stats_before[6]; /* refine: {||r-Kx0||_2, ||r-Kx0||_inf, ||x0||_2, ||x0||_inf,
+                             ||r||_2, ||K||_inf}  (nsr_before, refine.py:117)         */
+  double stats_after[6];  /* refine + KKT_FG_STATS_AFTER: the same for the returned x
+                             (nsr_after / nrbe_final, refine.py:129-131)             */
 } kkt_krylov_report;
 
 /* FGMRES(m) with CGS2, K = operator values, M = lu_solve with the current factors
@@ -208,6 +225,30 @@ typedef struct {
 int kkt_dev_fgmres(kkt_device *d, const double *b_dev, const double *x0_dev, double *x_dev,
                    const kkt_krylov_cfg *cfg, kkt_krylov_report *rep,
                    double *history_host, int hist_cap);
+
+/* Operators of the generic FGMRES (krylov.LinearOperator, krylov.py:36-54).
+ * KKT_OP_HANDLE: K = the handle's operator values (spmv), M = its LU factors (lu_solve);
+ * KKT_OP_IDENTITY: v -> v (LinearOperator.identity); KKT_OP_MATRIX: a kkt_operator's spmv;
+ * KKT_OP_CALLBACK: apply(user, in_host, out_host) — host code (the reference's numpy
+ * callback) that reads n doubles from in_host and writes n doubles to out_host (library-owned
+ * pinned buffers) and returns 0.  Non-HANDLE kinds need batch == 1. */
+typedef int (*kkt_apply_fn)(void *user, const double *in_host, double *out_host);
+enum { KKT_OP_HANDLE = 0, KKT_OP_IDENTITY = 1, KKT_OP_MATRIX = 2, KKT_OP_CALLBACK = 3 };
+typedef struct kkt_operator kkt_operator;
+typedef struct {
+  int kind;
+  kkt_operator *matrix;   /* KKT_OP_MATRIX */
+  kkt_apply_fn apply;     /* KKT_OP_CALLBACK */
+  void *user;
+} kkt_linop;
+
+/* fgmres(K, M, b, x0, cfg) (krylov.py:117-208) with any operator pair.  Device vectors.
+ * history_host[hist_cap] (may be NULL): est_residual_history; restart_pairs_host
+ * [pairs_cap][2] (may be NULL): KrylovResult.restart_residuals (krylov.py:193). */
+int kkt_dev_fgmres_ops(kkt_device *d, const kkt_linop *K, const kkt_linop *M, const double *b_dev,
+                       const double *x0_dev, double *x_dev, const kkt_krylov_cfg *cfg,
+                       kkt_krylov_report *rep, double *history_host, int hist_cap,
+                       double *restart_pairs_host, int pairs_cap);
 
 /* refine_fgmres (refine.py:103-132): trigger on ||r-Kx0||_2 > delta*||r||_2, then
  * FGMRES with tol = delta_tol.  Device pointers. */
@@ -234,7 +275,6 @@ int kkt_dev_download_factors(kkt_device *d, double *Lx, double *Ux, double *Udia
  * row_ptr/col_idx: CSR as stored (symmetric_lower != 0 => lower triangle incl. diagonal,
  * applied with both halves exactly like sparsecore.py:296-302).
  * ====================================================================== */
-typedef struct kkt_operator kkt_operator;
 int kkt_op_create(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
                   int symmetric_lower, int device, kkt_operator **out);
 void kkt_op_destroy(kkt_operator *op);

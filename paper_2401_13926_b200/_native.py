@@ -13,7 +13,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkktb200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 KKT_OK = 0
 KKT_ERR_SINGULAR = 1
@@ -23,6 +23,11 @@ KKT_ERR_NONFINITE = 4
 KKT_ERR_CUDA = 5
 KKT_ERR_OOM = 6
 KKT_ERR_BAD_ARG = 7
+KKT_ERR_CALLBACK = 8
+FG_STATS_AFTER = 1
+FG_HOST_LOOP = 2
+FG_MGS = 4
+OP_HANDLE, OP_IDENTITY, OP_MATRIX, OP_CALLBACK = 0, 1, 2, 3
 LAYOUT_GENERAL = 0
 LAYOUT_SYMMETRIC_LOWER = 1
 
@@ -34,19 +39,29 @@ vp = C.c_void_p
 
 class DeviceOpts(C.Structure):
     _fields_ = [("device", C.c_int), ("batch", C.c_int), ("restart_m", C.c_int),
-                ("trisolve_mode", C.c_int), ("flags", C.c_int)]
+                ("reserved", C.c_int), ("flags", C.c_int)]
 
 
 class KrylovCfg(C.Structure):
     _fields_ = [("m", C.c_int), ("max_outer", C.c_int), ("tol", C.c_double),
-                ("delta_tol", C.c_double), ("delta_sys", C.POINTER(C.c_double))]
+                ("delta_tol", C.c_double), ("delta_sys", C.POINTER(C.c_double)),
+                ("flags", C.c_int)]
 
 
 class KrylovReport(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int),
                 ("precond_applications", C.c_int), ("restarts", C.c_int),
                 ("beta0", C.c_double), ("est_final", C.c_double),
-                ("true_final", C.c_double), ("triggered", C.c_int), ("nonfinite", C.c_int)]
+                ("true_final", C.c_double), ("triggered", C.c_int), ("nonfinite", C.c_int),
+                ("stats_before", C.c_double * 6), ("stats_after", C.c_double * 6)]
+
+
+APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class LinOp(C.Structure):
+    _fields_ = [("kind", C.c_int), ("matrix", C.c_void_p), ("apply", APPLY_FN),
+                ("user", C.c_void_p)]
 
 
 # (name, restype, argtypes) — every symbol include/kktb200.h declares.
@@ -79,6 +94,9 @@ SIGNATURES = [
     ("kkt_mm_read_array", C.c_int, [C.c_char_p, i64, f64p]),
     ("kkt_dev_fgmres", C.c_int, [vp, vp, vp, vp, C.POINTER(KrylovCfg), C.POINTER(KrylovReport),
                                  f64p, C.c_int]),
+    ("kkt_dev_fgmres_ops", C.c_int, [vp, C.POINTER(LinOp), C.POINTER(LinOp), vp, vp, vp,
+                                     C.POINTER(KrylovCfg), C.POINTER(KrylovReport), f64p, C.c_int,
+                                     f64p, C.c_int]),
     ("kkt_dev_refine_fgmres", C.c_int, [vp, vp, vp, vp, C.POINTER(KrylovCfg),
                                         C.POINTER(KrylovReport)]),
     ("kkt_dev_step", C.c_int, [vp, vp, C.c_int, vp, vp, C.c_int, C.POINTER(KrylovCfg),
@@ -150,6 +168,8 @@ def check(rc: int, what: str = "") -> None:
         raise ValueError(msg)
     if rc == KKT_ERR_NONFINITE:
         raise OperatorOutputError(msg)
+    if rc == KKT_ERR_CALLBACK:
+        raise RuntimeError(f"operator callback failed: {msg}")
     if rc == KKT_ERR_OOM:
         raise MemoryError(msg)
     raise RuntimeError(f"kktb200 CUDA error: {msg}")

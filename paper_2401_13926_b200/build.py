@@ -8,6 +8,7 @@ need numpy's two-rounding ``x - (l*xr)``); the kernels by nvcc for sm_100a only.
 
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import shutil
 import subprocess
@@ -31,6 +32,13 @@ def _nvcc() -> str:
         if cand and os.path.exists(cand):
             return cand
     raise RuntimeError("nvcc not found: cannot build the sm_100a kernels")
+
+
+def _run_capture(cmd) -> str:
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"build step failed: {' '.join(cmd)}\n{proc.stdout}\n{proc.stderr}")
+    return "$ " + " ".join(cmd) + "\n" + proc.stdout + proc.stderr
 
 
 def _run(cmd, log):
@@ -60,17 +68,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = _nvcc()
     objs = []
     log_path = os.path.join(BUILD, "build.log")
+    jobs = []
+    for f in sorted(os.listdir(CSRC)):
+        src = os.path.join(CSRC, f)
+        obj = os.path.join(BUILD, f + ".o")
+        if f.endswith(".cpp"):
+            jobs.append(["g++", *HOST_FLAGS, "-I", INCLUDE, "-c", src, "-o", obj])
+        elif f.endswith(".cu"):
+            jobs.append([nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-c", src, "-o", obj])
+        else:
+            continue
+        objs.append(obj)
     with open(log_path, "w") as log:
-        for f in sorted(os.listdir(CSRC)):
-            src = os.path.join(CSRC, f)
-            obj = os.path.join(BUILD, f + ".o")
-            if f.endswith(".cpp"):
-                _run(["g++", *HOST_FLAGS, "-I", INCLUDE, "-c", src, "-o", obj], log)
-            elif f.endswith(".cu"):
-                _run([nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-c", src, "-o", obj], log)
-            else:
-                continue
-            objs.append(obj)
+        # translation units compile independently: one process each
+        with concurrent.futures.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+            logs = list(ex.map(lambda cmd: _run_capture(cmd), jobs))
+        for text in logs:
+            log.write(text)
         tmp = LIB + ".tmp"
         _run([nvcc, "-shared", *NVCC_ARCH, "-o", tmp, *objs, "-cudart=static"], log)
         os.replace(tmp, LIB)

@@ -600,7 +600,8 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
     if (d.trace_step) d.prof = d.trace_step;  // per-warp cycle counters
     dev->refactor_blocks = std::max(1, rbps) * dev->sm_count;
     dev->trsv_blocks = std::max(1, tbps) * dev->sm_count;
-    dev->pinned_bytes = 64 * 1024 + 64 * (size_t)nbp;
+    // residual statistics + scalar blocks of every system (dev_residual_norms, refactor diag)
+    dev->pinned_bytes = std::max<size_t>(64 * 1024, 8 * (5 + SCAL_STRIDE) * (size_t)nbp + 4096);
     CUDA_TRY(cudaMallocHost(&dev->pinned, dev->pinned_bytes));
     rc = alloc_krylov(dev, dev->restart_m);
     if (rc != KKT_OK) return rc;
@@ -711,6 +712,8 @@ int dev_spmv(Device *dev, const double *x, double *y, const double *bsub, double
 int dev_residual_norms(Device *dev, const double *r, const double *x, double *out6) {
   DevPlan &d = dev->d;
   const size_t nb = (size_t)d.nb;
+  if (8 * (5 + SCAL_STRIDE) * nb > dev->pinned_bytes)
+    return set_error(KKT_ERR_BAD_ARG, "residual statistics exceed the pinned staging buffer");
   double *out5 = d.partials + 5 * (size_t)d.rb * d.nbp;  // after the [nbp][5][rb] partials
   LAUNCH(d.nbp > 1 ? b_launch_resid_stats(d, r, x, d.partials, out5, dev->stream)
                    : launch_resid_stats(d, r, x, d.partials, out5, dev->stream));
@@ -727,17 +730,8 @@ int dev_residual_norms(Device *dev, const double *r, const double *x, double *ou
 }
 
 // ---------------------------------------------------------------------------
-// Standalone operator handle: only the operator part of DevPlan is populated.
+// Standalone operator handle (struct Operator, host_util.h)
 // ---------------------------------------------------------------------------
-struct Operator {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  DevPlan d{};
-  void *arena = nullptr;
-  double *pinned = nullptr;
-  long long launches = 0;
-};
-
 static int op_create(int64_t n, const int64_t *rp, const int64_t *ci, int sym, int device,
                      Operator *&out) {
   out = nullptr;
@@ -1015,59 +1009,52 @@ int kkt_dev_residual_norms(kkt_device *d, const double *r_dev, const double *x_d
 
 int kkt_dev_fgmres(kkt_device *d, const double *b_dev, const double *x0_dev, double *x_dev,
                    const kkt_krylov_cfg *cfg, kkt_krylov_report *rep, double *history_host, int hist_cap) {
+  return kkt_dev_fgmres_ops(d, nullptr, nullptr, b_dev, x0_dev, x_dev, cfg, rep, history_host, hist_cap,
+                            nullptr, 0);
+}
+
+int kkt_dev_fgmres_ops(kkt_device *d, const kkt_linop *K, const kkt_linop *M, const double *b_dev,
+                       const double *x0_dev, double *x_dev, const kkt_krylov_cfg *cfg,
+                       kkt_krylov_report *rep, double *history_host, int hist_cap,
+                       double *restart_pairs_host, int pairs_cap) {
   Device *dev = reinterpret_cast<Device *>(d);
   if (!dev || !b_dev || !x0_dev || !x_dev || !cfg || !rep)
     return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
-  cudaSetDevice(dev->device);
-  if (dev->d.nbp > 1) {
-    kkt::Krylov &K = *dev->kry;
-    IL_IN(b_dev, K.sr);
-    IL_IN(x0_dev, K.sx0);
-    int rc = kkt::dev_fgmres(dev, K.sr, K.sx0, K.sx, cfg, rep, history_host, hist_cap, nullptr);
-    if (rc) return rc;
-    IL_OUT(K.sx, x_dev);
-    return KKT_OK;
+  for (const kkt_linop *op : {K, M}) {
+    if (!op) continue;
+    if (op->kind < KKT_OP_HANDLE || op->kind > KKT_OP_CALLBACK)
+      return kkt::set_error(KKT_ERR_BAD_ARG, "unknown operator kind");
+    if (op->kind == KKT_OP_MATRIX &&
+        (!op->matrix || reinterpret_cast<kkt::Operator *>(op->matrix)->d.n != dev->d.n))
+      return kkt::set_error(KKT_ERR_BAD_ARG, "matrix operator missing or of the wrong dimension");
+    if (op->kind == KKT_OP_CALLBACK && !op->apply) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL callback");
   }
-  return kkt::dev_fgmres(dev, b_dev, x0_dev, x_dev, cfg, rep, history_host, hist_cap, nullptr);
+  cudaSetDevice(dev->device);
+  int rc = kkt::ensure_krylov(dev, cfg->m);  // before staging into the workspace
+  if (rc) return rc;
+  if (dev->d.nbp > 1) {
+    kkt::Krylov &Kr = *dev->kry;
+    IL_IN(b_dev, Kr.sr);
+    IL_IN(x0_dev, Kr.sx0);
+    rc = kkt::dev_fgmres(dev, Kr.sr, Kr.sx0, Kr.sx, cfg, 0, nullptr, K, M, rep, history_host, hist_cap,
+                         restart_pairs_host, pairs_cap);
+    if (rc && rc != KKT_ERR_NONFINITE) return rc;
+    IL_OUT(Kr.sx, x_dev);
+    return rc;
+  }
+  return kkt::dev_fgmres(dev, b_dev, x0_dev, x_dev, cfg, 0, nullptr, K, M, rep, history_host, hist_cap,
+                         restart_pairs_host, pairs_cap);
 }
 
-// refine_fgmres for every system of the handle (refine.py:103-132): per-system trigger
-// ||r - K x0||_2 > delta ||r||_2; untriggered systems return x0; the triggered ones run
-// FGMRES(tol = delta) together.
-// (vectors in the handle's native layout)
+// refine_fgmres for every system of the handle (refine.py:103-132): the per-system trigger
+// ||r - K x0||_2 > delta ||r||_2, FGMRES(tol = delta) on the triggered systems and x0 for the
+// others, all decided on the device (one graph, one host sync).  Vectors in the handle's
+// native layout.
 static int refine_native(Device *dev, const double *r_dev, const double *x0_dev, double *x_dev,
                          const kkt_krylov_cfg *cfg, kkt_krylov_report *rep) {
-  if (!(cfg->delta_tol > 0)) return kkt::set_error(KKT_ERR_BAD_ARG, "delta_tol must be positive");
-  const int nb = dev->d.nb;
-  std::vector<double> st(6 * (size_t)nb);
-  int rc = kkt::dev_residual_norms(dev, r_dev, x0_dev, st.data());
-  if (rc) return rc;
-  std::vector<int> trig(nb, 0);
-  int any = 0;
-  for (int q = 0; q < nb; ++q) {
-    const double dq = cfg->delta_sys ? cfg->delta_sys[q] : cfg->delta_tol;
-    if (!(dq > 0)) return kkt::set_error(KKT_ERR_BAD_ARG, "delta_tol must be positive");
-    trig[q] = st[6 * q] > dq * st[6 * q + 4] ? 1 : 0;
-    any |= trig[q];
-  }
-  if (!any) {
-    for (int q = 0; q < nb; ++q) {
-      std::memset(&rep[q], 0, sizeof rep[q]);
-      rep[q].converged = 1;
-    }
-    cudaError_t e = cudaMemcpyAsync(x_dev, x0_dev, 8 * (size_t)dev->d.n * dev->d.nbp,
-                                    cudaMemcpyDeviceToDevice, dev->stream);
-    if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
-    return KKT_OK;
-  }
-  kkt_krylov_cfg c = *cfg;
-  c.tol = cfg->delta_tol;
-  rc = kkt::dev_fgmres(dev, r_dev, x0_dev, x_dev, &c, rep, nullptr, 0, trig.data());
-  for (int q = 0; q < nb; ++q) {
-    rep[q].triggered = trig[q];
-    if (!trig[q]) rep[q].converged = 1;
-  }
-  return rc;
+  if (!(cfg->delta_tol > 0) && !cfg->delta_sys) return kkt::set_error(KKT_ERR_BAD_ARG, "delta_tol must be positive");
+  return kkt::dev_fgmres(dev, r_dev, x0_dev, x_dev, cfg, 1, nullptr, nullptr, nullptr, rep, nullptr, 0,
+                         nullptr, 0);
 }
 
 int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_dev, double *x_dev,
@@ -1076,14 +1063,16 @@ int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_d
   if (!dev || !r_dev || !x0_dev || !x_dev || !cfg || !rep)
     return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
   cudaSetDevice(dev->device);
+  int rc = kkt::ensure_krylov(dev, cfg->m);
+  if (rc) return rc;
   if (dev->d.nbp > 1) {
     kkt::Krylov &K = *dev->kry;
     IL_IN(r_dev, K.sr);
     IL_IN(x0_dev, K.sx0);
-    int rc = refine_native(dev, K.sr, K.sx0, K.sx, cfg, rep);
-    if (rc) return rc;
+    rc = refine_native(dev, K.sr, K.sx0, K.sx, cfg, rep);
+    if (rc && rc != KKT_ERR_NONFINITE) return rc;
     IL_OUT(K.sx, x_dev);
-    return KKT_OK;
+    return rc;
   }
   return refine_native(dev, r_dev, x0_dev, x_dev, cfg, rep);
 }
@@ -1105,7 +1094,8 @@ int kkt_dev_step_solve(kkt_device *d, const double *r_in, double *x_out, int io_
   Device *dev = reinterpret_cast<Device *>(d);
   if (!dev || !r_in || !x_out || !cfg || !rep) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
   cudaSetDevice(dev->device);
-  int rc = KKT_OK;
+  int rc = kkt::ensure_krylov(dev, cfg->m);  // before staging into the workspace
+  if (rc) return rc;
   kkt::Krylov &K = *dev->kry;
   const bool il = dev->d.nbp > 1;
   const size_t bytes = 8 * (size_t)dev->d.n * dev->d.nb;  // caller layout [nb][n]
@@ -1124,7 +1114,8 @@ int kkt_dev_step_solve(kkt_device *d, const double *r_in, double *x_out, int io_
   rc = kkt::dev_solve(dev, r_dev, K.sx0);  // x0 = lu_solve(r)      (harness.py:234)
   if (rc) return rc;
   rc = refine_native(dev, r_dev, K.sx0, K.sx, cfg, rep);  // (harness.py:240)
-  if (rc) return rc;
+  if (rc && rc != KKT_ERR_NONFINITE) return rc;
+  const int rc_refine = rc;  // per-system failures still return every x
   const double *xs = K.sx;
   if (il) {
     double *dst = io_on_device ? x_out : K.w;
@@ -1137,7 +1128,7 @@ int kkt_dev_step_solve(kkt_device *d, const double *r_in, double *x_out, int io_
   if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
   e = cudaStreamSynchronize(dev->stream);
   if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
-  return KKT_OK;
+  return rc_refine;
 }
 
 int kkt_op_create(int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int symmetric_lower,

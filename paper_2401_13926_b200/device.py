@@ -67,7 +67,7 @@ class DeviceSystem:
         lm = lower_map(G)
         self.lower = lm  # (row_ptr, col_idx, gen_src) or None (structurally unsymmetric)
         opts = nat.DeviceOpts(device=device, batch=self.nb, restart_m=int(restart_m),
-                              trisolve_mode=0, flags=0)
+                              reserved=0, flags=0)
         h = C.c_void_p()
         rp = np.ascontiguousarray(G.row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(G.col_idx, dtype=np.int64)
@@ -193,39 +193,79 @@ class DeviceSystem:
         """x += y on the device (kkt_dev_axpy)."""
         nat.check(self.lib.kkt_dev_axpy(self.h, _vp(x_t), _vp(y_t)), "kkt_dev_axpy")
 
-    def residual_stats_device(self, r_t, x_t) -> ResidualStats:
-        out = (C.c_double * 6)()
+    def residual_stats_device(self, r_t, x_t):
+        """ResidualStats of r - K x (one per system on a batched handle)."""
+        out = (C.c_double * (6 * self.nb))()
         nat.check(self.lib.kkt_dev_residual_norms(self.h, _vp(r_t), _vp(x_t), out))
-        return ResidualStats(*list(out))
+        stats = [ResidualStats(*out[6 * q:6 * q + 6]) for q in range(self.nb)]
+        return stats[0] if self.nb == 1 else stats
 
     def fgmres_device(self, b_t, x0_t, x_t, m: int, max_outer: int, tol: float,
-                      hist_cap: int = 4096):
-        """FGMRES on every system; returns (report, history) or lists of them (batch)."""
-        cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(tol), delta_tol=float(tol))
+                      K=None, M=None, host_loop: bool = False, flags: int = 0):
+        """FGMRES (krylov.py:117) on every system: returns (report, history, restart_pairs)
+        or a list of them (batch).  K / M: ``nat.LinOp`` (None = the handle's operator values /
+        LU factors).  The whole solve is one device-controlled CUDA graph unless a host
+        callback operator (or ``host_loop``) asks for the host-stepped control."""
+        cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(tol), delta_tol=float(tol),
+                            flags=flags | (nat.FG_HOST_LOOP if host_loop else 0))
         reps = (nat.KrylovReport * self.nb)()
-        hist = (C.c_double * (hist_cap * self.nb))()
-        nat.check(self.lib.kkt_dev_fgmres(self.h, _vp(b_t), _vp(x0_t), _vp(x_t), C.byref(cfg),
-                                          reps, hist, hist_cap), "kkt_dev_fgmres")
+        hcap = int(max_outer) * int(m) + 1
+        pcap = max(int(max_outer), 1)
+        hist = (C.c_double * (hcap * self.nb))()
+        pairs = (C.c_double * (2 * pcap * self.nb))()
+        rc = self.lib.kkt_dev_fgmres_ops(self.h, C.byref(K) if K is not None else None,
+                                         C.byref(M) if M is not None else None, _vp(b_t), _vp(x0_t),
+                                         _vp(x_t), C.byref(cfg), reps, hist, hcap, pairs, pcap)
+        nat.check(rc, "kkt_dev_fgmres_ops")
         out = []
         for q in range(self.nb):
-            nh = min(reps[q].iterations + 1, hist_cap)
-            out.append((reps[q], [hist[q * hist_cap + i] for i in range(nh)]))
+            nh = min(reps[q].iterations + 1, hcap)
+            npair = min(reps[q].restarts, pcap)
+            out.append((reps[q], [hist[q * hcap + i] for i in range(nh)],
+                        [(pairs[2 * (q * pcap + i)], pairs[2 * (q * pcap + i) + 1])
+                         for i in range(npair)]))
         return out[0] if self.nb == 1 else out
 
+    def refine_device(self, r_t, x0_t, x_t, m: int, max_outer: int, delta_tol,
+                      host_loop: bool = False, mgs: bool = False):
+        """refine_fgmres (refine.py:103-132) in one call: trigger, FGMRES and the residual
+        statistics before / after, decided on the device; one host synchronisation."""
+        dsys = None
+        if np.ndim(delta_tol):
+            dsys = (C.c_double * self.nb)(*[float(v) for v in delta_tol])
+            delta_tol = float(np.max(delta_tol))
+        flags = (nat.FG_STATS_AFTER | (nat.FG_HOST_LOOP if host_loop else 0)
+                 | (nat.FG_MGS if mgs else 0))
+        cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(delta_tol),
+                            delta_tol=float(delta_tol), delta_sys=dsys, flags=flags)
+        reps = (nat.KrylovReport * self.nb)()
+        rc = self.lib.kkt_dev_refine_fgmres(self.h, _vp(r_t), _vp(x0_t), _vp(x_t), C.byref(cfg), reps)
+        self._check_batch(rc, "kkt_dev_refine_fgmres")
+        return reps[0] if self.nb == 1 else list(reps)
+
+    def _check_batch(self, rc, what):
+        # a batch reports non-finite failures per system (KrylovReport.nonfinite) and still
+        # returns every other system's solution; a single system raises like the reference
+        if rc == nat.KKT_ERR_NONFINITE and self.nb > 1:
+            return
+        nat.check(rc, what)
+
     def step(self, values: np.ndarray | object, layout: int, r, x_out, on_device: bool,
-             m: int, max_outer: int, delta_tol, diag: bool = False):
+             m: int, max_outer: int, delta_tol, diag: bool = False, stats: bool = False):
         """refactor -> solve -> refine_fgmres in one C call (kkt_dev_step) for every system.
 
         ``delta_tol`` is a float or a per-system sequence.  Returns the KrylovReport (single
         system) or the list of reports (batch); with ``diag`` also the per-system
-        LuDiagnostics array ``[nb][4]``.
+        LuDiagnostics array ``[nb][4]``.  ``stats`` also fills the reports' residual statistics
+        of x0 and x (nsr / nrbe before and after, refine.py:117,129-131).
         """
         dsys = None
         if np.ndim(delta_tol):
             dsys = (C.c_double * self.nb)(*[float(v) for v in delta_tol])
             delta_tol = float(np.max(delta_tol))
         cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(delta_tol),
-                            delta_tol=float(delta_tol), delta_sys=dsys)
+                            delta_tol=float(delta_tol), delta_sys=dsys,
+                            flags=nat.FG_STATS_AFTER if stats else 0)
         reps = (nat.KrylovReport * self.nb)()
         dg = (C.c_double * (4 * self.nb))() if diag else None
         if on_device:
@@ -233,7 +273,7 @@ class DeviceSystem:
         else:
             args = (values.ctypes.data_as(C.c_void_p), layout, r.ctypes.data_as(C.c_void_p),
                     x_out.ctypes.data_as(C.c_void_p), 0)
-        nat.check(self.lib.kkt_dev_step(self.h, *args, C.byref(cfg), reps, dg), "kkt_dev_step")
+        self._check_batch(self.lib.kkt_dev_step(self.h, *args, C.byref(cfg), reps, dg), "kkt_dev_step")
         self._op_key = None
         rep = reps[0] if self.nb == 1 else list(reps)
         if diag:
@@ -254,7 +294,8 @@ class DeviceSystem:
             args = (_vp(r), _vp(x_out), 1)
         else:
             args = (r.ctypes.data_as(C.c_void_p), x_out.ctypes.data_as(C.c_void_p), 0)
-        nat.check(self.lib.kkt_dev_step_solve(self.h, *args, C.byref(cfg), reps), "kkt_dev_step_solve")
+        self._check_batch(self.lib.kkt_dev_step_solve(self.h, *args, C.byref(cfg), reps),
+                          "kkt_dev_step_solve")
         return reps[0] if self.nb == 1 else list(reps)
 
     def refactor_batch(self, values_t, layout: int) -> np.ndarray:

@@ -26,6 +26,7 @@ from . import _native as nat
 from .direct_lu import factorize, lu_solve, refactorize
 from .refine import (FixedTolerance, RefinementConfig, config_for_mu, refine_fgmres,
                      refine_richardson)
+from .device import ResidualStats
 from .sparse import SYMMETRIC_LOWER, CsMatrix, to_general
 
 
@@ -49,38 +50,57 @@ class MatrixSequence:
 
 
 def _lower_nnz(K: CsMatrix) -> int:
+    """Entries on or below the diagonal (the symmetric-lower storage size)."""
     if K.symmetry == SYMMETRIC_LOWER:
         return K.nnz
-    rows = np.repeat(np.arange(K.n_rows), np.diff(K.row_ptr))
-    return int(np.count_nonzero(rows >= K.col_idx))
+    row_of = np.repeat(np.arange(K.n_rows, dtype=np.int64), np.diff(K.row_ptr))
+    return int((K.col_idx <= row_of).sum())
 
 
-def load_sequence(manifest_path: str) -> MatrixSequence:
-    """A manifest's systems through the C++ Matrix Market reader, validating the shared
-    pattern (harness.load_sequence, harness.py:118-146)."""
+def load_sequence(manifest_path: str, workers: int | None = None) -> MatrixSequence:
+    """Load a manifest's systems (harness.load_sequence, harness.py:118-146).
+
+    The Matrix Market files are parsed concurrently by the C++ reader (``kkt_mm_*`` releases
+    the GIL), then validated in manifest order so the first failing system raises the
+    reference's ``SequenceError`` (rhs length before pattern).  Every system after the first
+    shares system 0's pattern arrays: a sequence costs one pattern plus M value arrays.
+    """
+    from concurrent.futures import ThreadPoolExecutor
+
     from .mmio import load_matrix_market, load_vector
     with open(manifest_path, "r") as fh:
         manifest = json.load(fh)
-    systems = manifest.get("systems", [])
-    if not systems:
+    entries = manifest.get("systems", [])
+    if not entries:
         raise SequenceError("sequence must contain at least one system")
     base = os.path.dirname(os.path.abspath(manifest_path))
+    paths = [(os.path.join(base, e["matrix"]), os.path.join(base, e["rhs"])) for e in entries]
+
+    def parse(pair):
+        try:
+            return load_matrix_market(pair[0]), load_vector(pair[1]), None
+        except Exception as exc:  # raised in manifest order below
+            return None, None, exc
+
+    with ThreadPoolExecutor(max_workers=workers or min(8, len(paths))) as ex:
+        parsed = list(ex.map(parse, paths))
     items: list[SequenceItem] = []
-    for i, entry in enumerate(systems):
-        mpath = os.path.join(base, entry["matrix"])
-        rpath = os.path.join(base, entry["rhs"])
-        K = load_matrix_market(mpath)
-        rhs = load_vector(rpath)
+    K0 = None
+    for i, ((mpath, rpath), (K, rhs, err)) in enumerate(zip(paths, parsed)):
+        if err is not None:
+            raise err
         if rhs.size != K.n_rows:
             raise SequenceError(f"system {i}: rhs length {rhs.size} does not "
                                 f"match matrix dimension {K.n_rows}")
-        if items and not K.same_pattern(items[0].K):
+        if K0 is None:
+            K0 = K
+        elif not K.same_pattern(K0):
             raise SequenceError(f"system {i}: sparsity pattern differs from system 0")
+        else:
+            K = K0.with_values(K.values)
         items.append(SequenceItem(K=K, rhs=rhs, matrix_path=mpath, rhs_path=rpath))
-    metadata = {"N": items[0].K.n_rows, "nnz": _lower_nnz(items[0].K)}
-    for key in ("n", "m", "mu"):
-        if key in manifest:
-            metadata[key] = manifest[key]
+    metadata = {"N": K0.n_rows, "nnz": _lower_nnz(K0)}
+    metadata.update({k: manifest[k] for k in ("n", "m", "mu") if k in manifest})
     return MatrixSequence(name=manifest.get("name", "sequence"), items=items, metadata=metadata)
 
 
@@ -157,7 +177,7 @@ def run_refactor_ir(matrices, rhss, cfg: RefinementConfig | None = None, mus=Non
             x = np.empty_like(r)
             t0 = time.perf_counter()
             krep = dev.step(np.ascontiguousarray(K.values), layout, r, x, False,
-                            rc.krylov.m, rc.krylov.max_outer, rc.delta_tol)
+                            rc.krylov.m, rc.krylov.max_outer, rc.delta_tol, stats=True)
             t_fact, t_solve, t_ref = time.perf_counter() - t0, 0.0, 0.0
             factors._host_vals = None
             factors.from_refactorization = True
@@ -165,15 +185,13 @@ def run_refactor_ir(matrices, rhss, cfg: RefinementConfig | None = None, mus=Non
             conv = bool(krep.converged)
             tsolves = 1 + iters
             factors.triangular_solve_count += tsolves
-            nsr_b = nsr_a = float("nan")
+            nsr_b = ResidualStats(*krep.stats_before).nsr()
+            nsr_a = ResidualStats(*krep.stats_after).nsr() if krep.triggered else nsr_b
         # quality metrics of the returned x, one device residual pass (harness.py:249-266)
         dev.set_operator(K)
         dev.h2d(dev.r, r)
         dev.h2d(dev.x, x)
         s = dev.residual_stats_device(dev.r, dev.x)
-        if np.isnan(nsr_a):
-            nsr_a = s.nsr()
-            nsr_b = nsr_a if iters == 0 else float("nan")
         if not np.all(np.isfinite(x)):
             conv = False
         rr = s.err2 / s.r2 if s.r2 > 0 else 0.0

@@ -117,29 +117,35 @@ def needs_refinement(K, x0, r, delta_tol: float) -> bool:
 
 
 def refine_fgmres(K, factors, x0, r, cfg: RefinementConfig):
-    """FGMRES refinement of a direct solve, LU factors as right preconditioner (refine.py:103)."""
+    """FGMRES refinement of a direct solve, LU factors as right preconditioner (refine.py:103).
+
+    One device call (``kkt_dev_refine_fgmres``): the trigger ``||r - K x0||_2 > delta ||r||_2``
+    (:113), NSR before (:117), FGMRES with ``tol = delta_tol`` (:119-126) and NSR / NRBE after
+    (:129-131) are all computed and decided on the device; the host synchronises once.
+    """
+    from .device import ResidualStats
     x0 = np.asarray(x0, dtype=np.float64)
     r = np.asarray(r, dtype=np.float64)
     dev = factors.device(restart_m=cfg.krylov.m)
     dev.set_operator(K)
     dev.h2d(dev.r, r)
     dev.h2d(dev.x0, x0)
-    s0 = dev.residual_stats_device(dev.r, dev.x0)
-    if not (s0.err2 > cfg.delta_tol * s0.r2):
+    if cfg.krylov.ortho not in ("cgs2", "mgs"):
+        raise ValueError(f"unknown orthogonalization {cfg.krylov.ortho!r}")
+    rep = dev.refine_device(dev.r, dev.x0, dev.x, cfg.krylov.m, cfg.krylov.max_outer, cfg.delta_tol,
+                            mgs=cfg.krylov.ortho == "mgs")
+    s0 = ResidualStats(*rep.stats_before)
+    if not rep.triggered:                                                    # (:113-114)
         q = s0.nsr()
         return x0.copy(), RefinementReport(
             triggered=False, method="none", ir_iterations=0, triangular_solves_used=0,
             nsr_before=q, nsr_after=q, rr_final=1.0, nrbe_final=s0.nrbe(), converged=True)
-    if cfg.krylov.ortho != "cgs2":
-        raise NotImplementedError("the device Arnoldi step implements CGS2")
     count0 = factors.triangular_solve_count
-    kcfg = replace(cfg.krylov, tol=cfg.delta_tol)
-    rep, hist = dev.fgmres_device(dev.r, dev.x0, dev.x, kcfg.m, kcfg.max_outer, kcfg.tol)
     factors.triangular_solve_count += rep.precond_applications
-    s1 = dev.residual_stats_device(dev.r, dev.x)
+    s1 = ResidualStats(*rep.stats_after)
     x = dev.d2h(dev.x)
-    rho0 = hist[0]
-    rr_final = (hist[-1] / rho0) if rho0 > 0 else 0.0
+    rho0 = rep.beta0
+    rr_final = (rep.est_final / rho0) if rho0 > 0 else 0.0               # (:123-124)
     return x, RefinementReport(
         triggered=True, method="fgmres", ir_iterations=rep.iterations,
         triangular_solves_used=factors.triangular_solve_count - count0,
