@@ -270,6 +270,10 @@ int kkt_dev_step_solve(kkt_device *d, const double *r_in, double *x_out, int io_
 /* Download the current factor values in the LuFactors layout (_Lx, _Ux, _Udiag). */
 int kkt_dev_download_factors(kkt_device *d, double *Lx, double *Ux, double *Udiag);
 
+/* The inverse (batch == 1): make (_Lx, _Ux, _Udiag) the handle's current factors, e.g. to
+ * re-create a device handle for LuFactors whose values came from an earlier refactorize. */
+int kkt_dev_upload_factors(kkt_device *d, const double *Lx, const double *Ux, const double *Udiag);
+
 /* ======================================================================
  * Standalone operator (sparsecore.spmv / refine.nsr / refine.nrbe on a bare matrix).
  * row_ptr/col_idx: CSR as stored (symmetric_lower != 0 => lower triangle incl. diagonal,

@@ -103,6 +103,7 @@ SIGNATURES = [
                                C.POINTER(KrylovReport), f64p]),
     ("kkt_dev_step_solve", C.c_int, [vp, vp, vp, C.c_int, C.POINTER(KrylovCfg), C.POINTER(KrylovReport)]),
     ("kkt_dev_download_factors", C.c_int, [vp, f64p, f64p, f64p]),
+    ("kkt_dev_upload_factors", C.c_int, [vp, f64p, f64p, f64p]),
     ("kkt_op_create", C.c_int, [i64, i64p, i64p, C.c_int, C.c_int, C.POINTER(vp)]),
     ("kkt_op_destroy", None, [vp]),
     ("kkt_op_stream", vp, [vp]),

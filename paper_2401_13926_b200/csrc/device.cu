@@ -911,6 +911,29 @@ int kkt_dev_download_factors(kkt_device *d, double *Lx, double *Ux, double *Udia
   return KKT_OK;
 }
 
+int kkt_dev_upload_factors(kkt_device *d, const double *Lx, const double *Ux, const double *Udiag) {
+  Device *dev = reinterpret_cast<Device *>(d);
+  if (!dev || !Lx || !Ux || !Udiag) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
+  if (dev->d.nbp != 1) return kkt::set_error(KKT_ERR_BAD_ARG, "kkt_dev_upload_factors needs batch == 1");
+  cudaSetDevice(dev->device);
+  const kkt::HostPlan &h = dev->h;
+  const kkt::DevPlan &p = dev->d;
+  // both layouts: CSC (the refactor's) and CSR (the solves'), through the CSC->CSR maps
+  std::vector<double> lv(h.nnz_L), uv(h.nnz_U);
+  for (int64_t q = 0; q < h.nnz_L; ++q) lv[h.Lmap[q]] = Lx[q];
+  for (int64_t q = 0; q < h.nnz_U; ++q) uv[h.Umap[q]] = Ux[q];
+  cudaStream_t s = dev->stream;
+  cudaError_t e = cudaSuccess;
+  if (h.nnz_L) e = cudaMemcpyAsync(p.Lx, Lx, 8 * (size_t)h.nnz_L, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && h.nnz_L) e = cudaMemcpyAsync(p.Lv, lv.data(), 8 * lv.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && h.nnz_U) e = cudaMemcpyAsync(p.Ux, Ux, 8 * (size_t)h.nnz_U, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && h.nnz_U) e = cudaMemcpyAsync(p.Uv, uv.data(), 8 * uv.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && p.n) e = cudaMemcpyAsync(p.udiag, Udiag, 8 * (size_t)p.n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
+  return KKT_OK;
+}
+
 // Batched handles keep vectors interleaved internally; the ABI takes [nb][n] and converts
 // through the handle's staging vectors.
 #define IL_IN(src, dst)                                                                   \

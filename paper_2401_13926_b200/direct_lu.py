@@ -122,10 +122,17 @@ class LuFactors:
         if self._dev is None:
             from .device import DeviceSystem
             self._dev = DeviceSystem(self, restart_m=restart_m)
+            if self.from_refactorization and self._host_vals is not None:
+                # the values of the last refactorize (kept on the host by close())
+                Lx, Ux, Ud = (np.ascontiguousarray(v, dtype=np.float64) for v in self._host_vals)
+                nat.check(self._dev.lib.kkt_dev_upload_factors(
+                    self._dev.h, nat.ptr_f64(Lx), nat.ptr_f64(Ux), nat.ptr_f64(Ud)))
         return self._dev
 
     def close(self):
+        """Free the device handle; the current factor values stay available on the host."""
         if self._dev is not None:
+            self._values()
             self._dev.close()
             self._dev = None
 

@@ -5,7 +5,8 @@
 CASE is one of ``activsg200`` (N = 9,030, configs[0]), ``activsg200p`` (the same family with
 imbalance slacks on half the buses: the reference's threshold pivoting then picks ~1,400
 off-diagonal pivots), ``activsg2000`` (N = 90,320, configs[1]) and ``activsg2000p``
-(imbalance slacks on 75 % of the buses: ~7,600 off-diagonal pivots, fill ~10x).
+(imbalance slacks on 75 % of the buses: ~7,600 off-diagonal pivots, fill ~10x, 1.9 G update
+pairs per refactorization) and ``activsg2000q`` (90 %: ~3,200 off-diagonal pivots, fill ~2.6x).
 
 For each case the REFERENCE package (``kktsolve`` imported from /root/reference, never needed
 at test time) runs exactly the hot path of ``harness._run_direct_family`` (harness.py:217-269):
@@ -50,6 +51,7 @@ CASES = {
     "activsg200p": ("activsg200", 0.5, True, (1, 10, 19)),
     "activsg2000": ("activsg2000", 1.0, False, (19,)),
     "activsg2000p": ("activsg2000", 0.75, False, (19,)),
+    "activsg2000q": ("activsg2000", 0.9, False, (19,)),
 }
 M = 20
 FACTOR_KEYS = ["row_perm", "col_perm", "Lp", "Li", "Lx", "Up", "Ui", "Ux", "Udiag", "so_ptr",

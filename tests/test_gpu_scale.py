@@ -117,3 +117,99 @@ def test_full_size_batch_equals_single(config, nb):
         dev1.solve_device(r1, x1)
         assert np.array_equal(xb[q], dev1.d2h(x1))
     devb.close()
+
+
+def _oracle_refine_all(f, K0, pat, items, threads=8):
+    """Oracle refactorize + lu_solve + refine_fgmres of every (values, rhs, delta) item,
+    one OracleFactors per worker thread (the C oracle releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import oracle
+    out = [None] * len(items)
+
+    def work(w):
+        of, ex = _oracle(f, K0)
+        for i in range(w, len(items), threads):
+            vals, r, delta = items[i]
+            of.refactorize(vals[ex.src])
+            x0 = of.lu_solve(r)
+            x, rep = of.refine_fgmres(pat.K.row_ptr, pat.K.col_idx, vals, r, x0, delta)
+            rr = np.linalg.norm(r - oracle.spmv(pat.K.row_ptr, pat.K.col_idx, vals, x)) / np.linalg.norm(r)
+            out[i] = (x0, rep, rr)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(work, range(threads)))
+    return out
+
+
+def _check_vs_oracle(tag, rep, rr, orep, rr_o, delta):
+    from large_golden import rr_bound
+    assert bool(rep.triggered) == orep["triggered"], tag
+    assert abs(rep.iterations - orep["iterations"]) <= 1, (tag, rep.iterations, orep["iterations"])
+    assert bool(rep.converged) == orep["converged"] and rep.converged, tag
+    assert rr <= rr_bound(rr_o, delta), (tag, rr, rr_o)
+
+
+def test_bench_batch_against_oracle():
+    """The benchmarked configuration itself: bench.py's B = 64 batch at ACTIVSg10k (its value
+    streams, barrier-tied delta) through the exact call the bench times (kkt_dev_step on the
+    device-resident batch), at the three latest (most refined) barrier steps k = 17, 18, 19;
+    every one of the 192 systems against the oracle."""
+    import torch
+    import paper_2401_13926_b200._native as nat
+    from bench import make_batch, rank_seed_base
+    from paper_2401_13926_b200.device import DeviceSystem
+    from paper_2401_13926_b200.refine import BarrierTiedTolerance
+    pat, K0, f = _setup("activsg10k")
+    B = 64
+    dev = DeviceSystem(f, restart_m=10, batch=B)
+    LOWER = nat.LAYOUT_SYMMETRIC_LOWER
+    policy = BarrierTiedTolerance()
+    for k in (17, 18, 19):
+        vals, rhs, mu = make_batch(pat, B, k, rank_seed_base(0))
+        delta = policy(mu)
+        with torch.cuda.stream(dev.stream):
+            tv = torch.from_numpy(vals).to(dev.device)
+            tr = torch.from_numpy(rhs).to(dev.device)
+            tx = torch.empty_like(tr)
+        reps = dev.step(tv, LOWER, tr, tx, True, 10, 10, [delta] * B, stats=True)
+        x = dev.d2h(tx)
+        ores = _oracle_refine_all(f, K0, pat, [(vals[q], rhs[q], delta) for q in range(B)])
+        for q in range(B):
+            x0, orep, rr_o = ores[q]
+            rep = reps[q]
+            rr = rep.stats_after[0] / rep.stats_after[4] if rep.triggered else \
+                rep.stats_before[0] / rep.stats_before[4]
+            _check_vs_oracle((k, q), rep, rr, orep, rr_o, delta)
+            if not rep.triggered:
+                assert np.array_equal(x[q], x0), (k, q)
+    dev.close()
+
+
+def test_sequence_238k_against_oracle():
+    """The north-star sequence (configs[2]): systems 1..19 of the ACTIVSg10k barrier sequence
+    one at a time on a single-system handle, each against the oracle (factors and x0 bitwise,
+    refine within the bars)."""
+    import torch
+    import paper_2401_13926_b200._native as nat
+    from paper_2401_13926_b200.acopf import MU_STEP, system_rhs, system_values
+    from paper_2401_13926_b200.refine import BarrierTiedTolerance
+    pat, K0, f = _setup("activsg10k")
+    policy = BarrierTiedTolerance()
+    items = [(system_values(pat, k, 0), system_rhs(pat, k, 0), policy(10.0 ** (-MU_STEP * k)))
+             for k in range(1, 20)]
+    ores = _oracle_refine_all(f, K0, pat, items)
+    dev = f.device(restart_m=10)
+    LOWER = nat.LAYOUT_SYMMETRIC_LOWER
+    for i, (vals, r, delta) in enumerate(items):
+        with torch.cuda.stream(dev.stream):
+            tv = torch.from_numpy(vals).to(dev.device)
+            tr = torch.from_numpy(r).to(dev.device)
+            tx = torch.empty_like(tr)
+        dev.solve_device(tr, tx)  # warm path; the step below refactorizes first
+        rep = dev.step(tv, LOWER, tr, tx, True, 10, 10, delta, stats=True)
+        x0_o, orep, rr_o = ores[i]
+        dev.solve_device(tr, tx)
+        assert np.array_equal(dev.d2h(tx), x0_o), i + 1  # factors of system i+1 -> x0 bitwise
+        rr = rep.stats_after[0] / rep.stats_after[4] if rep.triggered else \
+            rep.stats_before[0] / rep.stats_before[4]
+        _check_vs_oracle(i + 1, rep, rr, orep, rr_o, delta)
