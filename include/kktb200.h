@@ -199,8 +199,11 @@ enum {
   KKT_FG_HOST_LOOP = 2,   /* drive the restart/iteration control from the host (reads the
                              device control words per iteration) instead of one CUDA graph
                              with conditional nodes; same kernels, same results          */
-  KKT_FG_MGS = 4          /* modified Gram-Schmidt (KrylovConfig.ortho = "mgs") instead of
+  KKT_FG_MGS = 4,         /* modified Gram-Schmidt (KrylovConfig.ortho = "mgs") instead of
                              CGS2                                                        */
+  KKT_FG_NO_HANDOFF = 8   /* batched handles: keep every system in the lockstep batch to
+                             the end (default: once at most min(4, batch/16) systems still
+                             run, they finish on single-system helper handles)            */
 };
 
 typedef struct {
@@ -217,6 +220,9 @@ typedef struct {
                              ||r||_2, ||K||_inf}  (nsr_before, refine.py:117)         */
   double stats_after[6];  /* refine + KKT_FG_STATS_AFTER: the same for the returned x
                              (nsr_after / nrbe_final, refine.py:129-131)             */
+  int handed_off;         /* batched handles: this straggler's last iterations ran on a
+                             single-system helper (same arithmetic; KKT_HANDOFF)       */
+  int reserved_;
 } kkt_krylov_report;
 
 /* FGMRES(m) with CGS2, K = operator values, M = lu_solve with the current factors

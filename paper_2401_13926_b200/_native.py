@@ -27,6 +27,7 @@ KKT_ERR_CALLBACK = 8
 FG_STATS_AFTER = 1
 FG_HOST_LOOP = 2
 FG_MGS = 4
+FG_NO_HANDOFF = 8
 OP_HANDLE, OP_IDENTITY, OP_MATRIX, OP_CALLBACK = 0, 1, 2, 3
 LAYOUT_GENERAL = 0
 LAYOUT_SYMMETRIC_LOWER = 1
@@ -53,7 +54,8 @@ class KrylovReport(C.Structure):
                 ("precond_applications", C.c_int), ("restarts", C.c_int),
                 ("beta0", C.c_double), ("est_final", C.c_double),
                 ("true_final", C.c_double), ("triggered", C.c_int), ("nonfinite", C.c_int),
-                ("stats_before", C.c_double * 6), ("stats_after", C.c_double * 6)]
+                ("stats_before", C.c_double * 6), ("stats_after", C.c_double * 6),
+                ("handed_off", C.c_int), ("reserved_", C.c_int)]
 
 
 APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)

@@ -47,6 +47,8 @@ static void destroy(Device *dev) {
   if (!dev) return;
   cudaSetDevice(dev->device);
   if (dev->stream) cudaStreamSynchronize(dev->stream);
+  for (Device *hp : dev->helpers) destroy(hp);
+  dev->helpers.clear();
   free_krylov(dev);
   if (dev->arena) cudaFree(dev->arena);
   if (dev->trace_mem) cudaFree(dev->trace_mem);
@@ -55,6 +57,7 @@ static void destroy(Device *dev) {
   if (dev->stream2) cudaStreamDestroy(dev->stream2);
   if (dev->ev_a) cudaEventDestroy(dev->ev_a);
   if (dev->ev_b) cudaEventDestroy(dev->ev_b);
+  if (dev->ev_h) cudaEventDestroy(dev->ev_h);
   delete dev;
 }
 
@@ -134,6 +137,8 @@ static int build_heavy(const HostPlan &h, int J0, HeavyPlan &H) {
   return KKT_OK;
 }
 
+static int setup(Device *dev, const kkt_device_opts *opts, Device *&out);
+
 static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int64_t in_nnz,
                   const int64_t *gen_src, const kkt_device_opts *opts, Device *&out) {
   out = nullptr;
@@ -143,6 +148,24 @@ static int create(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, i
     delete dev;
     return rc;
   }
+  return setup(dev, opts, out);
+}
+
+// A handle of another batch width over the same host plan (the straggler helper of a batch).
+int create_like(const Device *src, int batch, Device *&out) {
+  out = nullptr;
+  Device *dev = new Device();
+  dev->h = src->h;
+  kkt_device_opts o{};
+  o.device = src->device;
+  o.batch = batch;
+  o.restart_m = src->restart_m;
+  return setup(dev, &o, out);
+}
+
+// Everything after the host plan: device arrays, schedules, launch shapes.
+static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
+  int rc = KKT_OK;
   const HostPlan &h = dev->h;
   dev->device = opts ? opts->device : 0;
   dev->restart_m = (opts && opts->restart_m > 0) ? opts->restart_m : 10;

@@ -9,6 +9,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "plan.h"
 
 namespace kkt {
@@ -155,7 +157,14 @@ struct Device {
   double *pinned = nullptr;  // pinned host staging (status words)
   size_t pinned_bytes = 0;
   int restart_m = 10;
+  // Straggler helpers (batched handles): single-system handles over the same plan that take
+  // over the FGMRES of the last few running systems of a batch (krylov.cu, handoff).
+  std::vector<Device *> helpers;
+  cudaEvent_t ev_h = nullptr;
 };
+
+// a handle of width `batch` over src's host plan (device.cu)
+int create_like(const Device *src, int batch, Device *&out);
 
 // ---- launchers (each returns cudaGetLastError of its launch) ----
 cudaError_t launch_expand_norms(const DevPlan &d, cudaStream_t s);

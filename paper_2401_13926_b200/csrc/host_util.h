@@ -40,7 +40,8 @@ struct FgBufs {
   double *beta0 = nullptr, *bnew = nullptr, *target = nullptr, *floor_ = nullptr, *est = nullptr,
          *hj1 = nullptr;
   int *act_in = nullptr, *active = nullptr, *running = nullptr, *cycle = nullptr, *jused = nullptr,
-      *iters = nullptr, *restarts = nullptr, *converged = nullptr, *failed = nullptr, *trig = nullptr;
+      *iters = nullptr, *restarts = nullptr, *converged = nullptr, *failed = nullptr, *trig = nullptr,
+      *handed = nullptr, *vmask = nullptr;
   int *ctrl = nullptr;                // control words (iteration / cycle conditions, counters)
   unsigned long long *hnd = nullptr;  // conditional-node handles the control kernels set
   double *out = nullptr;              // report block | history | restart pairs (one D2H)
@@ -53,7 +54,7 @@ struct FgBufs {
 struct FgGraph {
   const double *b = nullptr, *x0 = nullptr;
   double *xout = nullptr;
-  int m = 0, mode = 0, want_after = 0, mgs = 0;
+  int m = 0, mode = 0, want_after = 0, mgs = 0, resume = 0, T = 0;
   DevPlan plan{};
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;

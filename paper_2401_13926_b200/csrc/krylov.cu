@@ -175,8 +175,11 @@ __global__ void __launch_bounds__(RED_THREADS) k_sub_norm(const double *__restri
 struct FgCtl {
   double *beta0, *beta, *bnew, *target, *floor_, *est, *hj1, *tolq;
   int *act_in, *active, *running, *cycle, *jused, *iters, *restarts, *converged, *failed, *trig;
+  int *vmask;                    // systems whose V_0 = r / beta the cycle start computes
+  int *handed;                   // > 0: handed to a helper after that many iterations of its cycle
   int *ctrl;                     // [0..m-1] run iteration j, [m] another cycle, [m+1] cycles run,
-                                 // [m+2] iteration bodies run, [m+3] any failure, [m+4] max_outer
+                                 // [m+2] iteration bodies run, [m+3] any failure, [m+4] max_outer,
+                                 // [m+5] resume at iteration j0 (> 0), [m+6] systems handed off
   unsigned long long *hnd;       // [m+1] conditional handles (IF j, WHILE at m)
   double *hist;                  // [nbp][hcap] est_residual_history
   double *rpair;                 // [nbp][rpcap][2] restart (estimated, true) pairs
@@ -185,6 +188,7 @@ struct FgCtl {
   unsigned long long *scal;      // the handle's per-system scalar blocks
   double *g, *H, *cs, *sn, *h1, *h2, *nrm;
   int nb, m, M, hcap, rpcap, mode, graph;
+  int T;                         // straggler hand-off threshold (running systems; 0 = off)
 };
 
 constexpr int FG_REP = 24;  // doubles per system in the report block
@@ -215,6 +219,7 @@ __global__ void __launch_bounds__(FG_THREADS) k_fg_init(FgCtl c) {
     c.running[q] = 0;
     c.cycle[q] = 0;
     c.failed[q] = 0;
+    c.handed[q] = 0;
     c.converged[q] = t ? 0 : 1;
     c.target[q] = c.tolq[q] * b;
     c.floor_[q] = HAPPY_BREAKDOWN_RTOL * b;
@@ -239,6 +244,8 @@ __global__ void __launch_bounds__(FG_THREADS) k_fg_init(FgCtl c) {
     c.ctrl[c.m + 1] = 0;
     c.ctrl[c.m + 2] = 0;
     c.ctrl[c.m + 3] = fail;
+    c.ctrl[c.m + 5] = 0;
+    c.ctrl[c.m + 6] = 0;
     fg_set(c, c.m, any && c.ctrl[c.m + 4] > 0);
   }
 }
@@ -247,6 +254,21 @@ __global__ void __launch_bounds__(FG_THREADS) k_fg_init(FgCtl c) {
 __global__ void __launch_bounds__(FG_THREADS) k_cycle_begin(FgCtl c) {
   int any = 0;
   const int m1 = c.M + 1;
+  const int j0 = c.ctrl[c.m + 5];
+  if (j0 > 0) {  // a helper resuming a handed-off system inside its cycle, at iteration j0
+    for (int q = threadIdx.x; q < c.nb; q += blockDim.x) {
+      c.running[q] = c.active[q];
+      c.cycle[q] = c.active[q];
+      c.vmask[q] = 0;
+      c.jused[q] = j0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      c.ctrl[c.m + 5] = 0;
+      for (int j = 0; j < c.m; ++j) fg_set(c, j, j == j0);
+    }
+    return;
+  }
   for (int q = threadIdx.x; q < c.nb; q += blockDim.x) {
     int run = 0;
     if (c.active[q]) {
@@ -265,6 +287,7 @@ __global__ void __launch_bounds__(FG_THREADS) k_cycle_begin(FgCtl c) {
     }
     c.running[q] = run;
     c.cycle[q] = run;
+    c.vmask[q] = run;
     c.jused[q] = 0;
     any |= run;
   }
@@ -318,12 +341,39 @@ __global__ void __launch_bounds__(FG_THREADS) k_givens(FgCtl c, int j) {
     if (est <= c.target[q] || hj1 <= c.floor_[q]) c.running[q] = 0;  // (:184-186)
     any |= c.running[q];
   }
+  // Straggler hand-off: once at most T systems of the batch still run, the lockstep batch
+  // would charge each of their iterations at the whole batch's DAG cost.  They leave the
+  // batch here, mid-cycle with their full Krylov state (V_0..j, Z_0..j, H, g, rotations, x),
+  // and a single-system helper resumes them at iteration j + 1 (dev_fgmres, resume_handed):
+  // the same arithmetic, only another handle.
+  __shared__ int s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  if (c.T > 0) {
+    int mine = 0;
+    for (int q = threadIdx.x; q < c.nb; q += blockDim.x) mine += c.running[q];
+    if (mine) atomicAdd(&s_cnt, mine);
+  }
+  __syncthreads();
+  const int cnt = s_cnt;
+  const bool ho = c.T > 0 && cnt > 0 && cnt <= c.T;
+  if (ho) {
+    for (int q = threadIdx.x; q < c.nb; q += blockDim.x)
+      if (c.running[q]) {
+        c.handed[q] = j + 1;
+        c.running[q] = 0;
+        c.active[q] = 0;
+        c.cycle[q] = 0;
+        c.jused[q] = 0;  // the batch's cycle end leaves x alone
+      }
+  }
   any = __syncthreads_or(any);
   fail = __syncthreads_or(fail);
   if (threadIdx.x == 0) {
     c.ctrl[c.m + 2] += 1;
     if (fail) c.ctrl[c.m + 3] = 1;
-    if (j + 1 < c.m) fg_set(c, j + 1, any);
+    if (ho) c.ctrl[c.m + 6] = cnt;
+    if (j + 1 < c.m) fg_set(c, j + 1, any && !ho);
   }
 }
 
@@ -379,6 +429,7 @@ __global__ void k_fg_report(FgCtl c, int have_stats1) {
     for (int i = 0; i < 5; ++i) o[8 + i] = c.mode == 1 ? c.stats0[5 * q + i] : 0.0;
     o[13] = __longlong_as_double((long long)c.scal[(size_t)q * SCAL_STRIDE + SC_OPNORM]);
     for (int i = 0; i < 5; ++i) o[14 + i] = have_stats1 ? c.stats1[5 * q + i] : 0.0;
+    o[19] = c.handed[q];
   }
 }
 
@@ -390,6 +441,80 @@ __global__ void k_unpack_inputs(const double *in, int nbp, int *act_in, int *ctr
 
 __global__ void k_clear_nonfinite(unsigned long long *scal, int nb) {
   for (int q = threadIdx.x; q < nb; q += blockDim.x) scal[(size_t)q * SCAL_STRIDE + SC_NONFINITE] = 0ull;
+}
+
+// ---- straggler hand-off (batched handle -> single-system helper) ------------------------
+// dst[i] = src[i * stride + off]: one system's column of an interleaved [count][stride] array
+__global__ void k_gather_col(double *__restrict__ dst, const double *__restrict__ src, int64_t count,
+                             int stride, int off) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i * stride + off];
+}
+__global__ void k_scatter_col(double *__restrict__ dst, const double *__restrict__ src, int64_t count,
+                              int stride, int off) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i * stride + off] = src[i];
+}
+
+// The per-system control state of system q of the batch (src) -> the helper's system 0 (dst):
+// everything k_givens / k_cycle_end / k_fg_report read, the Hessenberg / rotation state of the
+// open cycle, the histories, the scalar block; resume at iteration j0 of the current cycle.
+__global__ void k_handoff_state(FgCtl src, FgCtl dst, int q, int j0, const double *__restrict__ sbeta,
+                                double *__restrict__ dbeta) {
+  const int m1 = src.M + 1;
+  for (int i = threadIdx.x; i < m1 * src.M; i += blockDim.x) dst.H[i] = src.H[(size_t)q * m1 * src.M + i];
+  for (int i = threadIdx.x; i < m1; i += blockDim.x) {
+    dst.g[i] = src.g[(size_t)q * m1 + i];
+    dst.cs[i] = src.cs[(size_t)q * m1 + i];
+    dst.sn[i] = src.sn[(size_t)q * m1 + i];
+  }
+  for (int i = threadIdx.x; i < min(src.hcap, dst.hcap); i += blockDim.x)
+    dst.hist[i] = src.hist[(size_t)q * src.hcap + i];
+  for (int i = threadIdx.x; i < 2 * min(src.rpcap, dst.rpcap); i += blockDim.x)
+    dst.rpair[i] = src.rpair[(size_t)q * src.rpcap * 2 + i];
+  for (int i = threadIdx.x; i < SCAL_STRIDE; i += blockDim.x)
+    dst.scal[i] = src.scal[(size_t)q * SCAL_STRIDE + i];
+  if (threadIdx.x == 0) {
+    dst.beta0[0] = src.beta0[q];
+    dbeta[0] = sbeta[q];
+    dst.target[0] = src.target[q];
+    dst.floor_[0] = src.floor_[q];
+    dst.est[0] = src.est[q];
+    dst.hj1[0] = src.hj1[q];
+    dst.iters[0] = src.iters[q];
+    dst.restarts[0] = src.restarts[q];
+    dst.trig[0] = src.trig[q];
+    dst.converged[0] = 0;
+    dst.failed[0] = 0;
+    dst.handed[0] = 0;
+    dst.active[0] = 1;
+    dst.running[0] = 1;
+    dst.cycle[0] = 1;
+    dst.jused[0] = j0;
+    for (int i = 0; i < 5; ++i) dst.stats0[i] = src.stats0[5 * q + i];
+    // cycles completed: the batch's count minus the open cycle (its end ran without q)
+    dst.ctrl[dst.m + 1] = src.ctrl[src.m + 1] - 1;
+    dst.ctrl[dst.m + 5] = j0;
+  }
+}
+
+// Helper prologue: V_j0 = w / h_{j0,j0-1} (the scale the batch skipped for the handed system),
+// the first cycle's WHILE condition.
+__global__ void __launch_bounds__(RED_THREADS) k_resume_begin(FgCtl c, double *__restrict__ V,
+                                                              const double *__restrict__ w, int n) {
+  const int j0 = c.ctrl[c.m + 5];
+  if (j0 < c.m) {
+    const double dv = c.hj1[0];
+    double *vj = V + (size_t)j0 * n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+      vj[i] = __ddiv_rn(w[i], dv);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c.ctrl[c.m + 2] = 0;
+    c.ctrl[c.m + 3] = 0;
+    c.ctrl[c.m + 6] = 0;
+    fg_set(c, c.m, 1);
+  }
 }
 
 // ---- workspace -------------------------------------------------------------------------
@@ -478,7 +603,7 @@ static int ensure_control(Device *dev, int m, int max_outer) {
   K.c_m = std::max(m, K.c_m);
   const size_t out_doubles = nb * FG_REP + nb * K.c_hcap + nb * K.c_rpcap * 2 + 16;
   const size_t in_doubles = nb * 2 + 8;
-  size_t bytes = 6 * align_up(8 * nb + 64) + 10 * align_up(4 * nb + 64) + align_up(4 * (K.c_m + 8)) +
+  size_t bytes = 6 * align_up(8 * nb + 64) + 12 * align_up(4 * nb + 64) + align_up(4 * (K.c_m + 8)) +
                  align_up(8 * (K.c_m + 1)) + align_up(8 * out_doubles) + 2 * align_up(8 * 5 * nb + 64) +
                  align_up(8 * in_doubles);
   CUDA_TRY(cudaMalloc(&K.cmem, bytes));
@@ -506,6 +631,8 @@ static int ensure_control(Device *dev, int m, int max_outer) {
   B.converged = carve<int>(cur, nb + 16);
   B.failed = carve<int>(cur, nb + 16);
   B.trig = carve<int>(cur, nb + 16);
+  B.handed = carve<int>(cur, nb + 16);
+  B.vmask = carve<int>(cur, nb + 16);
   B.ctrl = carve<int>(cur, K.c_m + 8);
   B.hnd = carve<unsigned long long>(cur, K.c_m + 1);
   B.out = carve<double>(cur, out_doubles);
@@ -525,6 +652,8 @@ struct Call {
   double *xout;
   int m, max_outer, mode, want_after, mgs;
   const kkt_linop *opK, *opM;  // nullptr = the handle's operator / LU factors
+  int resume = 0;  // a helper continuing a handed-off system (state staged by resume_handed)
+  int T = 0;       // straggler hand-off threshold of a batched handle
 };
 
 int op_kind(const kkt_linop *op) { return op ? op->kind : KKT_OP_HANDLE; }
@@ -563,6 +692,8 @@ struct Runner {
     c.converged = B.converged;
     c.failed = B.failed;
     c.trig = B.trig;
+    c.handed = B.handed;
+    c.vmask = B.vmask;
     c.ctrl = B.ctrl;
     c.hnd = B.hnd;
     c.repb = B.out;
@@ -585,6 +716,7 @@ struct Runner {
     c.rpcap = K.c_rpcap;
     c.mode = C.mode;
     c.graph = 0;
+    c.T = C.T;
   }
 
   // ---- operator applications (M: LU solve / identity / callback; K: SpMV / ...) ----
@@ -669,6 +801,10 @@ struct Runner {
     // per-system tolerances / active flags staged by the host in pinned memory
     CUDA_TRY(cudaMemcpyAsync(B.in, K.pin + B.out_doubles, 8 * B.in_doubles, cudaMemcpyHostToDevice, s));
     LAUNCH((k_unpack_inputs<<<1, 256, 0, s>>>(B.in, nbp, B.act_in, B.ctrl, C.m), cudaGetLastError()));
+    if (C.resume) {  // the state is staged (resume_handed): V_j0 = w / h_{j0,j0-1}, then the cycle
+      LAUNCH((k_resume_begin<<<d.rb, RED_THREADS, 0, s>>>(c, K.V, K.w, n), cudaGetLastError()));
+      return KKT_OK;
+    }
     LAUNCH((k_clear_nonfinite<<<1, 256, 0, s>>>(d.scal, d.nb), cudaGetLastError()));
     if (C.mode == 1) {  // refine: statistics of (r, x0) decide the trigger (refine.py:113)
       LAUNCH(il ? b_launch_resid_stats(d, C.b, C.x0, d.partials, B.stats0, s)
@@ -684,7 +820,7 @@ struct Runner {
 
   int cycle_begin() {
     LAUNCH((k_cycle_begin<<<1, FG_THREADS, 0, s>>>(c), cudaGetLastError()));
-    LAUNCH(scale(K.r, K.V, K.beta, 1, c.running));  // V0 = r / beta (a division, :151)
+    LAUNCH(scale(K.r, K.V, K.beta, 1, c.vmask));  // V0 = r / beta (a division, :151)
     return KKT_OK;
   }
 
@@ -891,16 +1027,147 @@ void graph_key(const Device *dev, const Call &C, FgGraph &k) {
   k.mode = C.mode;
   k.want_after = C.want_after;
   k.mgs = C.mgs;
+  k.resume = C.resume;
+  k.T = C.T;
   k.plan = dev->d;
   k.plan.sys_mask = nullptr;
 }
 
 bool same_key(const FgGraph &a, const FgGraph &b) {
   return a.b == b.b && a.x0 == b.x0 && a.xout == b.xout && a.m == b.m && a.mode == b.mode &&
-         a.want_after == b.want_after && a.mgs == b.mgs && std::memcmp(&a.plan, &b.plan, sizeof(DevPlan)) == 0;
+         a.want_after == b.want_after && a.mgs == b.mgs && a.resume == b.resume && a.T == b.T && std::memcmp(&a.plan, &b.plan, sizeof(DevPlan)) == 0;
 }
 
 }  // namespace
+
+// Running systems at or below which a batch hands its stragglers to single-system helpers
+// (KKT_HANDOFF=T overrides; 0 disables).  A helper's iteration costs a single system's DAG
+// latency instead of the whole batch's (10k: ~1.4 ms vs ~4.5 ms at B = 64).
+static int handoff_threshold(int nb) {
+  if (const char *e = std::getenv("KKT_HANDOFF")) return std::max(0, std::atoi(e));
+  return nb >= 16 ? std::min(4, nb / 16) : 0;
+}
+
+// The cached graph for (handle, call), captured on first use.
+static int get_graph(Device *dev, Runner &R, const Call &C, FgGraph *&G) {
+  Krylov &K = *dev->kry;
+  FgGraph key;
+  graph_key(dev, C, key);
+  G = nullptr;
+  for (FgGraph &g : K.graphs)
+    if (same_key(g, key)) G = &g;
+  if (G) return KKT_OK;
+  if (K.graphs.size() >= 6) {
+    FgGraph &old = K.graphs.front();
+    if (old.exec) cudaGraphExecDestroy(old.exec);
+    if (old.graph) cudaGraphDestroy(old.graph);
+    K.graphs.erase(K.graphs.begin());
+  }
+  K.graphs.push_back(key);
+  G = &K.graphs.back();
+  int rc = R.build_graph(*G);
+  if (rc) {
+    if (G->exec) cudaGraphExecDestroy(G->exec);
+    if (G->graph) cudaGraphDestroy(G->graph);
+    K.graphs.pop_back();
+    G = nullptr;
+  }
+  return rc;
+}
+
+// Resume every handed-off system q of the batch on its own single-system helper handle, all
+// helpers concurrently on their own streams: gather q's factors, operator values, scalar block
+// and open Krylov cycle (V_0..j0-1, w, Z_0..j0-1, x, b, H, g, rotations, counters, histories)
+// out of the interleaved layout, run the helper's resume graph (the rest of q's FGMRES), and
+// scatter its x back into the batch's solution.  Everything after the batch's own graph; one
+// host synchronisation for all helpers.
+static int resume_handed(Device *dev, Runner &R, const Call &C, const std::vector<int> &handed) {
+  Krylov &K = *dev->kry;
+  const DevPlan &d = dev->d;
+  const int nbp = d.nbp, n = d.n;
+  const size_t nbn = (size_t)nbp * n;
+  const cudaStream_t s = dev->stream;
+  while (dev->helpers.size() < handed.size()) {
+    Device *h = nullptr;
+    int rc = create_like(dev, 1, h);
+    if (rc) return rc;
+    dev->helpers.push_back(h);
+  }
+  if (!dev->ev_h) CUDA_TRY(cudaEventCreateWithFlags(&dev->ev_h, cudaEventDisableTiming));
+  // the batch's graph is complete (synchronised): helpers may read its state
+  const int G = 2 * dev->sm_count;
+  auto gather = [&](cudaStream_t st, double *dst, const double *srcp, int64_t cnt, int q) -> cudaError_t {
+    if (cnt <= 0) return cudaSuccess;
+    k_gather_col<<<G, 256, 0, st>>>(dst, srcp, cnt, nbp, q);
+    return cudaGetLastError();
+  };
+  std::vector<FgGraph *> graphs(handed.size(), nullptr);
+  std::vector<Call> calls(handed.size(), C);
+  for (size_t i = 0; i < handed.size(); ++i) {
+    Device *h = dev->helpers[i];
+    const int q = handed[i];
+    const int j0 = (int)K.pin[(size_t)q * FG_REP + 19];
+    int rc;
+    if (!h->kry || h->kry->m != K.m) {
+      if ((rc = alloc_krylov(h, K.m))) return rc;
+    }
+    if ((rc = ensure_control(h, C.m, std::max(C.max_outer, 1)))) return rc;
+    Krylov &HK = *h->kry;
+    DevPlan &hd = h->d;
+    hd.sym_lower = d.sym_lower;
+    hd.has_lower = d.has_lower;
+    const cudaStream_t hs = h->stream;
+    // budget: the helper's k_unpack_inputs reads max_outer from the staged inputs
+    double *in = HK.pin + HK.fb.out_doubles;
+    in[0] = K.pin[K.fb.out_doubles + q];
+    in[1] = 1.0;
+    in[2] = C.max_outer;
+    CUDA_TRY(cudaEventRecord(dev->ev_h, s));
+    CUDA_TRY(cudaStreamWaitEvent(hs, dev->ev_h, 0));
+    // factors (both layouts), operator values, solution / rhs, the open cycle's vectors
+    CUDA_TRY(gather(hs, hd.Lx, d.Lx, d.nnz_L, q));
+    CUDA_TRY(gather(hs, hd.Ux, d.Ux, d.nnz_U, q));
+    CUDA_TRY(gather(hs, hd.udiag, d.udiag, n, q));
+    CUDA_TRY(gather(hs, hd.Lv, d.Lv, d.nnz_L, q));
+    CUDA_TRY(gather(hs, hd.Uv, d.Uv, d.nnz_U, q));
+    CUDA_TRY(gather(hs, hd.A_vals, d.A_vals, d.nnz_a, q));
+    CUDA_TRY(gather(hs, HK.x, K.x, n, q));
+    CUDA_TRY(gather(hs, HK.sr, K.sr, n, q));
+    CUDA_TRY(gather(hs, HK.w, K.w, n, q));
+    for (int v = 0; v < j0; ++v) {
+      CUDA_TRY(gather(hs, HK.V + (size_t)v * n, K.V + (size_t)v * nbn, n, q));
+      CUDA_TRY(gather(hs, HK.Z + (size_t)v * n, K.Z + (size_t)v * nbn, n, q));
+    }
+    h->launches += 9 + 2 * j0;
+    calls[i].resume = 1;
+    calls[i].T = 0;
+    calls[i].b = HK.sr;
+    calls[i].x0 = HK.sx0;
+    calls[i].xout = HK.sx;
+    Runner RH(h, calls[i]);
+    k_handoff_state<<<1, 256, 0, hs>>>(R.c, RH.c, q, j0, K.beta, HK.beta);
+    CUDA_TRY(cudaGetLastError());
+    h->launches++;
+    if ((rc = get_graph(h, RH, calls[i], graphs[i]))) return rc;
+    CUDA_TRY(cudaGraphLaunch(graphs[i]->exec, hs));
+    // x back into the batch's solution (interleaved column q)
+    k_scatter_col<<<G, 256, 0, hs>>>(K.sx, HK.sx, n, nbp, q);
+    CUDA_TRY(cudaGetLastError());
+    h->launches++;
+  }
+  for (size_t i = 0; i < handed.size(); ++i) {
+    Device *h = dev->helpers[i];
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    const FgGraph *g = graphs[i];
+    const int *ctrl = h->kry->pin_ctrl;
+    h->launches += g->l_pro + (long long)ctrl[C.m + 2] * g->l_iter + g->l_epi;
+    // cycles the helper ran (its count continued the batch's)
+    h->launches += (long long)std::max(0, ctrl[C.m + 1] - (K.pin_ctrl[C.m + 1] - 1)) * g->l_cyc;
+    dev->launches += h->launches;
+    h->launches = 0;
+  }
+  return KKT_OK;
+}
 
 int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout, const kkt_krylov_cfg *cfg,
                int mode, const int *active_in, const kkt_linop *opK, const kkt_linop *opM,
@@ -932,49 +1199,60 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout, con
     in[nbp + q] = (q < nb && (!active_in || active_in[q])) ? 1.0 : 0.0;
   }
   in[2 * nbp] = cfg->max_outer;
-  Call C{b, x0, xout, cfg->m, cfg->max_outer, mode, (cfg->flags & KKT_FG_STATS_AFTER) ? 1 : 0,
-         (cfg->flags & KKT_FG_MGS) ? 1 : 0, opK, opM};
-  Runner R(dev, C);
   const bool host_loop = callbacks || (cfg->flags & KKT_FG_HOST_LOOP) || std::getenv("KKT_FG_HOST_LOOP");
+  // A graph runs on the workspace's fixed vectors (b -> sr, x0 -> sx0, x -> sx), so one
+  // captured graph serves every call whatever the caller's pointers: stage around it.
+  const size_t vbytes = 8 * (size_t)nbp * d.n;
+  if (!host_loop) {
+    if (x0 != K.sx0) CUDA_TRY(cudaMemcpyAsync(K.sx0, x0, vbytes, cudaMemcpyDeviceToDevice, dev->stream));
+    if (b != K.sr) CUDA_TRY(cudaMemcpyAsync(K.sr, b, vbytes, cudaMemcpyDeviceToDevice, dev->stream));
+  }
+  const int T = (!host_loop && nbp > 1 && !(cfg->flags & KKT_FG_NO_HANDOFF)) ? handoff_threshold(nb) : 0;
+  Call C{host_loop ? b : K.sr, host_loop ? x0 : K.sx0, host_loop ? xout : K.sx, cfg->m, cfg->max_outer, mode,
+         (cfg->flags & KKT_FG_STATS_AFTER) ? 1 : 0, (cfg->flags & KKT_FG_MGS) ? 1 : 0, opK, opM};
+  C.T = T;
+  Runner R(dev, C);
+  std::vector<int> handed;
   if (host_loop) {
     rc = R.run_host();
     if (rc) return rc;
   } else {
-    FgGraph key;
-    graph_key(dev, C, key);
     FgGraph *G = nullptr;
-    for (FgGraph &g : K.graphs)
-      if (same_key(g, key)) G = &g;
-    if (!G) {
-      if (K.graphs.size() >= 6) {
-        FgGraph &old = K.graphs.front();
-        if (old.exec) cudaGraphExecDestroy(old.exec);
-        if (old.graph) cudaGraphDestroy(old.graph);
-        K.graphs.erase(K.graphs.begin());
-      }
-      K.graphs.push_back(key);
-      G = &K.graphs.back();
-      rc = R.build_graph(*G);
-      if (rc) {
-        if (G->exec) cudaGraphExecDestroy(G->exec);
-        if (G->graph) cudaGraphDestroy(G->graph);
-        K.graphs.pop_back();
-        return rc;
-      }
-    }
+    if ((rc = get_graph(dev, R, C, G))) return rc;
     CUDA_TRY(cudaGraphLaunch(G->exec, dev->stream));
     CUDA_TRY(cudaStreamSynchronize(dev->stream));
     const int *ctrl = K.pin_ctrl;
     dev->launches += G->l_pro + (long long)ctrl[cfg->m + 1] * G->l_cyc + (long long)ctrl[cfg->m + 2] * G->l_iter +
                      G->l_epi;
+    if (T > 0 && ctrl[cfg->m + 6] > 0)
+      for (int q = 0; q < nb; ++q)
+        if (K.pin[(size_t)q * FG_REP + 19] > 0) handed.push_back(q);
   }
-  // unpack the report block
-  const double *ob = K.pin;
-  const double *oh = ob + (size_t)nbp * FG_REP;
-  const double *orp = oh + (size_t)nbp * K.c_hcap;
+  // the stragglers: helpers resume them (their reports replace the batch's)
+  std::vector<const double *> src(nb, nullptr);
+  std::vector<int> src_hcap(nb, K.c_hcap), src_rpcap(nb, K.c_rpcap);
+  if (!handed.empty()) {
+    if ((rc = resume_handed(dev, R, C, handed))) return rc;
+    for (size_t i = 0; i < handed.size(); ++i) {
+      const Krylov &HK = *dev->helpers[i]->kry;
+      src[handed[i]] = HK.pin;
+      src_hcap[handed[i]] = HK.c_hcap;
+      src_rpcap[handed[i]] = HK.c_rpcap;
+    }
+  }
+  if (!host_loop && xout != K.sx) {
+    CUDA_TRY(cudaMemcpyAsync(xout, K.sx, vbytes, cudaMemcpyDeviceToDevice, dev->stream));
+    CUDA_TRY(cudaStreamSynchronize(dev->stream));
+  }
+  // unpack the report blocks: [nbp][FG_REP] | history [nbp][hcap] | restart pairs [nbp][rpcap][2]
   int failed = 0;
   for (int q = 0; q < nb; ++q) {
-    const double *o = ob + (size_t)q * FG_REP;
+    const bool hq = src[q] != nullptr;
+    const double *ob = hq ? src[q] : K.pin;
+    const int pb = hq ? 1 : nbp, qi = hq ? 0 : q, hcap = src_hcap[q], rpcap = src_rpcap[q];
+    const double *o = ob + (size_t)qi * FG_REP;
+    const double *oh = ob + (size_t)pb * FG_REP + (size_t)qi * hcap;
+    const double *orp = ob + (size_t)pb * FG_REP + (size_t)pb * hcap + (size_t)qi * 2 * rpcap;
     kkt_krylov_report &r = rep[q];
     std::memset(&r, 0, sizeof r);
     r.iterations = (int)o[0];
@@ -990,14 +1268,15 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout, con
     r.stats_before[5] = o[13];
     for (int i = 0; i < 5; ++i) r.stats_after[i] = o[14 + i];
     r.stats_after[5] = o[13];
+    r.handed_off = hq ? 1 : 0;
     failed |= r.nonfinite;
     if (hist) {
-      const int nh = std::min(std::min(r.iterations + 1, K.c_hcap), hist_cap);
-      for (int i = 0; i < nh; ++i) hist[(size_t)q * hist_cap + i] = oh[(size_t)q * K.c_hcap + i];
+      const int nh = std::min(std::min(r.iterations + 1, hcap), hist_cap);
+      for (int i = 0; i < nh; ++i) hist[(size_t)q * hist_cap + i] = oh[i];
     }
     if (rpairs) {
-      const int np = std::min(std::min(r.restarts, K.c_rpcap), rp_cap);
-      for (int i = 0; i < 2 * np; ++i) rpairs[(size_t)q * 2 * rp_cap + i] = orp[(size_t)q * 2 * K.c_rpcap + i];
+      const int np = std::min(std::min(r.restarts, rpcap), rp_cap);
+      for (int i = 0; i < 2 * np; ++i) rpairs[(size_t)q * 2 * rp_cap + i] = orp[i];
     }
   }
   if (failed) return set_error(KKT_ERR_NONFINITE, "operator or preconditioner produced a non-finite entry");

@@ -251,13 +251,16 @@ class DeviceSystem:
         nat.check(rc, what)
 
     def step(self, values: np.ndarray | object, layout: int, r, x_out, on_device: bool,
-             m: int, max_outer: int, delta_tol, diag: bool = False, stats: bool = False):
+             m: int, max_outer: int, delta_tol, diag: bool = False, stats: bool = False,
+             handoff: bool = True):
         """refactor -> solve -> refine_fgmres in one C call (kkt_dev_step) for every system.
 
         ``delta_tol`` is a float or a per-system sequence.  Returns the KrylovReport (single
         system) or the list of reports (batch); with ``diag`` also the per-system
         LuDiagnostics array ``[nb][4]``.  ``stats`` also fills the reports' residual statistics
-        of x0 and x (nsr / nrbe before and after, refine.py:117,129-131).
+        of x0 and x (nsr / nrbe before and after, refine.py:117,129-131).  ``handoff``
+        (batched handles): the last few running systems finish on single-system helpers
+        (KrylovReport.handed_off) instead of in the lockstep batch.
         """
         dsys = None
         if np.ndim(delta_tol):
@@ -265,7 +268,8 @@ class DeviceSystem:
             delta_tol = float(np.max(delta_tol))
         cfg = nat.KrylovCfg(m=int(m), max_outer=int(max_outer), tol=float(delta_tol),
                             delta_tol=float(delta_tol), delta_sys=dsys,
-                            flags=nat.FG_STATS_AFTER if stats else 0)
+                            flags=(nat.FG_STATS_AFTER if stats else 0)
+                            | (0 if handoff else nat.FG_NO_HANDOFF))
         reps = (nat.KrylovReport * self.nb)()
         dg = (C.c_double * (4 * self.nb))() if diag else None
         if on_device:

@@ -62,17 +62,29 @@ def barrier_delta(seq, k: int) -> float:
     return BarrierTiedTolerance()(seq.mu(k))
 
 
-def rr_bound(rr_ref: float, delta: float) -> float:
-    """The residual parity bar: rr <= max(1.5 rr_ref, 4 eps, 1e-3 delta).
+# The reference's own final residual is reproducible only to a factor RR_SPREAD under another
+# summation order: the plain-C oracle (same algorithm, sequential dots instead of OpenBLAS)
+# lands at up to 2.06x the reference's rr on these goldens at EQUAL iteration counts
+# (activsg200p k = 18: 1.87e-14 vs 3.85e-14; profiles/r2_rr_spread.txt, tools/rr_spread.py).
+RR_SPREAD = 2.5
 
-    1.5x: reassociated dot products (tree reductions instead of OpenBLAS ddot) cost up to
-    1.5x rr near the rounding floor (SURVEY.md §7 hard part 5).  1e-3 delta: three orders of
-    magnitude below the refinement tolerance rr is rounding noise of computing r - K x itself
-    (activsg200p k = 18: the reference lands at 1.9e-14, the plain-C oracle at 3.9e-14, both
-    with nrbe ~ 6e-23), so only "at least 1000x below the tolerance" is asserted there.
+
+def rr_bound(rr_ref: float, delta: float, same_iterations: bool = True) -> float:
+    """The residual parity bar.
+
+    Equal iteration counts: rr <= max(RR_SPREAD rr_ref, 4 eps, 1e-3 delta) — the measured
+    reproducibility of the reference's rr under reassociated reductions (SURVEY.md §7 hard
+    part 5), and three orders of magnitude below the refinement tolerance rr is rounding noise
+    of computing r - K x itself.
+    One iteration fewer than the reference (the +-1 allowance): that iteration's gain is
+    not made, so rr is bounded by the stopping rule instead — rr <= delta (the oracle itself
+    stops one iteration early on activsg2000p barrier k = 17 and lands at 89x the reference's
+    rr, 5.98e-11 for delta = 2e-9).
     """
     eps = np.finfo(float).eps
-    return max(1.5 * rr_ref, 4 * eps, 1e-3 * delta)
+    if not same_iterations:
+        return max(RR_SPREAD * rr_ref, delta)
+    return max(RR_SPREAD * rr_ref, 4 * eps, 1e-3 * delta)
 
 
 def check_report(got: dict, ref_row, tag: str, delta: float):
@@ -80,5 +92,6 @@ def check_report(got: dict, ref_row, tag: str, delta: float):
     r = dict(zip(REPORT, ref_row))
     assert bool(got["triggered"]) == bool(r["triggered"]), (tag, got, r)
     assert abs(got["iterations"] - r["ir_iterations"]) <= 1, (tag, got, r)
-    assert got["rr"] <= rr_bound(r["rr_true"], delta), (tag, got, r)
+    same = got["iterations"] >= r["ir_iterations"]
+    assert got["rr"] <= rr_bound(r["rr_true"], delta, same), (tag, got, r)
     assert bool(got["converged"]) == bool(r["converged"]), (tag, got, r)
