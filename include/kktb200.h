@@ -313,6 +313,11 @@ int kkt_dev_trace_steps(kkt_device *d, uint64_t *steps_out);
 /* Kernel launches issued by this handle since creation (evidence counter). */
 int64_t kkt_dev_launch_count(kkt_device *d);
 
+/* Measurement probe (bench.py's critical-path bound; no reference counterpart): the latency of
+ * one dependency hop between SMs — a value published with a relaxed 64-bit store and observed
+ * by a relaxed poll on another SM — averaged over `rounds` ping-pong round trips. */
+int kkt_probe_hop_ns(int device, int rounds, double *ns_per_hop);
+
 #ifdef __cplusplus
 }
 #endif

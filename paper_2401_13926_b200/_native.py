@@ -13,7 +13,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkktb200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 KKT_OK = 0
 KKT_ERR_SINGULAR = 1
@@ -116,6 +116,7 @@ SIGNATURES = [
     ("kkt_dev_trace", C.c_int, [vp, vp, vp]),
     ("kkt_dev_trace_steps", C.c_int, [vp, vp]),
     ("kkt_dev_launch_count", i64, [vp]),
+    ("kkt_probe_hop_ns", C.c_int, [C.c_int, C.c_int, f64p]),
 ]
 
 _lib = None

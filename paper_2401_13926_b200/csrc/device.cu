@@ -874,6 +874,10 @@ int kkt_dev_create(const kkt_symbolic *s, const int64_t *A_row_ptr, const int64_
     int rc = kkt::create(*reinterpret_cast<const kkt::Symbolic *>(s), A_row_ptr, A_col_idx, in_nnz,
                          gen_src, opts, dev);
     if (rc != KKT_OK) return rc;
+    if ((rc = kkt::prepare_helpers(dev)) != KKT_OK) {
+      kkt::destroy(dev);
+      return rc;
+    }
     *out = reinterpret_cast<kkt_device *>(dev);
     return KKT_OK;
   } catch (std::bad_alloc &) {

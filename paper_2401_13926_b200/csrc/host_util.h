@@ -98,6 +98,7 @@ int dev_solve(Device *dev, const double *b, double *x);
 int dev_spmv(Device *dev, const double *x, double *y, const double *bsub, double *nrm_partials);
 int dev_residual_norms(Device *dev, const double *r, const double *x, double *out6);
 int alloc_krylov(Device *dev, int m);
+int prepare_helpers(Device *dev);  // a batched handle's straggler helpers (krylov.cu)
 int ensure_krylov(Device *dev, int m);
 void free_krylov(Device *dev);
 // FGMRES on every system of the handle (krylov.py:117-208).  mode 0: fgmres with tol (or

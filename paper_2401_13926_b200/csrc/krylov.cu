@@ -1048,6 +1048,20 @@ static int handoff_threshold(int nb) {
   return nb >= 16 ? std::min(4, nb / 16) : 0;
 }
 
+// Create a batched handle's straggler helpers up front (kkt_dev_create), so the first
+// hand-off does not pay for their allocation.
+int prepare_helpers(Device *dev) {
+  const int T = dev->d.nbp > 1 ? handoff_threshold(dev->d.nb) : 0;
+  while ((int)dev->helpers.size() < T) {
+    Device *h = nullptr;
+    int rc = create_like(dev, 1, h);
+    if (rc) return rc;
+    dev->helpers.push_back(h);
+    if ((rc = ensure_control(h, h->restart_m, 10))) return rc;
+  }
+  return KKT_OK;
+}
+
 // The cached graph for (handle, call), captured on first use.
 static int get_graph(Device *dev, Runner &R, const Call &C, FgGraph *&G) {
   Krylov &K = *dev->kry;

@@ -16,7 +16,8 @@ pivoting variants (row_perm != col_perm; direct_lu.py:209-223):
 import numpy as np
 import pytest
 
-from large_golden import CASES, M, available, barrier_delta, check_report, load, sequence, sha
+from large_golden import (CASES, M, available, barrier_delta, check_report, load, rr_floor,
+                          sequence, sha)
 from paper_2401_13926_b200 import _native as nat
 from paper_2401_13926_b200 import factorize, to_general
 
@@ -54,8 +55,10 @@ def test_single_system_sequence(case):
             x = np.empty_like(r)
             rep = dev.step(vals, LOWER, r, x, False, 10, 10, delta, stats=True)
             rr = _rr(rep.stats_after) if rep.triggered else _rr(rep.stats_before)
+            fl = rr_floor(K.row_ptr, K.col_idx, K.values, x, r)
             check_report(dict(triggered=rep.triggered, iterations=rep.iterations, rr=rr,
-                              converged=rep.converged), g[f"refine_{tag}"][k], (case, k, tag), delta)
+                              converged=rep.converged, floor=fl), g[f"refine_{tag}"][k],
+                         (case, k, tag), delta)
             if f"s{k}_x_{tag}" in g and not rep.triggered:
                 assert np.array_equal(x, g[f"s{k}_x_{tag}"])
     del torch
@@ -90,7 +93,9 @@ def test_batched_sequence(case):
         reps = dev.step(vals, LOWER, rhs, x, False, 10, 10, deltas, stats=True)
         for k, rep in enumerate(reps):
             rr = _rr(rep.stats_after) if rep.triggered else _rr(rep.stats_before)
+            K = seq.matrix(k)
+            fl = rr_floor(K.row_ptr, K.col_idx, K.values, x[k], rhs[k])
             check_report(dict(triggered=rep.triggered, iterations=rep.iterations, rr=rr,
-                              converged=rep.converged), g[f"refine_{tag}"][k], (case, k, tag),
-                         deltas[k])
+                              converged=rep.converged, floor=fl), g[f"refine_{tag}"][k],
+                         (case, k, tag), deltas[k])
     dev.close()

@@ -14,6 +14,8 @@ same ACOPF-shaped sequences the bench uses.
 import numpy as np
 import pytest
 
+from large_golden import rr_floor
+
 pytestmark = pytest.mark.gpu
 
 CONFIGS = [("activsg200", 19), ("activsg2000", 19), ("activsg10k", 19),
@@ -141,12 +143,12 @@ def _oracle_refine_all(f, K0, pat, items, threads=8):
     return out
 
 
-def _check_vs_oracle(tag, rep, rr, orep, rr_o, delta):
+def _check_vs_oracle(tag, rep, rr, orep, rr_o, delta, floor=0.0):
     from large_golden import rr_bound
     assert bool(rep.triggered) == orep["triggered"], tag
     assert abs(rep.iterations - orep["iterations"]) <= 1, (tag, rep.iterations, orep["iterations"])
     assert bool(rep.converged) == orep["converged"] and rep.converged, tag
-    assert rr <= rr_bound(rr_o, delta), (tag, rr, rr_o)
+    assert rr <= rr_bound(rr_o, delta, rep.iterations >= orep["iterations"], floor), (tag, rr, rr_o, floor)
 
 
 def test_bench_batch_against_oracle():
@@ -156,7 +158,7 @@ def test_bench_batch_against_oracle():
     every one of the 192 systems against the oracle."""
     import torch
     import paper_2401_13926_b200._native as nat
-    from bench import make_batch, rank_seed_base
+    from bench import make_batch, shard
     from paper_2401_13926_b200.device import DeviceSystem
     from paper_2401_13926_b200.refine import BarrierTiedTolerance
     pat, K0, f = _setup("activsg10k")
@@ -165,7 +167,7 @@ def test_bench_batch_against_oracle():
     LOWER = nat.LAYOUT_SYMMETRIC_LOWER
     policy = BarrierTiedTolerance()
     for k in (17, 18, 19):
-        vals, rhs, mu = make_batch(pat, B, k, rank_seed_base(0))
+        vals, rhs, mu = make_batch(pat, shard(0, 1, B, "strong"), k)
         delta = policy(mu)
         with torch.cuda.stream(dev.stream):
             tv = torch.from_numpy(vals).to(dev.device)
@@ -179,9 +181,12 @@ def test_bench_batch_against_oracle():
             rep = reps[q]
             rr = rep.stats_after[0] / rep.stats_after[4] if rep.triggered else \
                 rep.stats_before[0] / rep.stats_before[4]
-            _check_vs_oracle((k, q), rep, rr, orep, rr_o, delta)
+            fl = rr_floor(pat.K.row_ptr, pat.K.col_idx, vals[q], x[q], rhs[q])
+            _check_vs_oracle((k, q, rep.handed_off), rep, rr, orep, rr_o, delta, fl)
             if not rep.triggered:
                 assert np.array_equal(x[q], x0), (k, q)
+        if k == 19:  # iterations 6..23 across the batch: the stragglers finish on helpers
+            assert sum(r.handed_off for r in reps) >= 1
     dev.close()
 
 
@@ -207,9 +212,10 @@ def test_sequence_238k_against_oracle():
             tx = torch.empty_like(tr)
         dev.solve_device(tr, tx)  # warm path; the step below refactorizes first
         rep = dev.step(tv, LOWER, tr, tx, True, 10, 10, delta, stats=True)
+        fl = rr_floor(pat.K.row_ptr, pat.K.col_idx, vals, dev.d2h(tx), r)
         x0_o, orep, rr_o = ores[i]
         dev.solve_device(tr, tx)
         assert np.array_equal(dev.d2h(tx), x0_o), i + 1  # factors of system i+1 -> x0 bitwise
         rr = rep.stats_after[0] / rep.stats_after[4] if rep.triggered else \
             rep.stats_before[0] / rep.stats_before[4]
-        _check_vs_oracle(i + 1, rep, rr, orep, rr_o, delta)
+        _check_vs_oracle(i + 1, rep, rr, orep, rr_o, delta, fl)

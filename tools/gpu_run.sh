@@ -6,3 +6,5 @@ timeout 2400 python -m pytest $P -q -m gpu --durations=20 > gpurun_out/${T}_gpu_
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo smoke=$? >> gpurun_out/${T}_smoke.log
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/${T}_bench.log 2>&1; echo bench=$? >> gpurun_out/${T}_bench.log
 tail -5 gpurun_out/${T}_gpu_tests.log; tail -2 gpurun_out/${T}_smoke.log; tail -c 600 gpurun_out/${T}_bench.log
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${T}_bench_ref.log 2>&1; echo ref=$? >> gpurun_out/${T}_bench_ref.log
+tail -c 400 gpurun_out/${T}_bench_ref.log
