@@ -1158,8 +1158,12 @@ __global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__
     if (amask) {
       const bool tr = d.trace_step && sys == 0;  // timeline of system 0: {start, crit ready}
       if (tr) d.trace_step[2 * ((IS_U ? d.n : 0) + t.r)] = globaltimer();
-      // one lane waits (back-off) on the critical dependency of one system
-      if (t.cr >= 0 && lane == 31 - __clz(amask)) wait_value_bo(&ysrc[IL(d, t.cr, sys)], d.poll_ns);
+      // grid_wait 1: one lane waits (back-off) on the critical dependency of one system
+      // before the row.  Default 0: no up-front wait — the chunks are summed in order as their
+      // values arrive (each lane re-polls its own system's unpublished y, one 256-byte line
+      // per warp), so the row's chunks before the critical column run while it is in flight.
+      if (d.grid_wait && t.cr >= 0 && lane == 31 - __clz(amask))
+        wait_value_bo(&ysrc[IL(d, t.cr, sys)], d.poll_ns);
       __syncwarp();
       if (tr) d.trace_step[2 * ((IS_U ? d.n : 0) + t.r) + 1] = globaltimer();
       if (act) {  // per lane from here: systems are independent

@@ -332,6 +332,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   for (int l = 0; l <= h.n_small_levels; ++l) d.lev_ptr[l] = h.small_lev_ptr[l];
   d.ref_start = h.small_lev_ptr[h.n_small_levels];
   d.poll_ns = std::getenv("KKT_POLL_NS") ? std::atoi(std::getenv("KKT_POLL_NS")) : (nbp > 1 ? 64 : 0);
+  d.grid_wait = std::getenv("KKT_GRID_WAIT") ? std::atoi(std::getenv("KKT_GRID_WAIT")) : 0;
   d.pL = h.pL;
   d.pU = h.pU;
   d.nLg = (int)h.L_grid_order.size();
@@ -648,6 +649,8 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   int tb = 0;
   CUDA_TRY(trsv_configure(&tb));
   dev->trsv_blocks = std::max(1, tb) * dev->sm_count;
+  if (const char *e = std::getenv("KKT_TRSV_BLOCKS")) dev->trsv_blocks = std::max(1, std::atoi(e));
+  dev->trsv_blocks_full = dev->trsv_blocks;
   dev->pinned_bytes = 64 * 1024;
   CUDA_TRY(cudaMallocHost(&dev->pinned, dev->pinned_bytes));
   rc = alloc_krylov(dev, dev->restart_m);

@@ -76,6 +76,7 @@ struct DevPlan {
   int n_small_levels = 0;  // leading levels run by k_refactor_small
   int lev_ptr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // col_order offsets of those levels
   int poll_ns = 0;  // __nanosleep back-off while polling (env KKT_POLL_NS)
+  int grid_wait = 0;  // sync-free grid solves: 1 = wait on a row's critical dependency first
   // operator (pattern shared; values per system)
   int *A_rp, *A_ci, *A_split, *gen_src;
   double *in_vals, *A_vals;                 // [nb][in_cap], [nb][nnz_a]
@@ -152,6 +153,7 @@ struct Device {
   size_t refactor_smem2 = 0;
   size_t refactor_smem = 0;
   int trsv_blocks = 0;
+  int trsv_blocks_full = 0;  // the grid solve's full-GPU persistent grid (helpers may use less)
   long long launches = 0;
   Krylov *kry = nullptr;
   double *pinned = nullptr;  // pinned host staging (status words)

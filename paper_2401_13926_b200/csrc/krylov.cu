@@ -1108,6 +1108,11 @@ static int resume_handed(Device *dev, Runner &R, const Call &C, const std::vecto
     dev->helpers.push_back(h);
   }
   if (!dev->ev_h) CUDA_TRY(cudaEventCreateWithFlags(&dev->ev_h, cudaEventDisableTiming));
+  // Sequential by default: every helper runs on the batch's stream, one after the other.  The
+  // single-system grid solve is a persistent sync-free kernel sized to fill the GPU, so two of
+  // them side by side are not guaranteed co-resident (KKT_HANDOFF_CONCURRENT=1 runs the helpers
+  // on their own streams with their grids cut to a 1/T share of the GPU each).
+  const bool concurrent = std::getenv("KKT_HANDOFF_CONCURRENT") && std::atoi(std::getenv("KKT_HANDOFF_CONCURRENT"));
   // the batch's graph is complete (synchronised): helpers may read its state
   const int G = 2 * dev->sm_count;
   auto gather = [&](cudaStream_t st, double *dst, const double *srcp, int64_t cnt, int q) -> cudaError_t {
@@ -1130,14 +1135,18 @@ static int resume_handed(Device *dev, Runner &R, const Call &C, const std::vecto
     DevPlan &hd = h->d;
     hd.sym_lower = d.sym_lower;
     hd.has_lower = d.has_lower;
-    const cudaStream_t hs = h->stream;
+    const cudaStream_t hs = concurrent ? h->stream : s;
+    if (concurrent) h->trsv_blocks = std::max(dev->sm_count, h->trsv_blocks_full / (int)dev->helpers.size());
+    else h->trsv_blocks = h->trsv_blocks_full;
     // budget: the helper's k_unpack_inputs reads max_outer from the staged inputs
     double *in = HK.pin + HK.fb.out_doubles;
     in[0] = K.pin[K.fb.out_doubles + q];
     in[1] = 1.0;
     in[2] = C.max_outer;
-    CUDA_TRY(cudaEventRecord(dev->ev_h, s));
-    CUDA_TRY(cudaStreamWaitEvent(hs, dev->ev_h, 0));
+    if (concurrent) {
+      CUDA_TRY(cudaEventRecord(dev->ev_h, s));
+      CUDA_TRY(cudaStreamWaitEvent(hs, dev->ev_h, 0));
+    }
     // factors (both layouts), operator values, solution / rhs, the open cycle's vectors
     CUDA_TRY(gather(hs, hd.Lx, d.Lx, d.nnz_L, q));
     CUDA_TRY(gather(hs, hd.Ux, d.Ux, d.nnz_U, q));
@@ -1171,7 +1180,7 @@ static int resume_handed(Device *dev, Runner &R, const Call &C, const std::vecto
   }
   for (size_t i = 0; i < handed.size(); ++i) {
     Device *h = dev->helpers[i];
-    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    CUDA_TRY(cudaStreamSynchronize(concurrent ? h->stream : s));
     const FgGraph *g = graphs[i];
     const int *ctrl = h->kry->pin_ctrl;
     h->launches += g->l_pro + (long long)ctrl[C.m + 2] * g->l_iter + g->l_epi;
