@@ -43,6 +43,13 @@ ACOPF_CONFIGS = {
 }
 
 
+# Per-shape calibration of the D_x spread (active x = mu^d_exp * U(.5, 2)), checked with the
+# oracle (tools/calibrate.py, SURVEY.md §8d gates).  0.8 everywhere except ACTIVSg70k, where
+# 0.8 drives the last barrier step to 49-51 FGMRES iterations; 0.7 keeps k = 17..19 at 2
+# (delta = 1e-10 triggers on 8/19 systems, 2 iterations each; profiles/r2_calibration_70k.txt).
+ACOPF_D_EXP = {141600: 0.7}
+
+
 @dataclass
 class AcopfPattern:
     """Frozen structure of one ACOPF-shaped KKT family."""
@@ -204,6 +211,7 @@ def build_pattern(nbus: int, seed: int = 0, gen_frac: float = 0.25,
     pat = AcopfPattern(nbus=nbus, n=n, m=m, K=K, pos=pos, kind=kind,
                        var_of_diag=var_of_diag, base=raw,
                        meta=dict(nbus=nbus, lines=L, gens=G, imbalance=S, seed=seed,
+                                 d_exp=ACOPF_D_EXP.get(nbus, 0.8),
                                  vclass=vclass))
     K.values = system_values(pat, 0, seed)
     return pat
@@ -218,7 +226,7 @@ MU_STEP = 0.4  # mu_k = 10**(-MU_STEP*k): calibrated so IR triggers on ~1/3 of t
 
 
 def system_values(pat: AcopfPattern, k: int, seed: int = 0, mu_step: float = MU_STEP,
-                  d_exp: float = 0.8, active_prob=ACTIVE_PROB) -> np.ndarray:
+                  d_exp: float | None = None, active_prob=ACTIVE_PROB) -> np.ndarray:
     """Lower-triangle values of system ``k`` (mu_k = 10**(-mu_step*k))."""
     n = pat.n
     if k == 0:
@@ -231,6 +239,8 @@ def system_values(pat: AcopfPattern, k: int, seed: int = 0, mu_step: float = MU_
         vclass = pat.meta["vclass"]
         prob = np.asarray(active_prob)[vclass]
         active = np.random.default_rng([seed, 104729]).random(n) < prob
+        if d_exp is None:  # the pattern's calibration (ACOPF_D_EXP), else 0.8
+            d_exp = pat.meta.get("d_exp", 0.8)
         sm = mu ** d_exp
         x = np.where(active, sm * rng.uniform(0.5, 2.0, n), rng.uniform(0.5, 2.0, n))
         z = np.where(active, rng.uniform(0.5, 2.0, n), sm * rng.uniform(0.5, 2.0, n))

@@ -65,13 +65,9 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
       v = vals[beg + lane];
     }
     // lane 0 alone spins on the critical dependency; the other dependencies are then
-    // normally published already, so the lanes' loads below rarely have to wait.  The wait
-    // sits at the chunk holding that column (grid_wait 0): the row's earlier chunks — in the
-    // reference's order, so still bitwise — are summed while the dependency is in flight, and
-    // only the chunks from it on stay on the critical path (a long separator row's ~8 chunk
-    // round trips shrink to ~1).  grid_wait 1: wait before the row (KKT_GRID_WAIT=1).
+    // normally published already, so the lanes' loads below rarely have to wait
     const int cr = crit[idx];
-    if (d.grid_wait && lane == 0 && cr >= 0) wait_value(&ysrc[cr], d.poll_ns);
+    if (lane == 0 && cr >= 0) wait_value(&ysrc[cr], d.poll_ns);
     __syncwarp();
     for (int c0 = beg; c0 < end; c0 += 32) {
       const int cnt = min(32, end - c0);
@@ -81,11 +77,6 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
       if (c0 + 32 + lane < end) {
         ncol = ci[c0 + 32 + lane];
         nv = vals[c0 + 32 + lane];
-      }
-      if (!d.grid_wait && cr >= 0) {
-        const unsigned hit = __ballot_sync(0xffffffffu, lane < cnt && col == cr);
-        if (hit && lane == __ffs(hit) - 1) wait_value(&ysrc[cr], d.poll_ns);
-        __syncwarp();
       }
       if (lane < cnt) p = __dmul_rn(v, wait_value(&ysrc[col], d.poll_ns));
       for (int i = 0; i < cnt; ++i) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, p, i));

@@ -119,7 +119,7 @@ class LuFactors:
 
     def device(self, restart_m: int = 10):
         """The device-resident system for these factors (created on first use)."""
-        if self._dev is None:
+        if self._dev is None or self._dev.h is None:  # (a closed handle is replaced)
             from .device import DeviceSystem
             self._dev = DeviceSystem(self, restart_m=restart_m)
             if self.from_refactorization and self._host_vals is not None:

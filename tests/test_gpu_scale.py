@@ -19,7 +19,7 @@ from large_golden import rr_floor
 pytestmark = pytest.mark.gpu
 
 CONFIGS = [("activsg200", 19), ("activsg2000", 19), ("activsg10k", 19),
-           pytest.param("activsg70k", 12, marks=pytest.mark.slow)]
+           pytest.param("activsg70k", 19, marks=pytest.mark.slow)]
 
 
 def _setup(config):
@@ -93,8 +93,6 @@ def test_full_size_batch_equals_single(config, nb):
     from paper_2401_13926_b200.device import DeviceSystem
     pat, K0, f = _setup(config)
     ks = [3, 11, 17, 19] if nb == 4 else [1 + (7 * q) % 19 for q in range(nb)]
-    if config == "activsg70k":
-        ks = [min(k, 12) for k in ks]  # the calibrated range at 70k (CONFIGS above)
     vals = np.stack([system_values(pat, k, q % 4) for q, k in enumerate(ks)])
     rhs = np.stack([system_rhs(pat, k, q % 4) for q, k in enumerate(ks)])
     LOWER = nat.LAYOUT_SYMMETRIC_LOWER

@@ -37,11 +37,12 @@ for B in Bs:
         tx = torch.empty_like(tr)
     s.synchronize()
 
-    def timed(fn):
+    def timed(fn, cold=True):
         ts = []
         for _ in range(reps):
-            with torch.cuda.stream(s):
-                flush.fill_(1.0)
+            if cold:
+                with torch.cuda.stream(s):
+                    flush.fill_(1.0)
             a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(s)
             fn()
@@ -54,6 +55,19 @@ for B in Bs:
     out = {"config": cfg, "B": B, "env": {k: v for k, v in os.environ.items() if k.startswith("KKT_")},
            "refactor_ms": timed(ref), "solve_ms": timed(lambda: dev.solve_device(tr, tx)),
            "spmv_ms": timed(lambda: dev.spmv_device(tr, tx))}
+    out["solve_warm_ms"] = timed(lambda: dev.solve_device(tr, tx), cold=False)
+    out["refactor_then_solve_ms"] = timed(lambda: (ref(), dev.solve_device(tr, tx)))
+    if B == 1:
+        from paper_2401_13926_b200.acopf import MU_STEP
+        from paper_2401_13926_b200.refine import BarrierTiedTolerance
+        for k in (1, 19):
+            with torch.cuda.stream(s):
+                vk = torch.from_numpy(system_values(pat, k, 0)).to(dev.device)
+                rk = torch.from_numpy(system_rhs(pat, k, 0)).to(dev.device)
+            d = BarrierTiedTolerance()(10.0 ** (-MU_STEP * k))
+            it = []
+            out[f"step_k{k}_ms"] = timed(lambda: it.append(dev.step(vk, LOWER, rk, tx, True, 10, 10, d).iterations))
+            out[f"step_k{k}_iters"] = it[-1]
     out["refactor_per_sys"] = round(out["refactor_ms"] / B, 4)
     out["solve_per_sys"] = round(out["solve_ms"] / B, 4)
     print(json.dumps(out), flush=True)
