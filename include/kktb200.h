@@ -313,6 +313,12 @@ int kkt_dev_trace_steps(kkt_device *d, uint64_t *steps_out);
 /* Kernel launches issued by this handle since creation (evidence counter). */
 int64_t kkt_dev_launch_count(kkt_device *d);
 
+/* kkt_dev_solve / kkt_dev_spmv on vectors in the handle's INTERNAL layout (batched handles:
+ * [n][nbp] interleaved, nbp = batch rounded up to 32; single: [n]) — the kernels without the
+ * boundary transposes, for per-kernel timing (bench.py roofline). */
+int kkt_dev_solve_native(kkt_device *d, const double *b_dev, double *x_dev);
+int kkt_dev_spmv_native(kkt_device *d, const double *x_dev, double *y_dev);
+
 /* Measurement probe (bench.py's critical-path bound; no reference counterpart): the latency of
  * one dependency hop between SMs — a value published with a relaxed 64-bit store and observed
  * by a relaxed poll on another SM — averaged over `rounds` ping-pong round trips. */

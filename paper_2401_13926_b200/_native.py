@@ -117,6 +117,8 @@ SIGNATURES = [
     ("kkt_dev_trace_steps", C.c_int, [vp, vp]),
     ("kkt_dev_launch_count", i64, [vp]),
     ("kkt_probe_hop_ns", C.c_int, [C.c_int, C.c_int, f64p]),
+    ("kkt_dev_solve_native", C.c_int, [vp, vp, vp]),
+    ("kkt_dev_spmv_native", C.c_int, [vp, vp, vp]),
 ]
 
 _lib = None

@@ -62,24 +62,61 @@ __device__ __forceinline__ double patch_floor_b(const DevPlan &d, int sys) {
 // Values: interleaved caller values [in_nnz][nbp] (general or symmetric-lower) -> A_vals [nnz_a][nbp],
 // plus per-system max|a|, ||A||_inf (general) and the operator norm (entry-order sums).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_b_expand_norms(DevPlan d) {
+// One warp per tile of 32 rows (lanes = systems), the tile's entries walked flat with
+// EXP_T gathers per lane in flight (the next round's source indices prefetched); row sums of
+// |a| in entry order (the reference's bincount order), so the norms are bitwise the per-row
+// loop's.
+constexpr int EXP_T = 8;
+__global__ void __launch_bounds__(256, 3) k_b_expand_norms(DevPlan d) {
   __shared__ double sh[BY][32];
   const int lane = threadIdx.x, sys = blockIdx.y * 32 + lane;
-  const double *in = d.in_il;  // [in_nnz][nbp] (b_launch_transpose of the caller's values)
+  const double *__restrict__ in = d.in_il;  // [in_nnz][nbp] (b_launch_transpose of the caller's values)
+  const int *__restrict__ gs = d.gen_src;
+  const bool sym = d.sym_lower;
   double mx = 0.0, sg = 0.0, op = 0.0;
-  for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
-    const int rb = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
+  const int ntile = (d.n + 31) >> 5;
+  for (int t = blockIdx.x * BY + threadIdx.y; t < ntile; t += gridDim.x * BY) {
+    const int r0 = t << 5, nr = min(d.n, r0 + 32) - r0;
+    const int my_end = lane < nr ? d.A_rp[r0 + lane + 1] : 0;
+    const int my_split = lane < nr ? d.A_split[r0 + lane] : 0;
+    const int e_end = __shfl_sync(FULL, my_end, nr - 1);
+    int e = d.A_rp[r0], row = 0;
+    int rend = __shfl_sync(FULL, my_end, 0), rsplit = __shfl_sync(FULL, my_split, 0);
     double g = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int p = rb; p < e; ++p) {
-      const double v = in[IL(d, d.sym_lower ? d.gen_src[p] : p, sys)];
-      d.A_vals[IL(d, p, sys)] = v;
-      const double a = fabs(v);
-      g = __dadd_rn(g, a);
-      if (p < s) s1 = __dadd_rn(s1, a); else s2 = __dadd_rn(s2, a);
-      mx = fmax(mx, a);
+    int sn[EXP_T];
+#pragma unroll
+    for (int u = 0; u < EXP_T; ++u) sn[u] = e + u < e_end ? (sym ? gs[e + u] : e + u) : 0;
+    while (e < e_end) {
+      double v[EXP_T];
+#pragma unroll
+      for (int u = 0; u < EXP_T; ++u)
+        if (e + u < e_end) v[u] = in[IL(d, sn[u], sys)];
+#pragma unroll
+      for (int u = 0; u < EXP_T; ++u)
+        sn[u] = e + EXP_T + u < e_end ? (sym ? gs[e + EXP_T + u] : e + EXP_T + u) : 0;
+#pragma unroll
+      for (int u = 0; u < EXP_T; ++u) {
+        const int p = e + u;
+        if (p < e_end) {
+          d.A_vals[IL(d, p, sys)] = v[u];
+          while (p >= rend) {
+            sg = fmax(sg, g);
+            op = fmax(op, sym ? __dadd_rn(s1, s2) : g);
+            g = s1 = s2 = 0.0;
+            ++row;
+            rend = __shfl_sync(FULL, my_end, row);
+            rsplit = __shfl_sync(FULL, my_split, row);
+          }
+          const double a = fabs(v[u]);
+          g = __dadd_rn(g, a);
+          if (p < rsplit) s1 = __dadd_rn(s1, a); else s2 = __dadd_rn(s2, a);
+          mx = fmax(mx, a);
+        }
+      }
+      e += EXP_T;
     }
-    sg = fmax(sg, g);
-    op = fmax(op, d.sym_lower ? __dadd_rn(s1, s2) : g);
+    sg = fmax(sg, g);  // the last row with entries (the empty rows after it add 0)
+    op = fmax(op, sym ? __dadd_rn(s1, s2) : g);
   }
   mx = reduce_y<true>(mx, sh);
   sg = reduce_y<true>(sg, sh);
@@ -1341,58 +1378,88 @@ cudaError_t b_launch_trsv(const DevPlan &d, const double *b, double *x, int grid
 // ----------------------------------------------------------------------------
 // SpMV and residual statistics (sparsecore.spmv order; refine.py:62-92)
 // ----------------------------------------------------------------------------
-// Row i of K x for one system (lane), in the reference's order.  The row's products are
-// formed from loads issued SPMV_U entries at a time (all independent), then summed in order
-// (4: 48 registers; 8 measured 0.49 vs 0.36 ms at 10k x 64, 2 0.40 ms).
-constexpr int SPMV_U = 4;
-__device__ __forceinline__ double row_dot_b(const DevPlan &d, const double *__restrict__ x, int i,
-                                            int sys) {
-  const int b = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
-  const double *__restrict__ av = d.A_vals;
+// Rows [r0, r1) (r1 - r0 <= 32) of K x for one system per lane, as one flat walk over the
+// tile's entries: SPMV_T entries per round (their value and x loads all in flight, the next
+// round's column indices prefetched), each product added to its row's sum in entry order —
+// the reference's bincount order (sparsecore.py:296-302), so every row is bitwise the
+// per-row kernel's.  A row ends -> emit(row, value).  Row pointers / split points of the tile
+// sit in lane registers (lane l: row r0 + l) and are read by shuffle at row boundaries.
+template <int SPMV_T, typename Emit>
+__device__ __forceinline__ void spmv_tile(const DevPlan &d, const double *__restrict__ x, int r0, int r1,
+                                          int sys, int lane, Emit emit) {
   const int *__restrict__ ci = d.A_ci;
+  const double *__restrict__ av = d.A_vals;
+  const int nr = r1 - r0;
+  const int my_end = lane < nr ? d.A_rp[r0 + lane + 1] : 0;   // end of row r0 + lane
+  const int my_split = lane < nr ? d.A_split[r0 + lane] : 0;
+  const int e_end = __shfl_sync(FULL, my_end, nr - 1);
+  int e = d.A_rp[r0];
+  int row = 0;
+  int rend = __shfl_sync(FULL, my_end, 0), rsplit = __shfl_sync(FULL, my_split, 0);
   double s1 = 0.0, s2 = 0.0;
-  for (int p0 = b; p0 < e; p0 += SPMV_U) {
-    int c[SPMV_U];
-    double v[SPMV_U], xv[SPMV_U];
+  int cn[SPMV_T];
 #pragma unroll
-    for (int u = 0; u < SPMV_U; ++u)
-      if (p0 + u < e) {
-        c[u] = ci[p0 + u];
-        v[u] = av[IL(d, p0 + u, sys)];
-      }
+  for (int u = 0; u < SPMV_T; ++u) cn[u] = e + u < e_end ? ci[e + u] : 0;
+  while (e < e_end) {
+    int c[SPMV_T];
+    double v[SPMV_T], xv[SPMV_T];
 #pragma unroll
-    for (int u = 0; u < SPMV_U; ++u)
-      if (p0 + u < e) xv[u] = x[IL(d, c[u], sys)];
+    for (int u = 0; u < SPMV_T; ++u) {
+      c[u] = cn[u];
+      if (e + u < e_end) v[u] = av[IL(d, e + u, sys)];
+    }
 #pragma unroll
-    for (int u = 0; u < SPMV_U; ++u)
-      if (p0 + u < e) {
+    for (int u = 0; u < SPMV_T; ++u)
+      if (e + u < e_end) xv[u] = x[IL(d, c[u], sys)];
+#pragma unroll
+    for (int u = 0; u < SPMV_T; ++u) cn[u] = e + SPMV_T + u < e_end ? ci[e + SPMV_T + u] : 0;
+#pragma unroll
+    for (int u = 0; u < SPMV_T; ++u) {
+      const int p = e + u;
+      if (p < e_end) {
+        while (p >= rend) {  // rows ending before entry p (empty rows included)
+          emit(r0 + row, d.sym_lower ? __dadd_rn(s1, s2) : s1);
+          s1 = s2 = 0.0;
+          ++row;
+          rend = __shfl_sync(FULL, my_end, row);
+          rsplit = __shfl_sync(FULL, my_split, row);
+        }
         const double t = __dmul_rn(v[u], xv[u]);
-        // symmetric-lower operators sum the stored and the mirrored halves apart
-        // (sparsecore.py:296-302); general ones in one pass
-        if (d.sym_lower && p0 + u >= s) s2 = __dadd_rn(s2, t);
+        if (d.sym_lower && p >= rsplit) s2 = __dadd_rn(s2, t);
         else s1 = __dadd_rn(s1, t);
       }
+    }
+    e += SPMV_T;
   }
-  return d.sym_lower ? __dadd_rn(s1, s2) : s1;
+  for (; row < nr; ++row) {  // the last row with entries, then trailing empty rows
+    emit(r0 + row, d.sym_lower ? __dadd_rn(s1, s2) : s1);
+    s1 = s2 = 0.0;
+  }
 }
 
-__global__ void __launch_bounds__(256) k_b_spmv(DevPlan d, const double *__restrict__ x,
+template <int T>
+__global__ void __launch_bounds__(256, 3) k_b_spmv(DevPlan d, const double *__restrict__ x,
                                                 double *__restrict__ out,
                                                 const double *__restrict__ bsub,
                                                 double *__restrict__ nrm_out) {
   __shared__ double sh[BY][32];
-  const int sys = blockIdx.y * 32 + threadIdx.x;
+  const int lane = threadIdx.x;
+  const int sys = blockIdx.y * 32 + lane;
   const bool act = sys_active(d, sys);
   if (!__syncthreads_or(act)) return;
   double loc = 0.0;
   bool bad = false;
-  if (act) {
-    for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
-      const double y = row_dot_b(d, x, i, sys);
-      if (!isfinite(y)) bad = true;
-      const double o = bsub ? __dsub_rn(bsub[IL(d, i, sys)], y) : y;
-      out[IL(d, i, sys)] = o;
-      loc = __dadd_rn(loc, __dmul_rn(o, o));
+  if (__any_sync(FULL, act)) {
+    const int ntile = (d.n + 31) >> 5;
+    for (int t = blockIdx.x * BY + threadIdx.y; t < ntile; t += gridDim.x * BY) {
+      const int r0 = t << 5, r1 = min(d.n, r0 + 32);
+      spmv_tile<T>(d, x, r0, r1, sys, lane, [&](int i, double y) {
+        if (!act) return;
+        if (!isfinite(y)) bad = true;
+        const double o = bsub ? __dsub_rn(bsub[IL(d, i, sys)], y) : y;
+        out[IL(d, i, sys)] = o;
+        loc = __dadd_rn(loc, __dmul_rn(o, o));
+      });
     }
   }
   if (bad) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
@@ -1402,20 +1469,26 @@ __global__ void __launch_bounds__(256) k_b_spmv(DevPlan d, const double *__restr
   }
 }
 
-__global__ void __launch_bounds__(256) k_b_resid_stats(DevPlan d, const double *__restrict__ r,
+template <int T>
+__global__ void __launch_bounds__(256, 3) k_b_resid_stats(DevPlan d, const double *__restrict__ r,
                                                        const double *__restrict__ x,
                                                        double *__restrict__ partials) {
   __shared__ double sh[BY][32];
-  const int sys = blockIdx.y * 32 + threadIdx.x, nblk = gridDim.x;
+  const int lane = threadIdx.x;
+  const int sys = blockIdx.y * 32 + lane, nblk = gridDim.x;
   double e2 = 0.0, emax = 0.0, x2 = 0.0, xmax = 0.0, r2 = 0.0;
-  for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
-    const double ri = r[IL(d, i, sys)], xi = x[IL(d, i, sys)];
-    const double ei = __dsub_rn(ri, row_dot_b(d, x, i, sys));
-    e2 += ei * ei;
-    emax = fmax(emax, fabs(ei));
-    x2 += xi * xi;
-    xmax = fmax(xmax, fabs(xi));
-    r2 += ri * ri;
+  const int ntile = (d.n + 31) >> 5;
+  for (int t = blockIdx.x * BY + threadIdx.y; t < ntile; t += gridDim.x * BY) {
+    const int r0 = t << 5, r1 = min(d.n, r0 + 32);
+    spmv_tile<T>(d, x, r0, r1, sys, lane, [&](int i, double y) {
+      const double ri = r[IL(d, i, sys)], xi = x[IL(d, i, sys)];
+      const double ei = __dsub_rn(ri, y);
+      e2 += ei * ei;
+      emax = fmax(emax, fabs(ei));
+      x2 += xi * xi;
+      xmax = fmax(xmax, fabs(xi));
+      r2 += ri * ri;
+    });
   }
   double *part = partials + (size_t)sys * 5 * nblk;
   e2 = reduce_y<false>(e2, sh);
@@ -1677,7 +1750,7 @@ cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_
 }
 
 cudaError_t b_launch_expand_norms(const DevPlan &d, cudaStream_t s) {
-  if (d.n) k_b_expand_norms<<<row_grid(d, 8 * 148 / (d.nbp >> 5) + 1), ROW_BLOCK, 0, s>>>(d);
+  if (d.n) k_b_expand_norms<<<row_grid(d, 3 * 148 / (d.nbp >> 5) + 1), ROW_BLOCK, 0, s>>>(d);
   return cudaGetLastError();
 }
 
@@ -1917,15 +1990,23 @@ cudaError_t b_launch_diag_stats(const DevPlan &d, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// entries per lane per round of the tiled SpMV (KKT_B_SPMV_T = 4 | 8)
+static int spmv_entries() {
+  static const int t = std::getenv("KKT_B_SPMV_T") ? std::atoi(std::getenv("KKT_B_SPMV_T")) : 8;
+  return t;
+}
+
 cudaError_t b_launch_spmv(const DevPlan &d, const double *x, double *out, const double *bsub,
                           double *nrm_partials, cudaStream_t s) {
-  k_b_spmv<<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, x, out, bsub, nrm_partials);
+  if (spmv_entries() == 4) k_b_spmv<4><<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, x, out, bsub, nrm_partials);
+  else k_b_spmv<8><<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, x, out, bsub, nrm_partials);
   return cudaGetLastError();
 }
 
 cudaError_t b_launch_resid_stats(const DevPlan &d, const double *r, const double *x,
                                  double *partials, double *out5, cudaStream_t s) {
-  k_b_resid_stats<<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, r, x, partials);
+  if (spmv_entries() == 4) k_b_resid_stats<4><<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, r, x, partials);
+  else k_b_resid_stats<8><<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, r, x, partials);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_b_resid_final<<<dim3(5, d.nbp), 32, 0, s>>>(partials, d.rb, out5);

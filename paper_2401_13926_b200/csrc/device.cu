@@ -332,7 +332,10 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   for (int l = 0; l <= h.n_small_levels; ++l) d.lev_ptr[l] = h.small_lev_ptr[l];
   d.ref_start = h.small_lev_ptr[h.n_small_levels];
   d.poll_ns = std::getenv("KKT_POLL_NS") ? std::atoi(std::getenv("KKT_POLL_NS")) : (nbp > 1 ? 64 : 0);
-  d.grid_wait = std::getenv("KKT_GRID_WAIT") ? std::atoi(std::getenv("KKT_GRID_WAIT")) : 0;
+  // single system: one lane waits on the critical dependency before the row (without it the
+  // lanes poll their unpublished columns at once: 1.27 -> 3.16 ms at 10k); batch: no up-front
+  // wait (the lanes are systems, one 256-byte line per poll: 3.62 -> 1.84 ms at 10k x 64)
+  d.grid_wait = std::getenv("KKT_GRID_WAIT") ? std::atoi(std::getenv("KKT_GRID_WAIT")) : (nbp > 1 ? 0 : 1);
   d.pL = h.pL;
   d.pU = h.pU;
   d.nLg = (int)h.L_grid_order.size();
@@ -991,6 +994,22 @@ int kkt_dev_solve(kkt_device *d, const double *b_dev, double *x_dev) {
     return KKT_OK;
   }
   return kkt::dev_solve(dev, b_dev, x_dev);
+}
+
+// The kernels alone, on vectors in the handle's internal layout ([n][nbp] interleaved for a
+// batch): what bench.py times for the per-kernel roofline (no boundary transposes).
+int kkt_dev_solve_native(kkt_device *d, const double *b_dev, double *x_dev) {
+  Device *dev = reinterpret_cast<Device *>(d);
+  if (!dev || !b_dev || !x_dev) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
+  cudaSetDevice(dev->device);
+  return kkt::dev_solve(dev, b_dev, x_dev);
+}
+
+int kkt_dev_spmv_native(kkt_device *d, const double *x_dev, double *y_dev) {
+  Device *dev = reinterpret_cast<Device *>(d);
+  if (!dev || !x_dev || !y_dev) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
+  cudaSetDevice(dev->device);
+  return kkt::dev_spmv(dev, x_dev, y_dev, nullptr, nullptr);
 }
 
 int kkt_dev_spmv(kkt_device *d, const double *x_dev, double *y_dev) {

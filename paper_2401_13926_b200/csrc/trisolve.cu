@@ -64,11 +64,15 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
       col = ci[beg + lane];
       v = vals[beg + lane];
     }
-    // lane 0 alone spins on the critical dependency; the other dependencies are then
-    // normally published already, so the lanes' loads below rarely have to wait
-    const int cr = crit[idx];
-    if (lane == 0 && cr >= 0) wait_value(&ysrc[cr], d.poll_ns);
-    __syncwarp();
+    // grid_wait 1 (the single-system default): lane 0 alone spins on the critical dependency
+    // before the row; the other dependencies are then normally published already, so the
+    // lanes' loads below rarely have to wait.  (0: each lane polls its own unpublished column
+    // in the chunk loop — many pollers per row, measured 2.5x slower.)
+    if (d.grid_wait) {
+      const int cr = crit[idx];
+      if (lane == 0 && cr >= 0) wait_value(&ysrc[cr], d.poll_ns);
+      __syncwarp();
+    }
     for (int c0 = beg; c0 < end; c0 += 32) {
       const int cnt = min(32, end - c0);
       double p = 0.0;

@@ -179,6 +179,18 @@ class DeviceSystem:
         self.solve_device(self.b, self.x)
         return self.d2h(self.x)
 
+    def nbp(self) -> int:
+        """interleaved width of the handle's internal vectors (1 for a single system)"""
+        return 1 if self.nb == 1 else (self.nb + 31) // 32 * 32
+
+    def solve_native(self, b_t, x_t):
+        """lu_solve kernels on internal-layout vectors ([n][nbp]; no boundary transposes)"""
+        nat.check(self.lib.kkt_dev_solve_native(self.h, _vp(b_t), _vp(x_t)), "kkt_dev_solve_native")
+
+    def spmv_native(self, x_t, y_t):
+        """SpMV kernel on internal-layout vectors ([n][nbp]; no boundary transposes)"""
+        nat.check(self.lib.kkt_dev_spmv_native(self.h, _vp(x_t), _vp(y_t)), "kkt_dev_spmv_native")
+
     def spmv_device(self, x_t, y_t):
         nat.check(self.lib.kkt_dev_spmv(self.h, _vp(x_t), _vp(y_t)), "kkt_dev_spmv")
 
