@@ -30,6 +30,7 @@
 
 namespace kkt {
 
+static int rowwise();  // KKT_B_SPMV_TILES (below)
 constexpr int BY = 8;            // rows (warps) per block of the 2-D row kernels
 constexpr int SMALL_PAT_B = 64;
 constexpr unsigned FULL = 0xffffffffu;
@@ -1505,6 +1506,98 @@ __global__ void __launch_bounds__(256, 3) k_b_resid_stats(DevPlan d, const doubl
   }
 }
 
+// ---- the per-row SpMV / residual statistics (the default; see rowwise()) ----
+// Row i of K x for one system (lane), in the reference's order.  The row's products are
+// formed from loads issued SPMV_U entries at a time (all independent), then summed in order
+// (4: 48 registers; 8 measured 0.49 vs 0.36 ms at 10k x 64, 2 0.40 ms).
+constexpr int SPMV_U = 4;
+__device__ __forceinline__ double row_dot_b(const DevPlan &d, const double *__restrict__ x, int i,
+                                            int sys) {
+  const int b = d.A_rp[i], s = d.A_split[i], e = d.A_rp[i + 1];
+  const double *__restrict__ av = d.A_vals;
+  const int *__restrict__ ci = d.A_ci;
+  double s1 = 0.0, s2 = 0.0;
+  for (int p0 = b; p0 < e; p0 += SPMV_U) {
+    int c[SPMV_U];
+    double v[SPMV_U], xv[SPMV_U];
+#pragma unroll
+    for (int u = 0; u < SPMV_U; ++u)
+      if (p0 + u < e) {
+        c[u] = ci[p0 + u];
+        v[u] = av[IL(d, p0 + u, sys)];
+      }
+#pragma unroll
+    for (int u = 0; u < SPMV_U; ++u)
+      if (p0 + u < e) xv[u] = x[IL(d, c[u], sys)];
+#pragma unroll
+    for (int u = 0; u < SPMV_U; ++u)
+      if (p0 + u < e) {
+        const double t = __dmul_rn(v[u], xv[u]);
+        // symmetric-lower operators sum the stored and the mirrored halves apart
+        // (sparsecore.py:296-302); general ones in one pass
+        if (d.sym_lower && p0 + u >= s) s2 = __dadd_rn(s2, t);
+        else s1 = __dadd_rn(s1, t);
+      }
+  }
+  return d.sym_lower ? __dadd_rn(s1, s2) : s1;
+}
+
+__global__ void __launch_bounds__(256) k_b_spmv_row(DevPlan d, const double *__restrict__ x,
+                                                double *__restrict__ out,
+                                                const double *__restrict__ bsub,
+                                                double *__restrict__ nrm_out) {
+  __shared__ double sh[BY][32];
+  const int sys = blockIdx.y * 32 + threadIdx.x;
+  const bool act = sys_active(d, sys);
+  if (!__syncthreads_or(act)) return;
+  double loc = 0.0;
+  bool bad = false;
+  if (act) {
+    for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
+      const double y = row_dot_b(d, x, i, sys);
+      if (!isfinite(y)) bad = true;
+      const double o = bsub ? __dsub_rn(bsub[IL(d, i, sys)], y) : y;
+      out[IL(d, i, sys)] = o;
+      loc = __dadd_rn(loc, __dmul_rn(o, o));
+    }
+  }
+  if (bad) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
+  if (nrm_out) {
+    const double t = reduce_y<false>(loc, sh);
+    if (threadIdx.y == 0 && act) nrm_out[(size_t)sys * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_b_resid_stats_row(DevPlan d, const double *__restrict__ r,
+                                                       const double *__restrict__ x,
+                                                       double *__restrict__ partials) {
+  __shared__ double sh[BY][32];
+  const int sys = blockIdx.y * 32 + threadIdx.x, nblk = gridDim.x;
+  double e2 = 0.0, emax = 0.0, x2 = 0.0, xmax = 0.0, r2 = 0.0;
+  for (int i = blockIdx.x * BY + threadIdx.y; i < d.n; i += gridDim.x * BY) {
+    const double ri = r[IL(d, i, sys)], xi = x[IL(d, i, sys)];
+    const double ei = __dsub_rn(ri, row_dot_b(d, x, i, sys));
+    e2 += ei * ei;
+    emax = fmax(emax, fabs(ei));
+    x2 += xi * xi;
+    xmax = fmax(xmax, fabs(xi));
+    r2 += ri * ri;
+  }
+  double *part = partials + (size_t)sys * 5 * nblk;
+  e2 = reduce_y<false>(e2, sh);
+  emax = reduce_y<true>(emax, sh);
+  x2 = reduce_y<false>(x2, sh);
+  xmax = reduce_y<true>(xmax, sh);
+  r2 = reduce_y<false>(r2, sh);
+  if (threadIdx.y == 0) {
+    part[0 * nblk + blockIdx.x] = e2;
+    part[1 * nblk + blockIdx.x] = emax;
+    part[2 * nblk + blockIdx.x] = x2;
+    part[3 * nblk + blockIdx.x] = xmax;
+    part[4 * nblk + blockIdx.x] = r2;
+  }
+}
+
 // out[sys][5] = {||e||_2, ||e||_inf, ||x||_2, ||x||_inf, ||r||_2}
 __global__ void k_b_resid_final(const double *__restrict__ partials, int nblk, double *__restrict__ out) {
   const int v = blockIdx.x, sys = blockIdx.y;
@@ -1990,22 +2083,34 @@ cudaError_t b_launch_diag_stats(const DevPlan &d, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// SpMV / residual statistics kernel: the per-row one by default.  The tiled flat walk
+// (KKT_B_SPMV_TILES=1) gives bitwise the same K x but sums the norm partials in another order,
+// and the batched FGMRES is sensitive to that on its hardest systems: activsg2000p k = 18
+// converges (est <= delta beta0) at a true rr of 3.6e-10 instead of 2.3e-12 (both 9
+// iterations; the reference: 8, 4.9e-12) — so the row order stays the default.
+static int rowwise() {
+  const char *e = std::getenv("KKT_B_SPMV_TILES");
+  return e ? !std::atoi(e) : 1;
+}
+
 // entries per lane per round of the tiled SpMV (KKT_B_SPMV_T = 4 | 8)
 static int spmv_entries() {
-  static const int t = std::getenv("KKT_B_SPMV_T") ? std::atoi(std::getenv("KKT_B_SPMV_T")) : 8;
-  return t;
+  const char *e = std::getenv("KKT_B_SPMV_T");
+  return e ? std::atoi(e) : 8;
 }
 
 cudaError_t b_launch_spmv(const DevPlan &d, const double *x, double *out, const double *bsub,
                           double *nrm_partials, cudaStream_t s) {
-  if (spmv_entries() == 4) k_b_spmv<4><<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, x, out, bsub, nrm_partials);
+  if (rowwise()) k_b_spmv_row<<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, x, out, bsub, nrm_partials);
+  else if (spmv_entries() == 4) k_b_spmv<4><<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, x, out, bsub, nrm_partials);
   else k_b_spmv<8><<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, x, out, bsub, nrm_partials);
   return cudaGetLastError();
 }
 
 cudaError_t b_launch_resid_stats(const DevPlan &d, const double *r, const double *x,
                                  double *partials, double *out5, cudaStream_t s) {
-  if (spmv_entries() == 4) k_b_resid_stats<4><<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, r, x, partials);
+  if (rowwise()) k_b_resid_stats_row<<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, r, x, partials);
+  else if (spmv_entries() == 4) k_b_resid_stats<4><<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, r, x, partials);
   else k_b_resid_stats<8><<<dim3(d.rb, d.nbp >> 5), ROW_BLOCK, 0, s>>>(d, r, x, partials);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

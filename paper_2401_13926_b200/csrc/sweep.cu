@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(BS_THREADS) k_trsv_blocked(DevPlan d, double *
     }
     issue_tile(c + 1);
     cp_async_wait<1>();  // this thread's copies of tile c have landed
+    __syncwarp();        // (the copy loops leave warps diverged; the barrier is .aligned)
     __syncthreads();     // ... everyone's; and phase B of block c-1 is complete
     if (tr) tr[4 * c + 1] = globaltimer();
     const int b0 = sw.bptr[c], b1 = sw.bptr[c + 1];
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(BS_THREADS) k_trsv_blocked(DevPlan d, double *
       }
     }
     if (STAGED) cp_async_wait<0>();
+    __syncwarp();
     __syncthreads();  // the block's y values (and staged runs) are in shared memory
     // phase B: later rows (L: below the block; U: above it, inside the head) in CSR order
     if (STAGED) {

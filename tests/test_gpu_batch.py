@@ -83,3 +83,40 @@ def test_batch_step_matches_reference(case, nb):
         rr_ref = np.linalg.norm(rhs[q] - K.to_dense() @ xr) / np.linalg.norm(rhs[q])
         assert rr <= max(1.5 * rr_ref, 4 * np.finfo(float).eps), (q, k, rr, rr_ref)
     dev.close()
+
+
+@pytest.mark.parametrize("tiles", ["0", "1"])
+@pytest.mark.parametrize("case,nb", [("acopf_small", 33), ("standard_trace", 9), ("acopf_tiny", 40)])
+def test_batch_spmv_residual_and_norms_bitwise(case, nb, tiles, monkeypatch):
+    """The batched SpMV (per-row kernel, and the tiled flat walk with KKT_B_SPMV_TILES=1),
+    residual statistics and the tiled value expansion against the reference's spmv
+    (sparsecore.py:284-305) and inf_norm: every system bitwise."""
+    import torch
+    monkeypatch.setenv("KKT_B_SPMV_TILES", tiles)
+    from oracle import oracle
+    from paper_2401_13926_b200.device import DeviceSystem
+    from paper_2401_13926_b200.sparse import to_general
+    g = golden(case)
+    M = g["K_values"].shape[0]
+    systems = [(M - 1 - q) % M for q in range(nb)]
+    f, _ = factorize(to_general(lower_matrix(g, 0)))
+    dev = DeviceSystem(f, batch=nb)
+    vals = np.ascontiguousarray(np.stack([g["K_values"][k] for k in systems]))
+    x0 = np.ascontiguousarray(np.stack([g["x0"][k] for k in systems]))
+    rhs = np.ascontiguousarray(np.stack([g["rhs"][k] for k in systems]))
+    with torch.cuda.stream(dev.stream):
+        tv = torch.from_numpy(vals).to(dev.device)
+        tx = torch.from_numpy(x0).to(dev.device)
+        tr = torch.from_numpy(rhs).to(dev.device)
+        ty = torch.empty_like(tx)
+    dev.refactor_batch(tv, nat.LAYOUT_SYMMETRIC_LOWER)
+    dev.spmv_device(tx, ty)
+    y = dev.d2h(ty)
+    stats = dev.residual_stats_device(tr, tx)
+    for q, k in enumerate(systems):
+        assert np.array_equal(y[q], g["spmv_K_x0"][k]), (q, k)
+        K = lower_matrix(g, k)
+        e = rhs[q] - g["spmv_K_x0"][k]
+        assert stats[q].err_inf == np.max(np.abs(e)), (q, k)
+        assert stats[q].k_inf == oracle.inf_norm(K.row_ptr, K.col_idx, K.values), (q, k)
+    dev.close()
