@@ -23,10 +23,11 @@
 
 namespace kkt {
 
-constexpr int BS_THREADS = 256;
-
-template <bool IS_U, int S, bool STAGED>
-__global__ void __launch_bounds__(BS_THREADS) k_trsv_blocked(DevPlan d, double *__restrict__ xout) {
+// threads per sweep CTA (template NT; KKT_SWEEP_THREADS = 256 | 512 | 1024): phase A is one
+// warp per system whatever NT; the other warps stage the next block and run phase B.
+template <bool IS_U, int S, bool STAGED, int NT>
+__global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restrict__ xout) {
+  constexpr int BS_THREADS = NT;
   extern __shared__ double sm[];
   const SweepDev &sw = IS_U ? d.swU : d.swL;
   const int sys0 = blockIdx.x * S;
@@ -191,32 +192,49 @@ __global__ void __launch_bounds__(BS_THREADS) k_trsv_blocked(DevPlan d, double *
 }
 
 constexpr size_t SMEM_CAP = 227 * 1024;
+constexpr int SWEEP_THREADS_DEFAULT = 256;
 
 static size_t blocked_smem(int T, int S, int stage) {
   return ((size_t)T * S + 2 * 1024 * S + 32 * S + (size_t)stage * S) * sizeof(double) +
          (size_t)stage * sizeof(int);
 }
 
-template <bool IS_U, int S, bool STAGED>
+template <bool IS_U, int S, bool STAGED, int NT>
 static cudaError_t set_attr() {
-  return cudaFuncSetAttribute(k_trsv_blocked<IS_U, S, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(k_trsv_blocked<IS_U, S, STAGED, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)SMEM_CAP);
 }
 
-template <int S>
+template <int S, int NT>
 static cudaError_t set_attrs() {
-  cudaError_t e = set_attr<false, S, false>();
-  if (e == cudaSuccess) e = set_attr<true, S, false>();
-  if (e == cudaSuccess) e = set_attr<false, S, true>();
-  if (e == cudaSuccess) e = set_attr<true, S, true>();
+  cudaError_t e = set_attr<false, S, false, NT>();
+  if (e == cudaSuccess) e = set_attr<true, S, false, NT>();
+  if (e == cudaSuccess) e = set_attr<false, S, true, NT>();
+  if (e == cudaSuccess) e = set_attr<true, S, true, NT>();
   return e;
 }
 
+static int sweep_threads() {
+  const char *e = std::getenv("KKT_SWEEP_THREADS");
+  const int t = e ? std::atoi(e) : SWEEP_THREADS_DEFAULT;
+  return t >= 1024 ? 1024 : t >= 512 ? 512 : 256;
+}
+
 cudaError_t sweep_configure() {
-  cudaError_t e = set_attrs<1>();
-  if (e == cudaSuccess) e = set_attrs<2>();
-  if (e == cudaSuccess) e = set_attrs<4>();
+  cudaError_t e = set_attrs<1, 256>();
+  if (e == cudaSuccess) e = set_attrs<2, 256>();
+  if (e == cudaSuccess) e = set_attrs<4, 256>();
+  if (e == cudaSuccess) e = set_attrs<1, 512>();
+  if (e == cudaSuccess) e = set_attrs<1, 1024>();
   return e;
+}
+
+template <bool IS_U, int S, bool STAGED>
+static void launch_nt(const DevPlan &d, double *x, size_t smem, cudaStream_t s) {
+  const int nt = S == 1 ? sweep_threads() : 256;
+  if (nt == 1024) k_trsv_blocked<IS_U, S, STAGED, 1024><<<d.nbp / S, 1024, smem, s>>>(d, x);
+  else if (nt == 512) k_trsv_blocked<IS_U, S, STAGED, 512><<<d.nbp / S, 512, smem, s>>>(d, x);
+  else k_trsv_blocked<IS_U, S, STAGED, 256><<<d.nbp / S, 256, smem, s>>>(d, x);
 }
 
 // the staged variant when the largest block's runs fit in shared memory
@@ -226,12 +244,12 @@ static void launch_s(const DevPlan &d, bool upper, double *x, int T, cudaStream_
   static const bool no_stage = std::getenv("KKT_SWEEP_NOSTAGE") != nullptr;
   const size_t st = blocked_smem(T, S, sw.max_stage);
   if (!no_stage && st <= SMEM_CAP) {
-    if (upper) k_trsv_blocked<true, S, true><<<d.nbp / S, BS_THREADS, st, s>>>(d, x);
-    else k_trsv_blocked<false, S, true><<<d.nbp / S, BS_THREADS, st, s>>>(d, x);
+    if (upper) launch_nt<true, S, true>(d, x, st, s);
+    else launch_nt<false, S, true>(d, x, st, s);
   } else {
     const size_t sm = blocked_smem(T, S, 0);
-    if (upper) k_trsv_blocked<true, S, false><<<d.nbp / S, BS_THREADS, sm, s>>>(d, x);
-    else k_trsv_blocked<false, S, false><<<d.nbp / S, BS_THREADS, sm, s>>>(d, x);
+    if (upper) launch_nt<true, S, false>(d, x, sm, s);
+    else launch_nt<false, S, false>(d, x, sm, s);
   }
 }
 
