@@ -25,9 +25,14 @@ namespace kkt {
 
 // threads per sweep CTA (template NT; KKT_SWEEP_THREADS = 256 | 512 | 1024): phase A is one
 // warp per system whatever NT; the other warps stage the next block and run phase B.
-template <bool IS_U, int S, bool STAGED, int NT>
+// MODE 0: off-diagonal runs read from global in phase B; 1: staged into shared memory by the
+// non-chain warps while the chain runs; 2 (look-ahead): block c+1's tile AND runs are staged
+// (double-buffered) while block c's chain runs, so a block's critical path is barrier ->
+// chain -> barrier -> phase B from shared memory, with no load latency on it.
+template <bool IS_U, int S, int MODE, int NT>
 __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restrict__ xout) {
   constexpr int BS_THREADS = NT;
+  constexpr bool STAGED = MODE >= 1;
   extern __shared__ double sm[];
   const SweepDev &sw = IS_U ? d.swU : d.swL;
   const int sys0 = blockIdx.x * S;
@@ -42,8 +47,9 @@ __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restri
   double *acc = sm;                          // [T][S]
   double *tile = acc + (size_t)T * S;        // [2][32*32][S]
   double *yb = tile + 2 * 1024 * S;          // [32][S]
-  double *sv = yb + 32 * S;                  // [max_stage][S]   (STAGED)
-  int *scol = reinterpret_cast<int *>(sv + (size_t)sw.max_stage * S);  // [max_stage]
+  constexpr int NBUF = MODE == 2 ? 2 : 1;
+  double *sv = yb + 32 * S;                  // [NBUF][max_stage][S]   (STAGED)
+  int *scol = reinterpret_cast<int *>(sv + (size_t)NBUF * sw.max_stage * S);  // [NBUF][max_stage]
   const double *vals = IS_U ? d.Uv : d.Lv;
   const int *ci = IS_U ? d.Uci : d.Lci;
   for (int f = tid; f < T * S; f += BS_THREADS) {
@@ -67,7 +73,24 @@ __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restri
     }
     cp_async_commit();
   };
-  issue_tile(0);
+  // MODE 2: block c's off-diagonal runs into stage buffer c & 1 (issued a block ahead)
+  auto issue_runs = [&](int c, int t0, int nthr) {
+    if (c < sw.nblk) {
+      double *svb = sv + (size_t)(c & 1) * sw.max_stage * S;
+      int *scb = scol + (size_t)(c & 1) * sw.max_stage;
+      const int b0 = sw.bptr[c], b1 = sw.bptr[c + 1];
+      for (int k = b0 + t0; k < b1; k += nthr) {
+        const int beg = sw.bbeg[k], cnt = sw.bcnt[k], o = sw.bofs[k];
+        for (int e = 0; e < cnt; ++e) {
+#pragma unroll
+          for (int q = 0; q < S; ++q) cp_async8(&svb[(size_t)(o + e) * S + q], &vals[IL(d, beg + e, sys0 + q)]);
+          cp_async4(&scb[o + e], &ci[beg + e]);
+        }
+      }
+    }
+  };
+  if (MODE == 2) issue_runs(0, tid, BS_THREADS);
+  issue_tile(0);  // (commits the group: tile 0 + the runs of block 0)
   bool bad = false;
   // optional timeline (KKT_TRACE, single system): per block {top, tiles ready, y ready, end}
   unsigned long long *tr = (d.trace_trsv && blockIdx.x == 0 && tid == 0)
@@ -93,13 +116,21 @@ __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restri
       mask = sw.dmask[c * 32 + lane];
       if (IS_U) piv = d.udiag[IL(d, lo + lane, sys0 + s)];
     }
-    issue_tile(c + 1);
-    cp_async_wait<1>();  // this thread's copies of tile c have landed
+    if (MODE == 2) {
+      cp_async_wait<0>();  // this thread's copies of block c (tile + runs) have landed
+    } else {
+      issue_tile(c + 1);
+      cp_async_wait<1>();  // this thread's copies of tile c have landed
+    }
     __syncwarp();        // (the copy loops leave warps diverged; the barrier is .aligned)
     __syncthreads();     // ... everyone's; and phase B of block c-1 is complete
     if (tr) tr[4 * c + 1] = globaltimer();
     const int b0 = sw.bptr[c], b1 = sw.bptr[c + 1];
-    if (STAGED && warp >= S) {  // the other warps stream the block's off-diagonal runs
+    if (MODE == 2 && warp >= S) {  // the other warps stage block c+1 while the chain runs
+      issue_runs(c + 1, tid - 32 * S, BS_THREADS - 32 * S);
+      issue_tile(c + 1);
+    }
+    if (MODE == 1 && warp >= S) {  // the other warps stream the block's off-diagonal runs
       for (int k = b0 + tid - 32 * S; k < b1; k += BS_THREADS - 32 * S) {
         const int beg = sw.bbeg[k], cnt = sw.bcnt[k], o = sw.bofs[k];
         for (int e = 0; e < cnt; ++e) {
@@ -109,7 +140,7 @@ __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restri
         }
       }
     }
-    if (STAGED) cp_async_commit();
+    if (MODE == 1) cp_async_commit();
     if (chain) {
       // the lane's row of the diagonal triangle in registers, then a pure register chain
       const double *tl = tile + (size_t)(c & 1) * 1024 * S;
@@ -150,18 +181,20 @@ __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restri
         }
       }
     }
-    if (STAGED) cp_async_wait<0>();
+    if (MODE == 1) cp_async_wait<0>();
     __syncwarp();
     __syncthreads();  // the block's y values (and staged runs) are in shared memory
     // phase B: later rows (L: below the block; U: above it, inside the head) in CSR order
     if (STAGED) {
+      const double *svb = sv + (size_t)(MODE == 2 ? (c & 1) : 0) * sw.max_stage * S;
+      const int *scb = scol + (size_t)(MODE == 2 ? (c & 1) : 0) * sw.max_stage;
       for (int f = tid; f < (b1 - b0) * S; f += BS_THREADS) {
         const int k = b0 + f / S, q = f % S;
         const int r = sw.brow[k], cnt = sw.bcnt[k], o = sw.bofs[k];
         double a = acc[(size_t)(r - p) * S + q];
 #pragma unroll 4
         for (int e = 0; e < cnt; ++e)
-          a = __dsub_rn(a, __dmul_rn(sv[(size_t)(o + e) * S + q], yb[(scol[o + e] - lo) * S + q]));
+          a = __dsub_rn(a, __dmul_rn(svb[(size_t)(o + e) * S + q], yb[(scb[o + e] - lo) * S + q]));
         acc[(size_t)(r - p) * S + q] = a;
       }
       if (tr) tr[4 * c + 3] = globaltimer();
@@ -194,23 +227,25 @@ __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restri
 constexpr size_t SMEM_CAP = 227 * 1024;
 constexpr int SWEEP_THREADS_DEFAULT = 256;
 
-static size_t blocked_smem(int T, int S, int stage) {
-  return ((size_t)T * S + 2 * 1024 * S + 32 * S + (size_t)stage * S) * sizeof(double) +
-         (size_t)stage * sizeof(int);
+static size_t blocked_smem(int T, int S, int stage, int nbuf = 1) {
+  return ((size_t)T * S + 2 * 1024 * S + 32 * S + (size_t)nbuf * stage * S) * sizeof(double) +
+         (size_t)nbuf * stage * sizeof(int);
 }
 
-template <bool IS_U, int S, bool STAGED, int NT>
+template <bool IS_U, int S, int MODE, int NT>
 static cudaError_t set_attr() {
-  return cudaFuncSetAttribute(k_trsv_blocked<IS_U, S, STAGED, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(k_trsv_blocked<IS_U, S, MODE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)SMEM_CAP);
 }
 
 template <int S, int NT>
 static cudaError_t set_attrs() {
-  cudaError_t e = set_attr<false, S, false, NT>();
-  if (e == cudaSuccess) e = set_attr<true, S, false, NT>();
-  if (e == cudaSuccess) e = set_attr<false, S, true, NT>();
-  if (e == cudaSuccess) e = set_attr<true, S, true, NT>();
+  cudaError_t e = set_attr<false, S, 0, NT>();
+  if (e == cudaSuccess) e = set_attr<true, S, 0, NT>();
+  if (e == cudaSuccess) e = set_attr<false, S, 1, NT>();
+  if (e == cudaSuccess) e = set_attr<true, S, 1, NT>();
+  if (e == cudaSuccess) e = set_attr<false, S, 2, NT>();
+  if (e == cudaSuccess) e = set_attr<true, S, 2, NT>();
   return e;
 }
 
@@ -229,28 +264,36 @@ cudaError_t sweep_configure() {
   return e;
 }
 
-template <bool IS_U, int S, bool STAGED>
+template <bool IS_U, int S, int MODE>
 static void launch_nt(const DevPlan &d, double *x, size_t smem, cudaStream_t s) {
   const int nt = S == 1 ? sweep_threads() : 256;
-  if (nt == 1024) k_trsv_blocked<IS_U, S, STAGED, 1024><<<d.nbp / S, 1024, smem, s>>>(d, x);
-  else if (nt == 512) k_trsv_blocked<IS_U, S, STAGED, 512><<<d.nbp / S, 512, smem, s>>>(d, x);
-  else k_trsv_blocked<IS_U, S, STAGED, 256><<<d.nbp / S, 256, smem, s>>>(d, x);
+  if (nt == 1024) k_trsv_blocked<IS_U, S, MODE, 1024><<<d.nbp / S, 1024, smem, s>>>(d, x);
+  else if (nt == 512) k_trsv_blocked<IS_U, S, MODE, 512><<<d.nbp / S, 512, smem, s>>>(d, x);
+  else k_trsv_blocked<IS_U, S, MODE, 256><<<d.nbp / S, 256, smem, s>>>(d, x);
 }
 
-// the staged variant when the largest block's runs fit in shared memory
+template <bool IS_U, int S>
+static void launch_mode(const DevPlan &d, double *x, int mode, size_t smem, cudaStream_t s) {
+  if (mode == 2) launch_nt<IS_U, S, 2>(d, x, smem, s);
+  else if (mode == 1) launch_nt<IS_U, S, 1>(d, x, smem, s);
+  else launch_nt<IS_U, S, 0>(d, x, smem, s);
+}
+
+// the look-ahead variant when two blocks' runs fit in shared memory, else the staged one, else
+// runs from global (KKT_SWEEP_AHEAD=0 / KKT_SWEEP_NOSTAGE force the older variants)
 template <int S>
 static void launch_s(const DevPlan &d, bool upper, double *x, int T, cudaStream_t s) {
   const SweepDev &sw = upper ? d.swU : d.swL;
-  static const bool no_stage = std::getenv("KKT_SWEEP_NOSTAGE") != nullptr;
-  const size_t st = blocked_smem(T, S, sw.max_stage);
-  if (!no_stage && st <= SMEM_CAP) {
-    if (upper) launch_nt<true, S, true>(d, x, st, s);
-    else launch_nt<false, S, true>(d, x, st, s);
-  } else {
-    const size_t sm = blocked_smem(T, S, 0);
-    if (upper) launch_nt<true, S, false>(d, x, sm, s);
-    else launch_nt<false, S, false>(d, x, sm, s);
-  }
+  const char *na = std::getenv("KKT_SWEEP_AHEAD");
+  const bool ahead = !na || std::atoi(na) != 0;
+  const bool no_stage = std::getenv("KKT_SWEEP_NOSTAGE") != nullptr;
+  const size_t s2 = blocked_smem(T, S, sw.max_stage, 2), s1 = blocked_smem(T, S, sw.max_stage, 1);
+  int mode = 0;
+  size_t smem = blocked_smem(T, S, 0);
+  if (!no_stage && ahead && s2 <= SMEM_CAP) mode = 2, smem = s2;
+  else if (!no_stage && s1 <= SMEM_CAP) mode = 1, smem = s1;
+  if (upper) launch_mode<true, S>(d, x, mode, smem, s);
+  else launch_mode<false, S>(d, x, mode, smem, s);
 }
 
 cudaError_t launch_sweep_blocked(const DevPlan &d, bool upper, double *x, cudaStream_t s) {
