@@ -1145,7 +1145,7 @@ __device__ __forceinline__ void row_prefetch(const DevPlan &d, const double *__r
   const double *vals = IS_U ? d.Uv : d.Lv;
   t.r = order[idx];
   t.cr = (IS_U ? d.U_crit : d.L_crit)[idx];
-  t.beg = rp[t.r];
+  t.beg = (IS_U && d.u_partial) ? d.Ugrid_split[t.r] : rp[t.r];
   t.end = rp[t.r + 1];
 #pragma unroll
   for (int q = 0; q < RC; ++q)
@@ -1307,7 +1307,7 @@ __global__ void __launch_bounds__(256) k_b_trsv_levels(DevPlan d, const double *
       const int sys = (task % ngroups) * 32 + lane;
       if (!sys_active(d, sys)) continue;
       const int r = order[idx];
-      const int beg = rp[r], end = rp[r + 1];
+      const int beg = (IS_U && d.u_partial) ? d.Ugrid_split[r] : rp[r], end = rp[r + 1];
       double acc = IS_U ? ldcg(&d.yL[IL(d, r, sys)]) : b[IL(d, d.row_perm[r], sys)];
       for (int c0 = beg; c0 < end; c0 += 4) {
         double v[4], y[4];
@@ -1369,7 +1369,8 @@ cudaError_t b_launch_trsv(const DevPlan &d, const double *b, double *x, int grid
     ++*launches;
   }
   if (d.nUg) {
-    cudaError_t e = b_launch_grid<true>(d, b, x, grid_blocks, s);
+    cudaError_t e = launch_U_partial(d, s, launches);
+    if (e == cudaSuccess) e = b_launch_grid<true>(d, b, x, grid_blocks, s);
     if (e != cudaSuccess) return e;
     ++*launches;
   }

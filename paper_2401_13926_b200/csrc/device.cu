@@ -370,6 +370,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   acc(4 * h.L_crit.size()); acc(4 * h.U_crit.size()); acc(4 * h.Uhead_off.size());
   acc(4 * d.nnz_L); acc(4 * d.nnz_U);                                      // Li Ui (CSC)
   acc(4 * h.Ltail_split.size()); acc(8 * h.Ltail_split.size() * B);        // split, tacc
+  acc(4 * h.Ugrid_split.size()); acc(4 * h.U_part_rows.size());            // U head prefix
   acc(8 * d.nnz_L * B); acc(8 * d.nnz_U * B); acc(8 * n * B); acc(8 * n * B);  // Lv Uv yL yU
   acc(8 * SCAL_STRIDE * B); acc(64); acc(8 * 8 * (size_t)d.rb * B);        // scal ticket partials
   acc(8 * btask.size());                                                   // batched tasks
@@ -429,6 +430,10 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   d.Ui = carve<int>(cur, d.nnz_U);
   d.Ltail_split = carve<int>(cur, h.Ltail_split.size());
   d.tacc = carve<double>(cur, h.Ltail_split.size() * B);
+  d.Ugrid_split = carve<int>(cur, h.Ugrid_split.size());
+  d.U_part_rows = carve<int>(cur, h.U_part_rows.size());
+  d.n_upart = (int)h.U_part_rows.size();
+  d.u_partial = std::getenv("KKT_U_PARTIAL") ? std::atoi(std::getenv("KKT_U_PARTIAL")) : 1;
   d.Lv = carve<double>(cur, d.nnz_L * B);
   d.Uv = carve<double>(cur, d.nnz_U * B);
   d.yL = carve<double>(cur, n * B);
@@ -520,6 +525,8 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   UP(d.Li, h.Li32);
   UP(d.Ui, h.Ui32);
   UP(d.Ltail_split, h.Ltail_split);
+  UP(d.Ugrid_split, h.Ugrid_split);
+  UP(d.U_part_rows, h.U_part_rows);
   UP(d.btask, btask);
   UP(d.so_dep, so_dep);
   UP(d.hc_col, heavy.col);

@@ -91,6 +91,8 @@ struct DevPlan {
   int *Lrp, *Lci, *Urp, *Uci, *row_perm, *col_perm;
   int *L_grid_order, *L_tail_order, *U_head_order, *U_grid_order;
   int *L_crit, *U_crit, *Uhead_off, *Li, *Ui, *Ltail_split;
+  int *Ugrid_split = nullptr, *U_part_rows = nullptr;  // U grid rows' head prefix (plan.h)
+  int n_upart = 0, u_partial = 1;  // rows with a head prefix; 0 = grid rows sum it (KKT_U_PARTIAL)
   double *tacc;                             // [nb][n - pL] tail partial sums (grid -> sweep)
   int pL, pU, nLg, nUg;                     // split positions and grid-phase row counts
   int L_nsync = 0, L_sync_ptr[5] = {0, 0, 0, 0, 0};  // level-synchronous leading L levels
@@ -186,6 +188,8 @@ cudaError_t launch_L_front(const DevPlan &d, const double *b, double *x, int gri
 cudaError_t b_launch_grid_L(const DevPlan &d, const double *b, double *x, int grid_blocks, cudaStream_t s);
 cudaError_t launch_fill_sentinel(double *p, int64_t n, cudaStream_t s);
 cudaError_t launch_add_inplace(double *x, const double *y, int64_t n, cudaStream_t s);
+// the U grid rows' head-column prefix sums into yL (row-parallel; after the U sweep)
+cudaError_t launch_U_partial(const DevPlan &d, cudaStream_t s, long long *launches);
 // blocked sweep of the trailing block (sweep.cu), single and batched handles
 cudaError_t sweep_configure();
 cudaError_t launch_sweep_blocked(const DevPlan &d, bool upper, double *x, cudaStream_t s);

@@ -301,6 +301,16 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
       lu[r] = l;
     }
     P.U_grid_order = order_by_level(lu);
+    // the grid rows' head-column prefix (final before the grid phase): summed by a separate
+    // row-parallel launch into yL, so the grid kernel starts each row at Ugrid_split
+    P.Ugrid_split.assign(P.pU, 0);
+    P.U_part_rows.clear();
+    for (int64_t r = 0; r < P.pU; ++r) {
+      int32_t q = P.Urp[r];
+      while (q < P.Urp[r + 1] && P.Uci[q] >= P.pU) ++q;
+      P.Ugrid_split[r] = q;
+      if (q > P.Urp[r]) P.U_part_rows.push_back((int32_t)r);
+    }
     // level boundaries of both grid orders (the batched level-synchronous kernel)
     auto lev_ptr = [](const std::vector<int32_t> &lev, std::vector<int32_t> &ptr) {
       int32_t nl = 0;

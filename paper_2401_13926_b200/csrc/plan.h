@@ -57,6 +57,9 @@ struct HostPlan {
   std::vector<int32_t> Uhead_off;
   std::vector<int32_t> Li32, Ui32;  // CSC row indices (int32) for the sweep phase
   std::vector<int32_t> Ltail_split;  // tail row r: CSR index of its first entry >= pL
+  // U grid row r (< pU): CSR index of its first entry < pU (the head columns come first in the
+  // descending CSR order); U_part_rows: the grid rows with at least one head entry
+  std::vector<int32_t> Ugrid_split, U_part_rows;
   int32_t sweep_maxL = 0, sweep_maxU = 0;  // longest column inside each sweep block
   HostSweep swL, swU;
 };

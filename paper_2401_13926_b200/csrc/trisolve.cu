@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
     const double *vals = (IS_U ? d.Uv : d.Lv) + (size_t)sys * nnz;
     double *ysrc = (IS_U ? d.yU : d.yL) + (size_t)sys * d.n;  // published by this sweep
     double *yres = (IS_U ? d.yL : d.yU) + (size_t)sys * d.n;  // reset for the next solve
-    const int beg = rp[r], end = rp[r + 1];
+    const int beg = (IS_U && d.u_partial) ? d.Ugrid_split[r] : rp[r], end = rp[r + 1];
     // independent loads first: the initial value and the first chunk's pattern/values
     double acc = IS_U ? ldcg(&d.yL[(size_t)sys * d.n + r]) : b[(size_t)sys * d.n + d.row_perm[r]];
     const double piv = IS_U ? d.udiag[(size_t)sys * d.n + r] : 1.0;  // off the critical path
@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(256) k_trsv_rows(DevPlan d, const int *__restr
     const int idx = (int)(f / d.nbp), sys = (int)(f - (int64_t)idx * d.nbp);
     if (!sys_active(d, sys)) continue;
     const int r = rows[idx];
-    const int beg = rp[r], end = PARTIAL ? d.Ltail_split[r - d.pL] : rp[r + 1];
+    const int beg = rp[r];
+    const int end = PARTIAL ? (IS_U ? d.Ugrid_split[r] : d.Ltail_split[r - d.pL]) : rp[r + 1];
     double acc = IS_U ? ldcg(&d.yL[IL(d, r, sys)]) : b[IL(d, d.row_perm[r], sys)];
     for (int c0 = beg; c0 < end; c0 += 4) {
       double v[4], y[4];
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(256) k_trsv_rows(DevPlan d, const int *__restr
         if (c0 + q < end) acc = __dsub_rn(acc, __dmul_rn(v[q], y[q]));
     }
     if (PARTIAL) {
-      d.tacc[IL(d, r - d.pL, sys)] = acc;
+      if (IS_U) d.yL[IL(d, r, sys)] = acc;  // the grid row resumes from here (Ugrid_split)
+      else d.tacc[IL(d, r - d.pL, sys)] = acc;
       continue;
     }
     const double w = IS_U ? __ddiv_rn(acc, d.udiag[IL(d, r, sys)]) : acc;
@@ -155,6 +157,15 @@ cudaError_t launch_trsv_rows(const DevPlan &d, bool partial, const int *rows, in
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 16 * 148);
   if (partial) k_trsv_rows<false, true><<<grid, 256, 0, s>>>(d, rows, count, b, x);
   else k_trsv_rows<false, false><<<grid, 256, 0, s>>>(d, rows, count, b, x);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_U_partial(const DevPlan &d, cudaStream_t s, long long *launches) {
+  if (!d.u_partial || d.n_upart <= 0) return cudaSuccess;
+  const int64_t total = (int64_t)d.n_upart * d.nbp;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 16 * 148);
+  k_trsv_rows<true, true><<<grid, 256, 0, s>>>(d, d.U_part_rows, d.n_upart, nullptr, nullptr);
+  ++*launches;
   return cudaGetLastError();
 }
 
@@ -234,6 +245,8 @@ cudaError_t launch_trsv(const DevPlan &d, const double *b, double *x, int grid_b
     ++*launches;
   }
   if (d.nUg) {
+    cudaError_t e = launch_U_partial(d, s, launches);
+    if (e != cudaSuccess) return e;
     k_trsv_grid<true><<<grid_blocks, 256, 0, s>>>(d, b, x);
     ++*launches;
   }
