@@ -62,11 +62,11 @@ __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restri
       d.yU[IL(d, r, sys)] = __longlong_as_double((long long)SENTINEL_BITS);
     }
   }
-  auto issue_tile = [&](int c) {
+  auto issue_tile = [&](int c, int t0, int nthr) {
     if (c < sw.nblk) {
       double *tl = tile + (size_t)(c & 1) * 1024 * S;
       const int k0 = sw.dptr[c], k1 = sw.dptr[c + 1];
-      for (int f = tid; f < (k1 - k0) * S; f += BS_THREADS) {
+      for (int f = t0; f < (k1 - k0) * S; f += nthr) {
         const int k = k0 + f / S, q = f % S;
         cp_async8(&tl[(size_t)sw.ddst[k] * S + q], &vals[IL(d, sw.dsrc[k], sys0 + q)]);
       }
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restri
     }
   };
   if (MODE == 2) issue_runs(0, tid, BS_THREADS);
-  issue_tile(0);  // (commits the group: tile 0 + the runs of block 0)
+  issue_tile(0, tid, BS_THREADS);  // (commits the group: tile 0 + the runs of block 0)
   bool bad = false;
   // optional timeline (KKT_TRACE, single system): per block {top, tiles ready, y ready, end}
   unsigned long long *tr = (d.trace_trsv && blockIdx.x == 0 && tid == 0)
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restri
     if (MODE == 2) {
       cp_async_wait<0>();  // this thread's copies of block c (tile + runs) have landed
     } else {
-      issue_tile(c + 1);
+      issue_tile(c + 1, tid, BS_THREADS);
       cp_async_wait<1>();  // this thread's copies of tile c have landed
     }
     __syncwarp();        // (the copy loops leave warps diverged; the barrier is .aligned)
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(NT) k_trsv_blocked(DevPlan d, double *__restri
     const int b0 = sw.bptr[c], b1 = sw.bptr[c + 1];
     if (MODE == 2 && warp >= S) {  // the other warps stage block c+1 while the chain runs
       issue_runs(c + 1, tid - 32 * S, BS_THREADS - 32 * S);
-      issue_tile(c + 1);
+      issue_tile(c + 1, tid - 32 * S, BS_THREADS - 32 * S);
     }
     if (MODE == 1 && warp >= S) {  // the other warps stream the block's off-diagonal runs
       for (int k = b0 + tid - 32 * S; k < b1; k += BS_THREADS - 32 * S) {
@@ -279,13 +279,15 @@ static void launch_mode(const DevPlan &d, double *x, int mode, size_t smem, cuda
   else launch_nt<IS_U, S, 0>(d, x, smem, s);
 }
 
-// the look-ahead variant when two blocks' runs fit in shared memory, else the staged one, else
-// runs from global (KKT_SWEEP_AHEAD=0 / KKT_SWEEP_NOSTAGE force the older variants)
+// the staged variant when a block's runs fit in shared memory, else runs from global.  The
+// look-ahead variant (KKT_SWEEP_AHEAD=1, two blocks' runs in shared memory) is bitwise too but
+// measured slower (10k: batch pair 1.85 -> 2.02 ms, single 1.24 -> 1.28 ms): the blocks are
+// bound by their chains and barriers, not by the staging latency it hides.
 template <int S>
 static void launch_s(const DevPlan &d, bool upper, double *x, int T, cudaStream_t s) {
   const SweepDev &sw = upper ? d.swU : d.swL;
   const char *na = std::getenv("KKT_SWEEP_AHEAD");
-  const bool ahead = !na || std::atoi(na) != 0;
+  const bool ahead = na && std::atoi(na) != 0;
   const bool no_stage = std::getenv("KKT_SWEEP_NOSTAGE") != nullptr;
   const size_t s2 = blocked_smem(T, S, sw.max_stage, 2), s1 = blocked_smem(T, S, sw.max_stage, 1);
   int mode = 0;
