@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <new>
 #include <queue>
 #include <string>
@@ -1130,10 +1131,11 @@ int kkt_dev_fgmres_ops(kkt_device *d, const kkt_linop *K, const kkt_linop *M, co
 // others, all decided on the device (one graph, one host sync).  Vectors in the handle's
 // native layout.
 static int refine_native(Device *dev, const double *r_dev, const double *x0_dev, double *x_dev,
-                         const kkt_krylov_cfg *cfg, kkt_krylov_report *rep) {
+                         const kkt_krylov_cfg *cfg, kkt_krylov_report *rep,
+                         const std::function<int()> *post = nullptr) {
   if (!(cfg->delta_tol > 0) && !cfg->delta_sys) return kkt::set_error(KKT_ERR_BAD_ARG, "delta_tol must be positive");
   return kkt::dev_fgmres(dev, r_dev, x0_dev, x_dev, cfg, 1, nullptr, nullptr, nullptr, rep, nullptr, 0,
-                         nullptr, 0);
+                         nullptr, 0, post);
 }
 
 int kkt_dev_refine_fgmres(kkt_device *d, const double *r_dev, const double *x0_dev, double *x_dev,
@@ -1192,22 +1194,26 @@ int kkt_dev_step_solve(kkt_device *d, const double *r_in, double *x_out, int io_
   }
   rc = kkt::dev_solve(dev, r_dev, K.sx0);  // x0 = lu_solve(r)      (harness.py:234)
   if (rc) return rc;
-  rc = refine_native(dev, r_dev, K.sx0, K.sx, cfg, rep);  // (harness.py:240)
+  // x out of the workspace (caller layout, host or device), enqueued behind the FGMRES graph
+  // so the whole step synchronises once (again after a straggler hand-off)
+  const std::function<int()> post = [&]() -> int {
+    const double *xs = K.sx;
+    if (il) {
+      double *dst = io_on_device ? x_out : K.w;
+      IL_OUT(K.sx, dst);
+      xs = dst;
+    }
+    if (xs != x_out) {
+      cudaError_t ce = cudaMemcpyAsync(x_out, xs, bytes,
+                                       io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                       dev->stream);
+      if (ce != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(ce));
+    }
+    return KKT_OK;
+  };
+  rc = refine_native(dev, r_dev, K.sx0, K.sx, cfg, rep, &post);  // (harness.py:240)
   if (rc && rc != KKT_ERR_NONFINITE) return rc;
-  const int rc_refine = rc;  // per-system failures still return every x
-  const double *xs = K.sx;
-  if (il) {
-    double *dst = io_on_device ? x_out : K.w;
-    IL_OUT(K.sx, dst);
-    xs = dst;
-  }
-  if (xs != x_out)
-    e = cudaMemcpyAsync(x_out, xs, bytes, io_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                        dev->stream);
-  if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
-  e = cudaStreamSynchronize(dev->stream);
-  if (e != cudaSuccess) return kkt::set_error(KKT_ERR_CUDA, cudaGetErrorString(e));
-  return rc_refine;
+  return rc;  // per-system failures (NONFINITE) still return every x
 }
 
 int kkt_op_create(int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int symmetric_lower,

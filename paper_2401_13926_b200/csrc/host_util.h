@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -108,8 +109,11 @@ void free_krylov(Device *dev);
 // LU factors.  rep[nb]; hist[nb][hist_cap] and rpairs[nb][rp_cap][2] may be NULL.  Failing
 // systems (non-finite operator output) are reported per system; the call then returns
 // KKT_ERR_NONFINITE after finishing the others.
+// `post` (may be null) enqueues the caller's follow-up copies of xout; it runs before the one
+// host synchronisation (and again after a straggler hand-off), so a kkt_dev_step waits once.
 int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout, const kkt_krylov_cfg *cfg,
                int mode, const int *active_in, const kkt_linop *opK, const kkt_linop *opM,
-               kkt_krylov_report *rep, double *hist, int hist_cap, double *rpairs, int rp_cap);
+               kkt_krylov_report *rep, double *hist, int hist_cap, double *rpairs, int rp_cap,
+               const std::function<int()> *post = nullptr);
 
 }  // namespace kkt

@@ -1197,7 +1197,8 @@ static int resume_handed(Device *dev, Runner &R, const Call &C, const std::vecto
 
 int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout, const kkt_krylov_cfg *cfg,
                int mode, const int *active_in, const kkt_linop *opK, const kkt_linop *opM,
-               kkt_krylov_report *rep, double *hist, int hist_cap, double *rpairs, int rp_cap) {
+               kkt_krylov_report *rep, double *hist, int hist_cap, double *rpairs, int rp_cap,
+               const std::function<int()> *post) {
   DevPlan &d = dev->d;
   const int nb = d.nb;
   if (cfg->m < 1) return set_error(KKT_ERR_BAD_ARG, "restart length m must be >= 1");
@@ -1246,6 +1247,9 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout, con
     FgGraph *G = nullptr;
     if ((rc = get_graph(dev, R, C, G))) return rc;
     CUDA_TRY(cudaGraphLaunch(G->exec, dev->stream));
+    // the copies of x behind the graph, then the call's one synchronisation
+    if (xout != K.sx) CUDA_TRY(cudaMemcpyAsync(xout, K.sx, vbytes, cudaMemcpyDeviceToDevice, dev->stream));
+    if (post && (rc = (*post)())) return rc;
     CUDA_TRY(cudaStreamSynchronize(dev->stream));
     const int *ctrl = K.pin_ctrl;
     dev->launches += G->l_pro + (long long)ctrl[cfg->m + 1] * G->l_cyc + (long long)ctrl[cfg->m + 2] * G->l_iter +
@@ -1266,8 +1270,12 @@ int dev_fgmres(Device *dev, const double *b, const double *x0, double *xout, con
       src_rpcap[handed[i]] = HK.c_rpcap;
     }
   }
-  if (!host_loop && xout != K.sx) {
-    CUDA_TRY(cudaMemcpyAsync(xout, K.sx, vbytes, cudaMemcpyDeviceToDevice, dev->stream));
+  if (!handed.empty()) {  // the helpers changed x: repeat the copies
+    if (xout != K.sx) CUDA_TRY(cudaMemcpyAsync(xout, K.sx, vbytes, cudaMemcpyDeviceToDevice, dev->stream));
+    if (post && (rc = (*post)())) return rc;
+    CUDA_TRY(cudaStreamSynchronize(dev->stream));
+  } else if (host_loop && post) {
+    if ((rc = (*post)())) return rc;
     CUDA_TRY(cudaStreamSynchronize(dev->stream));
   }
   // unpack the report blocks: [nbp][FG_REP] | history [nbp][hcap] | restart pairs [nbp][rpcap][2]

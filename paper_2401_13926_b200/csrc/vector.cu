@@ -42,6 +42,53 @@ __device__ __forceinline__ double row_dot(const DevPlan &d, const double *__rest
   return d.sym_lower ? __dadd_rn(s1, s2) : s1;
 }
 
+// The same row sums for the 32 rows r0 .. r0+31 of a warp (lane l: row r0 + l), with the
+// tile's entries loaded coalesced (lanes over entries, 8 per lane in flight per 256-entry
+// chunk) and their products staged in shared memory; each lane then adds its own row's
+// products in entry order (the split as above), so every row is bitwise row_dot's.  The
+// kernels keep the thread -> row mapping of the per-row loop (thread t of block b: rows
+// 256 b + t + k * 256 * grid), so the norm partials are bitwise unchanged too.
+constexpr int TILE_CHUNK = 256;
+__device__ __forceinline__ double tile_dot(const DevPlan &d, const double *__restrict__ av,
+                                           const double *__restrict__ x, int r0, int lane,
+                                           double *__restrict__ prod) {
+  const int *__restrict__ ci = d.A_ci;
+  const int r = r0 + lane;
+  const bool valid = r < d.n;
+  const int rb = valid ? d.A_rp[r] : 0, re = valid ? d.A_rp[r + 1] : 0, rs = valid ? d.A_split[r] : 0;
+  const int e0 = __shfl_sync(0xffffffffu, rb, 0);
+  const int e1 = __shfl_sync(0xffffffffu, re, min(31, d.n - 1 - r0));
+  double s1 = 0.0, s2 = 0.0;
+  for (int c0 = e0; c0 < e1; c0 += TILE_CHUNK) {
+    const int cn = min(TILE_CHUNK, e1 - c0);
+    int c[8];
+    double v[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = lane + 32 * u;
+      if (q < cn) {
+        c[u] = ci[c0 + q];
+        v[u] = av[c0 + q];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (lane + 32 * u < cn) xv[u] = x[c[u]];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (lane + 32 * u < cn) prod[lane + 32 * u] = __dmul_rn(v[u], xv[u]);
+    __syncwarp();
+    const int b = max(rb, c0), e = min(re, c0 + cn);
+    for (int q = b; q < e; ++q) {
+      const double t = prod[q - c0];
+      if (d.sym_lower && q >= rs) s2 = __dadd_rn(s2, t);
+      else s1 = __dadd_rn(s1, t);
+    }
+    __syncwarp();
+  }
+  return d.sym_lower ? __dadd_rn(s1, s2) : s1;
+}
+
 // out = K x, or out = bsub - K x; optional ||out||^2 block partials [nb][rb].
 __global__ void __launch_bounds__(RED_THREADS) k_spmv(DevPlan d, const double *__restrict__ x,
                                                       double *__restrict__ out,
@@ -55,14 +102,20 @@ __global__ void __launch_bounds__(RED_THREADS) k_spmv(DevPlan d, const double *_
   x += off;
   out += off;
   if (bsub) bsub += off;
+  __shared__ double prod_all[RED_THREADS / 32][TILE_CHUNK];
+  double *prod = prod_all[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
   double loc = 0.0;
   bool bad = false;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x) {
-    const double y = row_dot(d, av, x, i);
-    if (!isfinite(y)) bad = true;
-    const double o = bsub ? __dsub_rn(bsub[i], y) : y;
-    out[i] = o;
-    loc = __dadd_rn(loc, __dmul_rn(o, o));
+  for (int r0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); r0 < d.n; r0 += gridDim.x * blockDim.x) {
+    const int i = r0 + lane;
+    const double y = tile_dot(d, av, x, r0, lane, prod);
+    if (i < d.n) {
+      if (!isfinite(y)) bad = true;
+      const double o = bsub ? __dsub_rn(bsub[i], y) : y;
+      out[i] = o;
+      loc = __dadd_rn(loc, __dmul_rn(o, o));
+    }
   }
   if (bad) atomicOr(&d.scal[(size_t)sys * SCAL_STRIDE + SC_NONFINITE], 1ull);
   if (nrm_out) {
@@ -95,14 +148,21 @@ __global__ void __launch_bounds__(RED_THREADS) k_resid_stats(DevPlan d, const do
   r += off;
   x += off;
   double *part = partials + (size_t)sys * 5 * nblk;
+  __shared__ double prod_all[RED_THREADS / 32][TILE_CHUNK];
+  double *prod = prod_all[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
   double e2 = 0.0, emax = 0.0, x2 = 0.0, xmax = 0.0, r2 = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x) {
-    const double ei = __dsub_rn(r[i], row_dot(d, av, x, i));
-    e2 += ei * ei;
-    emax = fmax(emax, fabs(ei));
-    x2 += x[i] * x[i];
-    xmax = fmax(xmax, fabs(x[i]));
-    r2 += r[i] * r[i];
+  for (int r0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); r0 < d.n; r0 += gridDim.x * blockDim.x) {
+    const int i = r0 + lane;
+    const double y = tile_dot(d, av, x, r0, lane, prod);
+    if (i < d.n) {
+      const double ei = __dsub_rn(r[i], y);
+      e2 += ei * ei;
+      emax = fmax(emax, fabs(ei));
+      x2 += x[i] * x[i];
+      xmax = fmax(xmax, fabs(x[i]));
+      r2 += r[i] * r[i];
+    }
   }
   double t;
   t = block_sum<RED_THREADS>(e2, sh);
