@@ -75,6 +75,9 @@ def parse(argv=None):
     ap.add_argument("--no-fixed", action="store_true")
     ap.add_argument("--no-handoff", action="store_true")
     ap.add_argument("--kernel-reps", type=int, default=3)
+    ap.add_argument("--imbalance-frac", type=float, default=1.0,
+                    help="fraction of buses with an imbalance slack; < 1 gives the reference's "
+                         "off-diagonal pivoting regime (acopf.build_pattern)")
     return ap.parse_args(argv)
 
 
@@ -269,7 +272,7 @@ def setup(args):
     from paper_2401_13926_b200 import factorize, to_general
     from paper_2401_13926_b200.acopf import ACOPF_CONFIGS, build_pattern, system_values
     t0 = time.perf_counter()
-    pat = build_pattern(ACOPF_CONFIGS[args.config], 0)
+    pat = build_pattern(ACOPF_CONFIGS[args.config], 0, imbalance_frac=args.imbalance_frac)
     gen_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     f, _ = factorize(to_general(pat.K.with_values(system_values(pat, 0, 0))))
@@ -608,8 +611,9 @@ def main():
             cpu1 = float(np.mean(per) * 1e3)
         mean1, e2e_mean1 = float(np.mean(lat)), float(np.mean(e2e1))
         sequence = {
-            "workload": f"configs[2]: systems 1..{M - 1} of value stream 0 in barrier order "
-                        "on a single-system handle (refactor + lu_solve + refine_fgmres each)",
+            "workload": f"{args.config} sequence (configs[2] shape at activsg10k): systems 1.."
+                        f"{M - 1} of value stream 0 in barrier order on a single-system handle "
+                        "(refactor + lu_solve + refine_fgmres each)",
             "ms_per_system_mean": mean1, "ms_median": float(np.median(lat)),
             "e2e_ms_per_system_mean": e2e_mean1,
             "ms_per_system": [round(x, 3) for x in lat],
@@ -646,7 +650,8 @@ def main():
                 "N": N, "nnz_lower": nnz_lower, "nnz_general": nnz_g,
                 "nnz_L": nL, "nnz_U": nU, "refactor_flops_per_system": st["refactor_flops"],
                 "levels_refactor_L_U": [lev_ref, lev_L, lev_U],
-                "offdiag_pivots": st["offdiag_pivots"],
+                "offdiag_pivots": st["offdiag_pivots"], "imbalance_frac": args.imbalance_frac,
+                "update_pairs_per_system": st["update_pairs"],
                 "tolerance": ("delta(mu)=clamp(1e-2*mu,1e-10,1e-8) per system"
                               if args.tol == "barrier" else f"{args.delta}"),
                 "straggler_handoff": handoff,

@@ -1198,8 +1198,8 @@ int kkt_dev_step_solve(kkt_device *d, const double *r_in, double *x_out, int io_
   // so the whole step synchronises once (again after a straggler hand-off)
   const std::function<int()> post = [&]() -> int {
     const double *xs = K.sx;
-    if (il) {
-      double *dst = io_on_device ? x_out : K.w;
+    if (il) {  // (staging in w1: a straggler hand-off after this reads the batch's w)
+      double *dst = io_on_device ? x_out : K.w1;
       IL_OUT(K.sx, dst);
       xs = dst;
     }

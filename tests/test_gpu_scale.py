@@ -19,13 +19,15 @@ from large_golden import rr_floor
 pytestmark = pytest.mark.gpu
 
 CONFIGS = [("activsg200", 19), ("activsg2000", 19), ("activsg10k", 19),
+           ("activsg10k/0.95", 19),  # the off-diagonal pivoting regime at 238k (4,214 pivots)
            pytest.param("activsg70k", 19, marks=pytest.mark.slow)]
 
 
 def _setup(config):
     from paper_2401_13926_b200 import factorize, to_general
     from paper_2401_13926_b200.acopf import ACOPF_CONFIGS, build_pattern, system_values
-    pat = build_pattern(ACOPF_CONFIGS[config], 0)
+    config, _, frac = config.partition("/")
+    pat = build_pattern(ACOPF_CONFIGS[config], 0, imbalance_frac=float(frac or 1.0))
     K0 = pat.K.with_values(system_values(pat, 0, 0))
     f, _ = factorize(to_general(K0))
     return pat, K0, f
@@ -49,6 +51,8 @@ def test_full_size_against_oracle(config, k):
     from paper_2401_13926_b200.acopf import MU_STEP, system_rhs, system_values
     from paper_2401_13926_b200.refine import BarrierTiedTolerance
     pat, K0, f = _setup(config)
+    if "/" in config:  # row_perm != col_perm (direct_lu.py:209-223)
+        assert f.stats["offdiag_pivots"] > 0
     of, ex = _oracle(f, K0)
     vals = system_values(pat, k, 0)
     r = system_rhs(pat, k, 0)
@@ -82,6 +86,7 @@ def test_full_size_against_oracle(config, k):
 
 
 @pytest.mark.parametrize("config,nb", [("activsg200", 4), ("activsg10k", 4), ("activsg2000", 40),
+                                       ("activsg10k/0.95", 4),
                                        pytest.param("activsg70k", 8, marks=pytest.mark.slow)])
 def test_full_size_batch_equals_single(config, nb):
     """The interleaved batch reproduces each system's single-system factors and solve (nb = 40:
