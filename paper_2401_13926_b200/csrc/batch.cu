@@ -1129,16 +1129,19 @@ __global__ void __launch_bounds__(256) k_b_diag_stats(DevPlan d) {
 // order.  Each warp prefetches its NEXT task's static data (row pointers, the first chunk's
 // column indices and values, the initial value and pivot) while the current task waits on
 // its dependency, so a task's critical path is the dependency's y values only.
-constexpr int RC = 6;  // entries of a row prefetched with the task
+// RC: entries of a row prefetched with the task.  B_RC = 6: 4 and 8 measured 1.89 / 1.89 ms
+// vs 1.86 for the batched pair at 10k x 64 (registers 80 / 128 vs 108-114)
+constexpr int B_RC = 6;
+template <int RC>
 struct RowTask {
   int r, cr, beg, end;
   int cols[RC];
   double vs[RC], ys[RC], acc, piv;
 };
 
-template <bool IS_U>
+template <bool IS_U, int RC>
 __device__ __forceinline__ void row_prefetch(const DevPlan &d, const double *__restrict__ b, int idx,
-                                             int sys, bool act, RowTask &t) {
+                                             int sys, bool act, RowTask<RC> &t) {
   const int *order = IS_U ? d.U_grid_order : d.L_grid_order;
   const int *rp = IS_U ? d.Urp : d.Lrp;
   const int *ci = IS_U ? d.Uci : d.Lci;
@@ -1159,7 +1162,7 @@ __device__ __forceinline__ void row_prefetch(const DevPlan &d, const double *__r
   }
 }
 
-template <bool IS_U>
+template <bool IS_U, int RC>
 __global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__restrict__ b,
                                                      double *__restrict__ xout) {
   constexpr int C = RC;  // entries per chunk
@@ -1176,7 +1179,7 @@ __global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__
   const int gstart = IS_U ? 0 : d.L_sync_ptr[d.L_nsync];  // leading levels ran row-parallel
   // speculative y loads of a prefetched task's first chunk (the non-critical dependencies
   // are normally published already; sentinels are re-read after the critical wait)
-  auto load_ys = [&](RowTask &t, int sys, bool act) {
+  auto load_ys = [&](RowTask<RC> &t, int sys, bool act) {
     if (act) {
 #pragma unroll
       for (int q = 0; q < C; ++q)
@@ -1185,13 +1188,13 @@ __global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__
   };
   // one row: wait for its critical dependency, sum in the reference order, publish; the
   // next row's static data is prefetched into `n` first and its y loads issued at the end
-  auto run_row = [&](int task, RowTask &t, RowTask &n) {
+  auto run_row = [&](int task, RowTask<RC> &t, RowTask<RC> &n) {
     const int sys = (task % ngroups) * 32 + lane;
     const bool act = sys_active(d, sys);
     const int nxt = task + nwarps;
     const int nsys = (nxt % ngroups) * 32 + lane;
     const bool nact = nxt < ntask && sys_active(d, nsys);
-    if (nxt < ntask) row_prefetch<IS_U>(d, b, nxt / ngroups, nsys, nact, n);
+    if (nxt < ntask) row_prefetch<IS_U, RC>(d, b, nxt / ngroups, nsys, nact, n);
     const unsigned amask = __ballot_sync(FULL, act);
     if (amask) {
       const bool tr = d.trace_step && sys == 0;  // timeline of system 0: {start, crit ready}
@@ -1240,10 +1243,10 @@ __global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__
   };
   // two task buffers used alternately (no register copy of a whole task)
   int task = gstart * ngroups + gwarp;
-  RowTask ta, tb;
+  RowTask<RC> ta, tb;
   if (task < ntask) {
     const int sys = (task % ngroups) * 32 + lane;
-    row_prefetch<IS_U>(d, b, task / ngroups, sys, sys_active(d, sys), ta);
+    row_prefetch<IS_U, RC>(d, b, task / ngroups, sys, sys_active(d, sys), ta);
     load_ys(ta, sys, sys_active(d, sys));
   }
   while (task < ntask) {
@@ -1342,7 +1345,7 @@ static cudaError_t b_launch_grid(const DevPlan &d, const double *b, double *x, i
   }
   const int groups = d.nbp >> 5;
   (void)groups;  // (G > 1 measured slower: fewer, longer tasks)
-  k_b_trsv_grid<IS_U><<<grid_blocks, 256, 0, s>>>(d, b, x);
+  k_b_trsv_grid<IS_U, B_RC><<<grid_blocks, 256, 0, s>>>(d, b, x);
   return cudaGetLastError();
 }
 
@@ -1837,8 +1840,8 @@ cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_
   occ((const void *)k_b_trsv_levels<true>);
   const int groups = nbp >> 5;  // occupancy of the variant b_launch_grid picks
   (void)groups;
-  occ((const void *)k_b_trsv_grid<false>);
-  occ((const void *)k_b_trsv_grid<true>);
+  occ((const void *)k_b_trsv_grid<false, B_RC>);
+  occ((const void *)k_b_trsv_grid<true, B_RC>);
   *trsv_blocks_per_sm = m;
   return e;
 }
