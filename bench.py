@@ -484,6 +484,23 @@ def main():
     torch.cuda.synchronize()
     e2e_total = reduce_max((time.perf_counter() - t0) * 1e3, dist, dev.device)
     e2e_value = e2e_total / n_job
+    # the PCIe floor of the e2e leg: this box's pinned H2D bandwidth (one step's input size)
+    h2d_bytes = 8 * B * (nnz_lower + N)
+    hsrc = hp[ks[0]][0]
+    with torch.cuda.stream(stream):
+        ddst = torch.empty(hsrc.shape, dtype=torch.float64, device=dev.device)
+    for _ in range(2):
+        ddst.copy_(hsrc, non_blocking=True)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        a.record(stream)
+        for _ in range(3):
+            ddst.copy_(hsrc, non_blocking=True)
+        b.record(stream)
+    b.synchronize()
+    h2d_gbs = 3 * hsrc.numel() * 8 / (a.elapsed_time(b) * 1e6)
+    del ddst
 
     # ---- fixed delta = 1e-10 (the reference's RefinementConfig default order of magnitude) ----
     fixed = None
@@ -667,8 +684,10 @@ def main():
             },
             "check": check,
             "e2e": {"value": e2e_value, "unit": "ms/system",
-                    "h2d_bytes_per_step": 8 * B * (nnz_lower + N),
-                    "d2h_bytes_per_step": 8 * B * N},
+                    "h2d_bytes_per_step": h2d_bytes,
+                    "d2h_bytes_per_step": 8 * B * N,
+                    "h2d_gbs_measured": h2d_gbs,
+                    "pcie_floor_ms_per_system": h2d_bytes / (h2d_gbs * 1e6) / B},
             "sequence": sequence,
             "fixed_delta": fixed,
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": kd["GBs"], "peak": peak,

@@ -19,7 +19,7 @@ from paper_2401_13926_b200.device import DeviceSystem
 cfg = sys.argv[1]
 Bs = [int(b) for b in sys.argv[2].split(",")]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
-pat = build_pattern(ACOPF_CONFIGS[cfg], 0)
+pat = build_pattern(ACOPF_CONFIGS[cfg], 0, imbalance_frac=float(os.environ.get("IMBALANCE_FRAC", "1.0")))
 f, _ = factorize(to_general(pat.K.with_values(system_values(pat, 0, 0))))
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 LOWER = nat.LAYOUT_SYMMETRIC_LOWER

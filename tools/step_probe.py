@@ -15,7 +15,7 @@ from paper_2401_13926_b200.device import DeviceSystem
 
 cfg, B, k = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
-args = bench.parse(["--config", cfg])
+args = bench.parse(["--config", cfg, "--imbalance-frac", os.environ.get("IMBALANCE_FRAC", "1.0")])
 pat, f, _, _ = bench.setup(args)
 vals, rhs, mu = bench.make_batch(pat, list(range(B)), k)
 delta = bench.policy_of(args)(mu)

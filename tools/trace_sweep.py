@@ -27,7 +27,8 @@ ref = np.zeros(2 * n, dtype=np.uint64)
 tri = np.zeros(2 * n, dtype=np.uint64)
 nat.check(dev.lib.kkt_dev_trace(dev.h, ref.ctypes.data_as(C.c_void_p), tri.ctypes.data_as(C.c_void_p)))
 info = dev.info()
-for name, T, off in (("L", info["L_tail_rows"], 0), ("U", info["U_head_rows"], 4 * ((info["L_tail_rows"] + 31) // 32))):
+# the sweeps write {top, tiles ready, y ready, end} per block at trace_trsv + (U ? n : 0) + p + 4 c
+for name, T, off in (("L", info["L_tail_rows"], info["pL"]), ("U", info["U_head_rows"], n + info["pU"])):
     nb = (T + 31) // 32
     t = tri[off:off + 4 * nb].astype(np.int64).reshape(nb, 4)
     if not t.any():
