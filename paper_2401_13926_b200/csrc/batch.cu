@@ -1132,6 +1132,16 @@ __global__ void __launch_bounds__(256) k_b_diag_stats(DevPlan d) {
 // RC: entries of a row prefetched with the task.  B_RC = 6: 4 and 8 measured 1.89 / 1.89 ms
 // vs 1.86 for the batched pair at 10k x 64 (registers 80 / 128 vs 108-114)
 constexpr int B_RC = 6;
+// KKT_B_GRIDV selects the grid solve's (chunk, CTAs per SM); read at configure and launch
+// alike, so the persistent grid is always sized to the variant that runs.  The U grid phase
+// walks ~236k rows in 196 levels (the L front takes its wide levels row-parallel), so tasks
+// in flight matter more than entries per chunk: batched pair at 10k x 64 / x 128 —
+// 0: (6, 2) 1.85 / 2.82 ms; 1: (4, 3) 1.77 / 2.54; 2: (6, 3, spilling) 1.81 / 2.66;
+// 3 (default): (4, 4) 1.71 / 2.45; 4: (2, 4) 1.86 / 2.72.
+static int grid_variant() {
+  const char *e = std::getenv("KKT_B_GRIDV");
+  return e ? std::atoi(e) : 3;
+}
 template <int RC>
 struct RowTask {
   int r, cr, beg, end;
@@ -1162,8 +1172,8 @@ __device__ __forceinline__ void row_prefetch(const DevPlan &d, const double *__r
   }
 }
 
-template <bool IS_U, int RC>
-__global__ void __launch_bounds__(256) k_b_trsv_grid(DevPlan d, const double *__restrict__ b,
+template <bool IS_U, int RC, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_b_trsv_grid(DevPlan d, const double *__restrict__ b,
                                                      double *__restrict__ xout) {
   constexpr int C = RC;  // entries per chunk
   const int lane = threadIdx.x & 31;
@@ -1345,7 +1355,13 @@ static cudaError_t b_launch_grid(const DevPlan &d, const double *b, double *x, i
   }
   const int groups = d.nbp >> 5;
   (void)groups;  // (G > 1 measured slower: fewer, longer tasks)
-  k_b_trsv_grid<IS_U, B_RC><<<grid_blocks, 256, 0, s>>>(d, b, x);
+  switch (grid_variant()) {
+    case 1: k_b_trsv_grid<IS_U, 4, 3><<<grid_blocks, 256, 0, s>>>(d, b, x); break;
+    case 2: k_b_trsv_grid<IS_U, 6, 3><<<grid_blocks, 256, 0, s>>>(d, b, x); break;
+    case 3: k_b_trsv_grid<IS_U, 4, 4><<<grid_blocks, 256, 0, s>>>(d, b, x); break;
+    case 4: k_b_trsv_grid<IS_U, 2, 4><<<grid_blocks, 256, 0, s>>>(d, b, x); break;
+    default: k_b_trsv_grid<IS_U, B_RC><<<grid_blocks, 256, 0, s>>>(d, b, x);
+  }
   return cudaGetLastError();
 }
 
@@ -1840,8 +1856,14 @@ cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_
   occ((const void *)k_b_trsv_levels<true>);
   const int groups = nbp >> 5;  // occupancy of the variant b_launch_grid picks
   (void)groups;
-  occ((const void *)k_b_trsv_grid<false, B_RC>);
-  occ((const void *)k_b_trsv_grid<true, B_RC>);
+  // the persistent grid's co-residency: the occupancy of the variant b_launch_grid runs
+  switch (grid_variant()) {
+    case 1: occ((const void *)k_b_trsv_grid<false, 4, 3>); occ((const void *)k_b_trsv_grid<true, 4, 3>); break;
+    case 2: occ((const void *)k_b_trsv_grid<false, 6, 3>); occ((const void *)k_b_trsv_grid<true, 6, 3>); break;
+    case 3: occ((const void *)k_b_trsv_grid<false, 4, 4>); occ((const void *)k_b_trsv_grid<true, 4, 4>); break;
+    case 4: occ((const void *)k_b_trsv_grid<false, 2, 4>); occ((const void *)k_b_trsv_grid<true, 2, 4>); break;
+    default: occ((const void *)k_b_trsv_grid<false, B_RC>); occ((const void *)k_b_trsv_grid<true, B_RC>);
+  }
   *trsv_blocks_per_sm = m;
   return e;
 }
