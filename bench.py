@@ -576,7 +576,7 @@ def main():
     if os.path.exists(tp):
         tk = json.load(open(tp))["kernels"]
         fam = {"refactor": ["k_b_refactor", "k_b_refactor_tma<"], "spmv": ["k_b_spmv"],
-               "trisolve_pair": ["k_b_trsv_grid<0>", "k_b_trsv_grid<1>", "k_trsv_blocked<0, 1,",
+               "trisolve_pair": ["k_b_trsv_grid<0,", "k_b_trsv_grid<1,", "k_trsv_blocked<0, 1,",
                                  "k_trsv_blocked<1, 1,"]}[dom]
         # a member ending in "<" or "," matches any instantiation of that template
         hit = [[k for k in tk if (k.startswith(f) if f.endswith(("<", ",")) else k == f)] for f in fam]

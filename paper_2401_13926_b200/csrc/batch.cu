@@ -1132,8 +1132,8 @@ __global__ void __launch_bounds__(256) k_b_diag_stats(DevPlan d) {
 // RC: entries of a row prefetched with the task.  B_RC = 6: 4 and 8 measured 1.89 / 1.89 ms
 // vs 1.86 for the batched pair at 10k x 64 (registers 80 / 128 vs 108-114)
 constexpr int B_RC = 6;
-// KKT_B_GRIDV selects the grid solve's (chunk, CTAs per SM); read at configure and launch
-// alike, so the persistent grid is always sized to the variant that runs.  The U grid phase
+// KKT_B_GRIDV selects the grid solve's (chunk, CTAs per SM), read once when a handle is
+// created (DevPlan::b_gridv): the persistent grid is sized to, and launched with, that variant.  The U grid phase
 // walks ~236k rows in 196 levels (the L front takes its wide levels row-parallel), so tasks
 // in flight matter more than entries per chunk: batched pair at 10k x 64 / x 128 —
 // 0: (6, 2) 1.85 / 2.82 ms; 1: (4, 3) 1.77 / 2.54; 2: (6, 3, spilling) 1.81 / 2.66;
@@ -1355,7 +1355,7 @@ static cudaError_t b_launch_grid(const DevPlan &d, const double *b, double *x, i
   }
   const int groups = d.nbp >> 5;
   (void)groups;  // (G > 1 measured slower: fewer, longer tasks)
-  switch (grid_variant()) {
+  switch (d.b_gridv) {
     case 1: k_b_trsv_grid<IS_U, 4, 3><<<grid_blocks, 256, 0, s>>>(d, b, x); break;
     case 2: k_b_trsv_grid<IS_U, 6, 3><<<grid_blocks, 256, 0, s>>>(d, b, x); break;
     case 3: k_b_trsv_grid<IS_U, 4, 4><<<grid_blocks, 256, 0, s>>>(d, b, x); break;
@@ -1835,7 +1835,10 @@ static dim3 row_grid(const DevPlan &d, int per_group) {
 }
 static const dim3 ROW_BLOCK(32, BY);
 
-cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm) {
+int b_grid_variant() { return grid_variant(); }
+
+cudaError_t b_configure(int nbp, size_t refactor_smem, int gridv, int *refactor_blocks_per_sm,
+                        int *trsv_blocks_per_sm) {
   const int sm = (int)refactor_smem;
   cudaError_t e = cudaFuncSetAttribute(k_b_refactor, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   if (e == cudaSuccess)
@@ -1857,7 +1860,7 @@ cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_
   const int groups = nbp >> 5;  // occupancy of the variant b_launch_grid picks
   (void)groups;
   // the persistent grid's co-residency: the occupancy of the variant b_launch_grid runs
-  switch (grid_variant()) {
+  switch (gridv) {
     case 1: occ((const void *)k_b_trsv_grid<false, 4, 3>); occ((const void *)k_b_trsv_grid<true, 4, 3>); break;
     case 2: occ((const void *)k_b_trsv_grid<false, 6, 3>); occ((const void *)k_b_trsv_grid<true, 6, 3>); break;
     case 3: occ((const void *)k_b_trsv_grid<false, 4, 4>); occ((const void *)k_b_trsv_grid<true, 4, 4>); break;

@@ -605,7 +605,8 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
     const size_t smem2 = d.ct_mode == 3 ? b_tma_smem(std::max(d.h_xp, 1), d.tma_ns, d.tma_stg)
                                         : b_cta_smem(std::max(d.h_xp, 1), d.ct_sc);
     int rbps2 = 0;
-    CUDA_TRY(b_configure(nbp, dev->refactor_smem, &rbps, &tbps));
+    d.b_gridv = b_grid_variant();
+    CUDA_TRY(b_configure(nbp, dev->refactor_smem, d.b_gridv, &rbps, &tbps));
     if (d.ct_mode == 3) {
       CUDA_TRY(b_tma_configure(d.tma_ns, d.tma_stg, d.tma_e, smem2, &rbps2));
       CUDA_TRY(b_tma_maps(d));

@@ -100,6 +100,7 @@ struct DevPlan {
   int L_nglev = 0, U_nglev = 0;
   unsigned *gbar = nullptr;                   // grid barrier {count, generation}
   int b_levelsync = 0;  // batched grid phases level-synchronous (KKT_B_LEVELSYNC=1; slower here)
+  int b_gridv = 3;      // batched grid-solve variant the persistent grid was sized for
   int sweep_maxL, sweep_maxU;
   SweepDev swL, swU;                        // blocked sweeps of the trailing blocks
   double *Lv, *Uv;                          // [nb][nnz_L], [nb][nnz_U] (CSR order)
@@ -201,7 +202,9 @@ constexpr int B_XBUDGET2 = 2304;  // ... for the wide separator columns (second 
 constexpr int B_STAGE2 = 768;
 constexpr int B_WARPS = 4;       // warps per refactor CTA
 size_t b_refactor_smem(int xbudget, int stage);
-cudaError_t b_configure(int nbp, size_t refactor_smem, int *refactor_blocks_per_sm, int *trsv_blocks_per_sm);
+int b_grid_variant();  // KKT_B_GRIDV (batch.cu)
+cudaError_t b_configure(int nbp, size_t refactor_smem, int gridv, int *refactor_blocks_per_sm,
+                        int *trsv_blocks_per_sm);
 cudaError_t b_launch_expand_norms(const DevPlan &d, cudaStream_t s);
 cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blocks2, size_t smem2,
                               cudaStream_t s, long long *launches, cudaStream_t s2 = nullptr,

@@ -26,7 +26,13 @@ pytestmark = pytest.mark.gpu
     ("standard_trace", 9, {"KKT_B_SPLIT_NP": "4", "KKT_B_TMA": "3,160"}),
     ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TAIL_ORDER": "1"}),
     ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_DIRECT": "1"}),
-    ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_E": "64"})])
+    ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_E": "64"}),
+    # solve variants: grid-solve (chunk, CTAs/SM), sweep look-ahead / width, U head prefix
+    ("acopf_small", 33, {"KKT_B_GRIDV": "0"}), ("standard_trace", 9, {"KKT_B_GRIDV": "1"}),
+    ("acopf_small", 40, {"KKT_B_GRIDV": "2"}), ("acopf_small", 33, {"KKT_B_GRIDV": "4"}),
+    ("acopf_small", 33, {"KKT_SWEEP_AHEAD": "1"}), ("standard_trace", 9, {"KKT_SWEEP_AHEAD": "1"}),
+    ("acopf_small", 33, {"KKT_SWEEP_THREADS": "512"}), ("acopf_small", 33, {"KKT_U_PARTIAL": "0"}),
+    ("acopf_small", 33, {"KKT_B_SPMV_TILES": "1"})])
 def test_batch_refactor_solve_bitwise(case, nb, env, monkeypatch):
     """env forces the alternative replay kernels onto small cases: KKT_B_SPLIT_NP (4-warp CTA
     tasks for the wide columns), KKT_B_HEAVY_NP (pull-form CTA per 32 systems)."""

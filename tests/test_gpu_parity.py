@@ -192,3 +192,21 @@ def test_harness_rows_device_mode(case):
             assert abs(row.ir_iterations - ref[i, 4]) <= 1, (mode, i)
             assert row.rr <= max(1.5 * ref[i, 3], 4 * EPS), (mode, i, row.rr, ref[i, 3])
             assert row.converged
+
+
+@pytest.mark.parametrize("env", [{"KKT_GRID_WAIT": "0"}, {"KKT_U_PARTIAL": "0"},
+                                 {"KKT_SWEEP_AHEAD": "1"}, {"KKT_SWEEP_NOSTAGE": "1"},
+                                 {"KKT_SWEEP_THREADS": "512"}, {"KKT_TRSV_BLOCKS": "148"}])
+@pytest.mark.parametrize("case", ["standard_trace", "acopf_small"])
+def test_single_system_solve_variants_bitwise(case, env, monkeypatch):
+    """The single-system solve's alternative schedules (grid critical wait, U head prefix,
+    sweep variants, a reduced persistent grid as the straggler helpers use) stay bitwise."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = golden(case)
+    f, _ = factorize(to_general(lower_matrix(g, 0)))
+    M = g["K_values"].shape[0]
+    for i in (M - 2, M - 1):
+        refactorize(f, to_general(lower_matrix(g, i)))
+        assert np.array_equal(lu_solve(f, g["rhs"][i]), g["x0"][i]), (i, env)
+    f.close()
