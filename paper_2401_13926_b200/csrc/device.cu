@@ -499,13 +499,12 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   UP(d.Up, to_i32(h.Up));
   UP(d.Lmap, h.Lmap);
   UP(d.Umap, h.Umap);
-  if (nbp > 1) {  // the batched replay derives L indices from the step metadata
+  {  // the replays derive L indices from the step metadata (L(:,k) is contiguous in Lx); the
+     // buffer holds int32 slots for their cp.async staging
     d.upd_slot32 = d.upd_lidx;
     d.upd_lidx = nullptr;
     const std::vector<int> slot32 = narrow<uint16_t, int>(h.upd_slot);
     UP(d.upd_slot32, slot32);
-  } else {
-    UP(d.upd_lidx, h.upd_lidx);
   }
   UP(d.so_meta, h.so_meta);
   UP(d.upd_slot, h.upd_slot);

@@ -75,6 +75,56 @@ __device__ __forceinline__ double patch_floor(const DevPlan &d, int b) {
                    __longlong_as_double((long long)d.scal[(size_t)b * SCAL_STRIDE + SC_INFNORM]));
 }
 
+// Stage buffers: two per warp, each REFACTOR_BUF update-pair values + REFACTOR_BUF_I slots
+// (the same shared memory as one 512-pair buffer had).
+constexpr int REFACTOR_BUF = REFACTOR_STAGE / 2;
+constexpr int REFACTOR_BUF_I = REFACTOR_STAGE / 2;
+
+// A chunk of replay steps whose pairs fit a stage buffer (or one step wider than it: big).
+struct StChunk {
+  int t0, nsteps, npairs, pair0;
+  bool big;
+  int4 m;     // this lane's step metadata {slot of k, |L(:,k)|, first pair, first L index}
+  int incl;   // inclusive prefix of the pair counts
+};
+
+__device__ __forceinline__ StChunk st_meta(const DevPlan &d, int t0, int t_end, int lane) {
+  StChunk c;
+  c.t0 = t0;
+  const int t = t0 + lane;
+  c.m = t < t_end ? d.so_meta[t] : make_int4(0, 0, 0, 0);
+  int incl = c.m.y;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  c.incl = incl;
+  const unsigned fits = __ballot_sync(0xffffffffu, t < t_end && incl <= REFACTOR_BUF);
+  c.nsteps = __popc(fits);
+  c.big = c.nsteps == 0;  // a single step with more pairs than a stage buffer
+  if (c.big) c.nsteps = 1;
+  c.pair0 = __shfl_sync(0xffffffffu, c.m.z, 0);
+  c.npairs = c.big ? 0 : __shfl_sync(0xffffffffu, incl, c.nsteps - 1);
+  return c;
+}
+
+// cp.async of a chunk's slots (contiguous int32) and L values (per step a contiguous
+// L(:,k)); one commit group per chunk (empty for a big step).
+__device__ __forceinline__ void st_issue(const DevPlan &d, const StChunk &c, double *stl, int *sts,
+                                         const double *Lx, int lane) {
+  if (!c.big) {
+    for (int p = lane; p < c.npairs; p += 32) cp_async4(&sts[p], &d.upd_slot32[c.pair0 + p]);
+    for (int i = 0; i < c.nsteps; ++i) {
+      const int cnt = __shfl_sync(0xffffffffu, c.m.y, i);
+      const int off = __shfl_sync(0xffffffffu, c.incl - c.m.y, i);
+      const int lbk = __shfl_sync(0xffffffffu, c.m.w, i);
+      for (int e = lane; e < cnt; e += 32) cp_async8(&stl[off + e], &Lx[lbk + e]);
+    }
+  }
+  cp_async_commit();
+}
+
 __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
@@ -102,65 +152,47 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
     const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
     const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
     const int np = nu + 1 + nl;
+    // for k in so(j) (topological): x[Li(k)] -= Lx(k) * x[k]                  (:324-326)
+    // Chunks of steps whose update pairs fit a stage buffer are staged with cp.async, the next
+    // chunk's copies in flight while this one replays (two buffers).  L(:,k) is the contiguous
+    // Lx[Lp[k], Lp[k+1]) and a chunk's slots are contiguous, so a chunk is one round trip.
+    const int t_end = d.so_ptr[j + 1];
+    StChunk cur = st_meta(d, d.so_ptr[j], t_end, lane);
+    st_issue(d, cur, st_l, st_s, Lx, lane);  // in flight during the A scatter
     for (int s = lane; s < np; s += 32) x[s] = 0.0;
     __syncwarp();
     // x[a_tgt] = avals[a_src]                                                 (:323)
     for (int q = d.ap_ptr[j] + lane; q < d.ap_ptr[j + 1]; q += 32) x[d.a_slot[q]] = av[d.a_src[q]];
     __syncwarp();
-    // for k in so(j) (topological): x[Li(k)] -= Lx(k) * x[k]                  (:324-326)
-    const int t_end = d.so_ptr[j + 1];
-    int t0 = d.so_ptr[j];
-    while (t0 < t_end) {
-      const int t = t0 + lane;
-      int4 m = make_int4(0, 0, 0, 0);
-      if (t < t_end) m = d.so_meta[t];
-      // inclusive scan of the pair counts => chunk of steps whose pairs fit the stage
-      int incl = m.y;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const unsigned fits = __ballot_sync(0xffffffffu, t < t_end && incl <= REFACTOR_STAGE);
-      int nsteps = __popc(fits);
-      const bool big = nsteps == 0;  // a single step with more pairs than the stage
-      if (big) nsteps = 1;
-      const int pair0 = __shfl_sync(0xffffffffu, m.z, 0);
-      const int npairs = big ? 0 : __shfl_sync(0xffffffffu, incl, nsteps - 1);
-      // stage: 4 independent gathers per lane in flight before the shared stores
-      for (int p0 = 0; p0 < npairs; p0 += 128) {
-        double lv[4];
-        int sv[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int p = p0 + q * 32 + lane;
-          if (p < npairs) {
-            lv[q] = ld_relaxed_f64(&Lx[d.upd_lidx[pair0 + p]]);
-            sv[q] = d.upd_slot[pair0 + p];
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int p = p0 + q * 32 + lane;
-          if (p < npairs) {
-            st_l[p] = lv[q];
-            st_s[p] = sv[q];
-          }
-        }
+    int buf = 0;
+    while (cur.t0 < t_end) {
+      const int tn = cur.t0 + cur.nsteps;
+      StChunk nxt;
+      nxt.t0 = tn;
+      nxt.nsteps = 0;
+      if (tn < t_end) {
+        nxt = st_meta(d, tn, t_end, lane);
+        st_issue(d, nxt, st_l + (buf ^ 1) * REFACTOR_BUF, st_s + (buf ^ 1) * REFACTOR_BUF_I, Lx, lane);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
       }
       __syncwarp();
+      double *stl = st_l + buf * REFACTOR_BUF;
+      const int *sts = st_s + buf * REFACTOR_BUF_I;
+      const int nsteps = cur.nsteps, t0 = cur.t0;
       for (int i = 0; i < nsteps; ++i) {
-        const int kslot = __shfl_sync(0xffffffffu, m.x, i);
-        const int cnt = __shfl_sync(0xffffffffu, m.y, i);
-        const int off = __shfl_sync(0xffffffffu, incl - m.y, i);
+        const int kslot = __shfl_sync(0xffffffffu, cur.m.x, i);
+        const int cnt = __shfl_sync(0xffffffffu, cur.m.y, i);
+        const int off = __shfl_sync(0xffffffffu, cur.incl - cur.m.y, i);
         const double xk = x[kslot];
-        const int lbk = __shfl_sync(0xffffffffu, m.w, i);  // L(:,k) = Lx[lbk, lbk+cnt)
-        if (!big) {
+        const int lbk = __shfl_sync(0xffffffffu, cur.m.w, i);  // L(:,k) = Lx[lbk, lbk+cnt)
+        if (!cur.big) {
           // L(:,k) not yet published when staged?  One lane waits so a column many warps
           // depend on is not polled by every lane of every consumer; then the whole step
           // is re-staged with one parallel round trip.
           bool miss = false;
-          for (int e = lane; e < cnt; e += 32) miss |= is_sentinel(st_l[off + e]);
+          for (int e = lane; e < cnt; e += 32) miss |= is_sentinel(stl[off + e]);
           const unsigned mm = __ballot_sync(0xffffffffu, miss);
           if (mm) {
             if (lane == __ffs(mm) - 1) wait_value(&Lx[lbk + cnt - 1], d.poll_ns);
@@ -171,8 +203,8 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
               if (lane + 32 * q < cnt) lv[q] = ld_relaxed_f64(&Lx[lbk + lane + 32 * q]);
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              if (lane + 32 * q < cnt) st_l[off + lane + 32 * q] = lv[q];
-            for (int e = lane + 256; e < cnt; e += 32) st_l[off + e] = ld_relaxed_f64(&Lx[lbk + e]);
+              if (lane + 32 * q < cnt) stl[off + lane + 32 * q] = lv[q];
+            for (int e = lane + 256; e < cnt; e += 32) stl[off + e] = ld_relaxed_f64(&Lx[lbk + e]);
           }
           // the targets of one step are distinct slots (R_U RMWs per lane in flight;
           // 1 measured fastest: 10k 2.89 ms vs 3.01 with 2, 3.04 with 4)
@@ -182,8 +214,8 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
 #pragma unroll
             for (int q = 0; q < R_U; ++q)
               if (e0 + 32 * q < cnt) {
-                lv[q] = st_l[off + e0 + 32 * q];
-                sl[q] = st_s[off + e0 + 32 * q];
+                lv[q] = stl[off + e0 + 32 * q];
+                sl[q] = sts[off + e0 + 32 * q];
               }
 #pragma unroll
             for (int q = 0; q < R_U; ++q)
@@ -198,7 +230,8 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
           }
           if (d.trace_step && sys == 0 && lane == 0)
             d.trace_step[t0 + i] = globaltimer() | (mm ? 1ull : 0ull);
-        } else {
+        } else {  // one step wider than a stage buffer: straight from L2
+          const int pair0 = __shfl_sync(0xffffffffu, cur.m.z, i);
           for (int e = lane; e < cnt; e += 32) {
             const double l = wait_value_backoff(&Lx[lbk + e]);
             const int s = d.upd_slot[pair0 + e];
@@ -207,8 +240,11 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
         }
         __syncwarp();
       }
-      t0 += nsteps;
+      cur = nxt;
+      buf ^= 1;
     }
+    cp_async_wait<0>();
+    __syncwarp();
     // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj; U(:,j) = x[Ui]                 (:327-344)
     // L(:,j) is what other tasks wait for: publish it first, bookkeeping after.
     double gm = 0.0;

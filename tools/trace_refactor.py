@@ -98,3 +98,37 @@ for r in range(pL):
 if hops:
     hops = np.array(hops)
     print(f"L grid hop (levels>=50): median {np.median(hops):.2f} us, p90 {np.percentile(hops, 90):.2f} us, n={hops.size}")
+# deep columns: time from the last dependency finishing to the column finishing, and how many
+# of the column's steps come after that dependency in so order (work left once it arrives)
+after, nafter, cnt_after = [], [], []
+for j in deep:
+    a, b = sop[j], sop[j + 1]
+    if b == a:
+        continue
+    ks = sod[a:b]
+    crit = int(np.argmax(en[ks]))
+    after.append(en[j] - en[ks[crit]])
+    nafter.append(b - a - crit)
+    cnt_after.append(int(sum(Lp_[k + 1] - Lp_[k] for k in ks[crit:])) if 'Lp_' in dir() else 0)
+if after:
+    after = np.array(after)
+    print(f"deep columns: last dependency -> finish median {np.median(after):.2f} us, p90 "
+          f"{np.percentile(after, 90):.2f}; steps at/after it median {np.median(nafter):.0f}, p90 "
+          f"{np.percentile(nafter, 90):.0f}; L entries of those steps median {np.median(cnt_after):.0f}")
+# per-step timing inside the deep columns: a step whose column k finished before the previous
+# step was applied is pure work (time = apply(t) - apply(t-1)); otherwise it waited for k
+work, waitd, nst = [], [], []
+for j in deep:
+    a, b = sop[j], sop[j + 1]
+    nst.append(b - a)
+    for t in range(a + 1, b):
+        k = sod[t]
+        d = stt[t] - stt[t - 1]
+        if en[k] < stt[t - 1]:
+            work.append(d)
+        else:
+            waitd.append(stt[t] - en[k])
+work, waitd = np.array(work), np.array(waitd)
+print(f"deep steps: {np.median(nst):.0f} per column (max {max(nst)}); ready steps {work.size}: median "
+      f"{np.median(work):.3f} us, sum per column {work.sum() / len(deep):.1f} us; waiting steps "
+      f"{waitd.size}: apply-after-F median {np.median(waitd):.2f} us")
