@@ -645,17 +645,18 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
     return KKT_OK;
   }
   dev->refactor_warps = 8;
-  dev->refactor_smem = refactor_smem_bytes(dev->refactor_warps, d.maxpat);
+  d.ref_buf = refactor_buf();
+  dev->refactor_smem = refactor_smem_bytes(dev->refactor_warps, d.maxpat, d.ref_buf);
   while (dev->refactor_smem > 200 * 1024 && dev->refactor_warps > 1) {
     dev->refactor_warps /= 2;
-    dev->refactor_smem = refactor_smem_bytes(dev->refactor_warps, d.maxpat);
+    dev->refactor_smem = refactor_smem_bytes(dev->refactor_warps, d.maxpat, d.ref_buf);
   }
   if (dev->refactor_smem > 220 * 1024) {
     destroy(dev);
     return set_error(KKT_ERR_BAD_SHAPE, "column pattern too large for the shared-memory workspace");
   }
   int bps = 0;
-  CUDA_TRY(refactor_configure(dev->refactor_warps, dev->refactor_smem, &bps));
+  CUDA_TRY(refactor_configure(dev->refactor_warps, dev->refactor_smem, d.ref_buf, &bps));
   dev->refactor_blocks = std::max(1, bps) * dev->sm_count;
   int tb = 0;
   CUDA_TRY(trsv_configure(&tb));

@@ -19,7 +19,6 @@ constexpr int RED_BLOCKS = 296;  // reduction blocks for one system (fixed => de
 constexpr int RED_THREADS = 256;
 constexpr double HAPPY_BREAKDOWN_RTOL = 1e-14;   // krylov.py:25
 constexpr double PATCH_RELATIVE_FLOOR = 1e-12;   // direct_lu.py:32
-constexpr int REFACTOR_STAGE = 512;              // update pairs staged per warp chunk
 constexpr int SCAL_STRIDE = 16;                  // per-system scalar block
 
 // Blocked tail sweep tables (HostSweep, plan.h)
@@ -76,6 +75,7 @@ struct DevPlan {
   int n_small_levels = 0;  // leading levels run by k_refactor_small
   int lev_ptr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // col_order offsets of those levels
   int poll_ns = 0;  // __nanosleep back-off while polling (env KKT_POLL_NS)
+  int ref_buf = 256;  // single-system refactor: update pairs per stage buffer (two buffers)
   int grid_wait = 0;  // sync-free grid solves: 1 = wait on a row's critical dependency first
   // operator (pattern shared; values per system)
   int *A_rp, *A_ci, *A_split, *gen_src;
@@ -177,8 +177,9 @@ cudaError_t launch_reset_scal(const DevPlan &d, int mode, cudaStream_t s);
 cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem, cudaStream_t s,
                             long long *launches);
 cudaError_t launch_diag_stats(const DevPlan &d, int blocks, cudaStream_t s);
-cudaError_t refactor_configure(int warps, size_t smem, int *blocks_per_sm);
-size_t refactor_smem_bytes(int warps, int maxpat);
+cudaError_t refactor_configure(int warps, size_t smem, int buf, int *blocks_per_sm);
+size_t refactor_smem_bytes(int warps, int maxpat, int buf);
+int refactor_buf();  // KKT_REF_BUF (refactor.cu)
 
 cudaError_t launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,
                         cudaStream_t s, long long *launches);

@@ -11,11 +11,13 @@
 // launch, and a consumer re-reads an entry of L(:,k) until it is no longer the sentinel —
 // the producer's store of the value is the signal (no fences, one L2 round trip per hop).
 // Producers publish L(:,j) before any other bookkeeping.  Update pairs are staged in shared
-// memory a chunk at a time so L2 latency overlaps across up to REFACTOR_STAGE pairs; the
-// sequential replay then runs from shared memory.  Products and differences are rounded
+// memory a chunk at a time with cp.async, two buffers per warp (the next chunk in flight
+// while one replays); the sequential replay runs from shared memory.  Products and differences are rounded
 // separately (no FMA) and every workspace entry receives its updates in the reference
 // order => bitwise equal factors.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "device.h"
 #include "kernels.cuh"
@@ -75,10 +77,8 @@ __device__ __forceinline__ double patch_floor(const DevPlan &d, int b) {
                    __longlong_as_double((long long)d.scal[(size_t)b * SCAL_STRIDE + SC_INFNORM]));
 }
 
-// Stage buffers: two per warp, each REFACTOR_BUF update-pair values + REFACTOR_BUF_I slots
-// (the same shared memory as one 512-pair buffer had).
-constexpr int REFACTOR_BUF = REFACTOR_STAGE / 2;
-constexpr int REFACTOR_BUF_I = REFACTOR_STAGE / 2;
+// Stage buffers: two per warp, each BUF update-pair values + BUF int slots (template BUF;
+// KKT_REF_BUF = 128 | 256 | 512, DevPlan::ref_buf, fixed when the handle is created).
 
 // A chunk of replay steps whose pairs fit a stage buffer (or one step wider than it: big).
 struct StChunk {
@@ -88,6 +88,7 @@ struct StChunk {
   int incl;   // inclusive prefix of the pair counts
 };
 
+template <int BUF>
 __device__ __forceinline__ StChunk st_meta(const DevPlan &d, int t0, int t_end, int lane) {
   StChunk c;
   c.t0 = t0;
@@ -100,7 +101,7 @@ __device__ __forceinline__ StChunk st_meta(const DevPlan &d, int t0, int t_end, 
     if (lane >= o) incl += v;
   }
   c.incl = incl;
-  const unsigned fits = __ballot_sync(0xffffffffu, t < t_end && incl <= REFACTOR_BUF);
+  const unsigned fits = __ballot_sync(0xffffffffu, t < t_end && incl <= BUF);
   c.nsteps = __popc(fits);
   c.big = c.nsteps == 0;  // a single step with more pairs than a stage buffer
   if (c.big) c.nsteps = 1;
@@ -125,14 +126,15 @@ __device__ __forceinline__ void st_issue(const DevPlan &d, const StChunk &c, dou
   cp_async_commit();
 }
 
+template <int BUF>
 __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int wstride = d.maxpat + REFACTOR_STAGE + REFACTOR_STAGE / 2;  // doubles per warp
+  const int wstride = d.maxpat + 3 * BUF;  // doubles per warp: x | 2 x BUF values | 2 x BUF slots
   double *x = smem + (size_t)wib * wstride;
   double *st_l = x + d.maxpat;
-  int *st_s = reinterpret_cast<int *>(st_l + REFACTOR_STAGE);
+  int *st_s = reinterpret_cast<int *>(st_l + 2 * BUF);
   const int ntask = (d.n - d.ref_start) * d.nb;
   while (true) {
     int task = 0;
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
     // chunk's copies in flight while this one replays (two buffers).  L(:,k) is the contiguous
     // Lx[Lp[k], Lp[k+1]) and a chunk's slots are contiguous, so a chunk is one round trip.
     const int t_end = d.so_ptr[j + 1];
-    StChunk cur = st_meta(d, d.so_ptr[j], t_end, lane);
+    StChunk cur = st_meta<BUF>(d, d.so_ptr[j], t_end, lane);
     st_issue(d, cur, st_l, st_s, Lx, lane);  // in flight during the A scatter
     for (int s = lane; s < np; s += 32) x[s] = 0.0;
     __syncwarp();
@@ -171,15 +173,15 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
       nxt.t0 = tn;
       nxt.nsteps = 0;
       if (tn < t_end) {
-        nxt = st_meta(d, tn, t_end, lane);
-        st_issue(d, nxt, st_l + (buf ^ 1) * REFACTOR_BUF, st_s + (buf ^ 1) * REFACTOR_BUF_I, Lx, lane);
+        nxt = st_meta<BUF>(d, tn, t_end, lane);
+        st_issue(d, nxt, st_l + (buf ^ 1) * BUF, st_s + (buf ^ 1) * BUF, Lx, lane);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncwarp();
-      double *stl = st_l + buf * REFACTOR_BUF;
-      const int *sts = st_s + buf * REFACTOR_BUF_I;
+      double *stl = st_l + buf * BUF;
+      const int *sts = st_s + buf * BUF;
       const int nsteps = cur.nsteps, t0 = cur.t0;
       for (int i = 0; i < nsteps; ++i) {
         const int kslot = __shfl_sync(0xffffffffu, cur.m.x, i);
@@ -414,15 +416,28 @@ cudaError_t launch_expand_norms(const DevPlan &d, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-size_t refactor_smem_bytes(int warps, int maxpat) {
-  return (size_t)warps * (maxpat + REFACTOR_STAGE + REFACTOR_STAGE / 2) * sizeof(double);
+int refactor_buf() {
+  const char *e = std::getenv("KKT_REF_BUF");
+  const int b = e ? std::atoi(e) : 256;
+  return b >= 512 ? 512 : b <= 128 ? 128 : 256;
 }
 
-cudaError_t refactor_configure(int warps, size_t smem, int *blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_refactor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+size_t refactor_smem_bytes(int warps, int maxpat, int buf) {
+  return (size_t)warps * (maxpat + 3 * buf) * sizeof(double);
+}
+
+template <int BUF>
+static cudaError_t ref_conf(int warps, size_t smem, int *blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_refactor<BUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(smem > 48 * 1024 ? smem : 48 * 1024));
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_refactor, 32 * warps, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_refactor<BUF>, 32 * warps, smem);
+}
+
+cudaError_t refactor_configure(int warps, size_t smem, int buf, int *blocks_per_sm) {
+  return buf == 512 ? ref_conf<512>(warps, smem, blocks_per_sm)
+         : buf == 128 ? ref_conf<128>(warps, smem, blocks_per_sm)
+                      : ref_conf<256>(warps, smem, blocks_per_sm);
 }
 
 cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem, cudaStream_t s,
@@ -442,7 +457,9 @@ cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem
     }
   }
   if (d.ref_start < d.n) {
-    k_refactor<<<blocks, 32 * warps, smem, s>>>(d);
+    if (d.ref_buf == 512) k_refactor<512><<<blocks, 32 * warps, smem, s>>>(d);
+    else if (d.ref_buf == 128) k_refactor<128><<<blocks, 32 * warps, smem, s>>>(d);
+    else k_refactor<256><<<blocks, 32 * warps, smem, s>>>(d);
     ++*launches;
   }
   return cudaGetLastError();
