@@ -67,7 +67,9 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
     // grid_wait 1 (the single-system default): lane 0 alone spins on the critical dependency
     // before the row; the other dependencies are then normally published already, so the
     // lanes' loads below rarely have to wait.  (0: each lane polls its own unpublished column
-    // in the chunk loop — many pollers per row, measured 2.5x slower.)
+    // in the chunk loop — many pollers per row, measured 2.5x slower.  Reading the first
+    // chunk's y speculatively before the wait measured no faster and costs 8 registers —
+    // above 32 the persistent grid loses occupancy: 1.24 -> 1.35 ms.)
     if (d.grid_wait) {
       const int cr = crit[idx];
       if (lane == 0 && cr >= 0) wait_value(&ysrc[cr], d.poll_ns);
