@@ -569,11 +569,12 @@ def main():
              "spmv": t_spmv * (max_iters + 3)}
     dom = max(share, key=share.get)
     kd = kern[dom]
-    traffic = None
+    traffic = None  # the committed capture is of the default workload only
+    same_workload = args.config == "activsg10k" and args.imbalance_frac == 1.0 and B == 64
     tp = os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")
     if not os.path.exists(tp):
         tp = os.path.join(ROOT, "profiles", "r1l_ncu_traffic.json")
-    if os.path.exists(tp):
+    if same_workload and os.path.exists(tp):
         tk = json.load(open(tp))["kernels"]
         fam = {"refactor": ["k_b_refactor", "k_b_refactor_tma<"], "spmv": ["k_b_spmv"],
                "trisolve_pair": ["k_b_trsv_grid<0,", "k_b_trsv_grid<1,", "k_trsv_blocked<0, 1,",
