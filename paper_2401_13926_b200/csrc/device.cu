@@ -646,6 +646,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   }
   dev->refactor_warps = 8;
   d.ref_buf = refactor_buf();
+  d.ref_direct = std::getenv("KKT_REF_DIRECT") ? std::atoi(std::getenv("KKT_REF_DIRECT")) : 1;
   dev->refactor_smem = refactor_smem_bytes(dev->refactor_warps, d.maxpat, d.ref_buf);
   while (dev->refactor_smem > 200 * 1024 && dev->refactor_warps > 1) {
     dev->refactor_warps /= 2;

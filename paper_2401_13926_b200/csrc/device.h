@@ -76,6 +76,7 @@ struct DevPlan {
   int lev_ptr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // col_order offsets of those levels
   int poll_ns = 0;  // __nanosleep back-off while polling (env KKT_POLL_NS)
   int ref_buf = 256;  // single-system refactor: update pairs per stage buffer (two buffers)
+  int ref_direct = 1;  // single-system refactor: lanes poll their own unpublished L entries
   int grid_wait = 0;  // sync-free grid solves: 1 = wait on a row's critical dependency first
   // operator (pattern shared; values per system)
   int *A_rp, *A_ci, *A_split, *gen_src;

@@ -190,11 +190,13 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
         const double xk = x[kslot];
         const int lbk = __shfl_sync(0xffffffffu, cur.m.w, i);  // L(:,k) = Lx[lbk, lbk+cnt)
         if (!cur.big) {
-          // L(:,k) not yet published when staged?  One lane waits so a column many warps
-          // depend on is not polled by every lane of every consumer; then the whole step
-          // is re-staged with one parallel round trip.
+          // L(:,k) not yet published when staged?  ref_direct (default): every lane polls its
+          // own unpublished entries in the replay below — the values arrive as they are
+          // published (10k sequence step 3.75 -> 3.40 ms).  ref_direct 0: one lane waits on the
+          // column's last entry, then the whole step is re-staged with one more round trip.
           bool miss = false;
-          for (int e = lane; e < cnt; e += 32) miss |= is_sentinel(stl[off + e]);
+          if (!d.ref_direct)
+            for (int e = lane; e < cnt; e += 32) miss |= is_sentinel(stl[off + e]);
           const unsigned mm = __ballot_sync(0xffffffffu, miss);
           if (mm) {
             if (lane == __ffs(mm) - 1) wait_value(&Lx[lbk + cnt - 1], d.poll_ns);

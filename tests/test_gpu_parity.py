@@ -196,11 +196,13 @@ def test_harness_rows_device_mode(case):
 
 @pytest.mark.parametrize("env", [{"KKT_GRID_WAIT": "0"}, {"KKT_U_PARTIAL": "0"},
                                  {"KKT_SWEEP_AHEAD": "1"}, {"KKT_SWEEP_NOSTAGE": "1"},
-                                 {"KKT_SWEEP_THREADS": "512"}, {"KKT_TRSV_BLOCKS": "148"}])
+                                 {"KKT_SWEEP_THREADS": "512"}, {"KKT_TRSV_BLOCKS": "148"},
+                                 {"KKT_REF_DIRECT": "0"}, {"KKT_REF_BUF": "128"}])
 @pytest.mark.parametrize("case", ["standard_trace", "acopf_small"])
 def test_single_system_solve_variants_bitwise(case, env, monkeypatch):
-    """The single-system solve's alternative schedules (grid critical wait, U head prefix,
-    sweep variants, a reduced persistent grid as the straggler helpers use) stay bitwise."""
+    """The single-system path's alternative schedules (grid critical wait, U head prefix,
+    sweep variants, a reduced persistent grid as the straggler helpers use, the refactor's
+    staged-restage miss path and stage size) stay bitwise."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     g = golden(case)
@@ -208,5 +210,7 @@ def test_single_system_solve_variants_bitwise(case, env, monkeypatch):
     M = g["K_values"].shape[0]
     for i in (M - 2, M - 1):
         refactorize(f, to_general(lower_matrix(g, i)))
+        if f"s{i}_Lx" in g:
+            assert np.array_equal(f._Lx, g[f"s{i}_Lx"]) and np.array_equal(f._Ux, g[f"s{i}_Ux"]), (i, env)
         assert np.array_equal(lu_solve(f, g["rhs"][i]), g["x0"][i]), (i, env)
     f.close()
