@@ -103,6 +103,10 @@ int kkt_symbolic_stats(const kkt_symbolic *s, int64_t stats[9]);
 
 /* ======================================================================
  * Device handle: one GPU, one stream, all buffers allocated once.
+ * Calls on one handle must be serialised by the caller.  Handles on different GPUs may run
+ * concurrently; handles on the SAME GPU must not: the refactorization and grid-solve
+ * kernels are persistent, sync-free grids sized to the GPU's resident-CTA capacity, so two
+ * of them running side by side are not guaranteed co-resident.
  * ====================================================================== */
 typedef struct kkt_device kkt_device;
 
