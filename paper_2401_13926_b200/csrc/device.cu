@@ -372,6 +372,9 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   acc(4 * d.nnz_L); acc(4 * d.nnz_U);                                      // Li Ui (CSC)
   acc(4 * h.Ltail_split.size()); acc(8 * h.Ltail_split.size() * B);        // split, tacc
   acc(4 * h.Ugrid_split.size()); acc(4 * h.U_part_rows.size());            // U head prefix
+  acc(4 * h.Lc_task.size()); acc(4 * h.Lc_aux.size()); acc(4 * h.Lc_split.size());  // chains
+  acc(4 * h.Uc_task.size()); acc(4 * h.Uc_aux.size()); acc(4 * h.Uc_split.size());
+  if (nbp == 1) acc(8 * n);                                                // cpart
   acc(8 * d.nnz_L * B); acc(8 * d.nnz_U * B); acc(8 * n * B); acc(8 * n * B);  // Lv Uv yL yU
   acc(8 * SCAL_STRIDE * B); acc(64); acc(8 * 8 * (size_t)d.rb * B);        // scal ticket partials
   acc(8 * btask.size());                                                   // batched tasks
@@ -435,6 +438,18 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   d.U_part_rows = carve<int>(cur, h.U_part_rows.size());
   d.n_upart = (int)h.U_part_rows.size();
   d.u_partial = std::getenv("KKT_U_PARTIAL") ? std::atoi(std::getenv("KKT_U_PARTIAL")) : 1;
+  d.Lc_task = carve<int>(cur, h.Lc_task.size());
+  d.Lc_aux = carve<int>(cur, h.Lc_aux.size());
+  d.Lc_split = carve<int>(cur, h.Lc_split.size());
+  d.Uc_task = carve<int>(cur, h.Uc_task.size());
+  d.Uc_aux = carve<int>(cur, h.Uc_aux.size());
+  d.Uc_split = carve<int>(cur, h.Uc_split.size());
+  d.nLc = (int)h.Lc_task.size();
+  d.nUc = (int)h.Uc_task.size();
+  if (nbp == 1) d.cpart = carve<double>(cur, n);
+  // chain tasks: single system, U grid rows starting at their head split (the plan's model)
+  d.chains = (nbp == 1 && d.u_partial && (d.nLc > 0 || d.nUc > 0)) ? 1 : 0;
+  if (std::getenv("KKT_CHAINS")) d.chains = d.chains && std::atoi(std::getenv("KKT_CHAINS")) != 0;
   d.Lv = carve<double>(cur, d.nnz_L * B);
   d.Uv = carve<double>(cur, d.nnz_U * B);
   d.yL = carve<double>(cur, n * B);
@@ -484,6 +499,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
       d.trace_ref = (unsigned long long *)dev->trace_mem;
       d.trace_trsv = d.trace_ref + 2 * n;
       d.trace_step = d.trace_trsv + 2 * n;
+      if (std::atoi(std::getenv("KKT_TRACE")) == 2) d.trace_trsv = nullptr;  // chain loop cycles only
       cudaMemsetAsync(dev->trace_mem, 0, tb, dev->stream);
     }
   }
@@ -527,6 +543,12 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   UP(d.Ltail_split, h.Ltail_split);
   UP(d.Ugrid_split, h.Ugrid_split);
   UP(d.U_part_rows, h.U_part_rows);
+  UP(d.Lc_task, h.Lc_task);
+  UP(d.Lc_aux, h.Lc_aux);
+  UP(d.Lc_split, h.Lc_split);
+  UP(d.Uc_task, h.Uc_task);
+  UP(d.Uc_aux, h.Uc_aux);
+  UP(d.Uc_split, h.Uc_split);
   UP(d.btask, btask);
   UP(d.so_dep, so_dep);
   UP(d.hc_col, heavy.col);
@@ -582,6 +604,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   }
   CUDA_TRY(launch_fill_sentinel(d.yL, (int64_t)(n * B), dev->stream));
   CUDA_TRY(launch_fill_sentinel(d.yU, (int64_t)(n * B), dev->stream));
+  if (d.cpart) CUDA_TRY(launch_fill_sentinel(d.cpart, (int64_t)n, dev->stream));
   CUDA_TRY(cudaMemsetAsync(d.scal, 0, 8 * SCAL_STRIDE * B, dev->stream));
   CUDA_TRY(cudaMemsetAsync(d.ticket, 0, 64, dev->stream));
   // launch shapes

@@ -96,6 +96,11 @@ struct DevPlan {
   int n_upart = 0, u_partial = 1;  // rows with a head prefix; 0 = grid rows sum it (KKT_U_PARTIAL)
   double *tacc;                             // [nb][n - pL] tail partial sums (grid -> sweep)
   int pL, pU, nLg, nUg;                     // split positions and grid-phase row counts
+  // single-system chain tasks of the grid phases (plan.h build_chains; KKT_CHAINS=0: off)
+  int *Lc_task = nullptr, *Lc_aux = nullptr, *Lc_split = nullptr;
+  int *Uc_task = nullptr, *Uc_aux = nullptr, *Uc_split = nullptr;
+  int nLc = 0, nUc = 0, chains = 0;
+  double *cpart = nullptr;                  // [n] chain rows' external prefix (sentinel-reset)
   int L_nsync = 0, L_sync_ptr[5] = {0, 0, 0, 0, 0};  // level-synchronous leading L levels
   int *L_glev = nullptr, *U_glev = nullptr;  // level boundaries of the grid orders
   int L_nglev = 0, U_nglev = 0;

@@ -83,6 +83,103 @@ static void build_sweep(const HostPlan &P, bool upper, HostSweep &H) {
   }
 }
 
+// Single-system grid phase as chain tasks (trisolve.cu k_trsv_chain).  A chain is a run of up
+// to 32 consecutive grid rows, each depending on its predecessor in the solve order (L: row
+// r-1 -> r, U: r+1 -> r).  One warp solves it row by row, lane i holding row i, so a link of
+// the chain costs a shuffle instead of an L2 publish/poll round trip (at 10k the grid phases
+// have 196 levels each, but only 28 once such runs are contracted).  A chain row's entries
+// split into external columns (outside the chain) and internal ones, and the external ones
+// come first in the row's update order (L ascending columns < r0, U descending columns > r0),
+// so their sum is an independent "partial" task (warp per row, published into cpart) that the
+// chain warp waits for.  Tasks are sorted by a modelled start time (HOP per L2 hand-off, LINK
+// per chain row) — every dependency finishes strictly before a task's modelled start, so the
+// order is topological and the persistent grid cannot deadlock.
+static void build_chains(HostPlan &P, bool upper) {
+  const double HOP = 1.5, LINK = 0.15;
+  const int32_t p = upper ? P.pU : P.pL;
+  const std::vector<int32_t> &rp = upper ? P.Urp : P.Lrp, &ci = upper ? P.Uci : P.Lci;
+  std::vector<int32_t> &task = upper ? P.Uc_task : P.Lc_task, &aux = upper ? P.Uc_aux : P.Lc_aux,
+                       &split = upper ? P.Uc_split : P.Lc_split;
+  task.clear();
+  aux.clear();
+  split.assign(std::max<int32_t>(p, 1), 0);
+  if (p <= 0 || P.n >= (1 << 26)) return;
+  std::vector<char> grid(p, 1);  // L: the leading levels run row-parallel before the grid
+  if (!upper)
+    for (int32_t i = 0; i < P.L_sync_ptr.back(); ++i) grid[P.L_grid_order[i]] = 0;
+  auto gbeg = [&](int32_t r) { return upper ? P.Ugrid_split[r] : rp[r]; };
+  // chain heads and lengths, walking the solve order
+  std::vector<int32_t> head(p, -1), len(p, 0);
+  for (int32_t s = 0; s < p; ++s) {
+    const int32_t r = upper ? p - 1 - s : s;
+    if (!grid[r]) continue;
+    const int32_t prev = upper ? r + 1 : r - 1;
+    const bool link = prev >= 0 && prev < p && grid[prev] && rp[r + 1] > gbeg(r) &&
+                      ci[rp[r + 1] - 1] == prev && len[head[prev]] < 32;
+    head[r] = link ? head[prev] : r;
+    len[head[r]]++;
+  }
+  struct T {
+    double t;
+    int32_t code, aux;
+  };
+  std::vector<T> tl;
+  tl.reserve(p);
+  std::vector<double> fin(p, 0.0);
+  // latest-finishing grid dependency among the entries [q0, q1) of a row
+  auto latest = [&](int32_t q0, int32_t q1, double *tmax) {
+    int32_t best = -1;
+    double bt = -1.0;
+    for (int32_t q = q0; q < q1; ++q) {
+      const int32_t c = ci[q];
+      if (c >= p || !grid[c]) continue;
+      if (fin[c] > bt) {
+        bt = fin[c];
+        best = c;
+      }
+    }
+    *tmax = std::max(bt, 0.0);
+    return best;
+  };
+  for (int32_t s = 0; s < p; ++s) {
+    const int32_t h = upper ? p - 1 - s : s;
+    if (!grid[h] || head[h] != h) continue;
+    const int32_t m = len[h];
+    if (m == 1) {
+      double t;
+      const int32_t cr = latest(gbeg(h), rp[h + 1], &t);
+      fin[h] = t + HOP;
+      tl.push_back({t + HOP, h, cr});
+      continue;
+    }
+    double start = 0.0;
+    uint32_t mask = 0;
+    for (int32_t i = 0; i < m; ++i) {
+      const int32_t r = upper ? h - i : h + i;
+      int32_t q = gbeg(r);
+      while (q < rp[r + 1] && (upper ? ci[q] > h : ci[q] < h)) ++q;
+      split[r] = q;
+      if (q > gbeg(r)) {  // external entries: a partial task
+        double t;
+        const int32_t cr = latest(gbeg(r), q, &t);
+        tl.push_back({t + HOP, -(r + 1), cr});
+        mask |= 1u << i;
+        start = std::max(start, t + HOP);
+      }
+    }
+    start += HOP;
+    tl.push_back({start, h | ((m - 1) << 26), (int32_t)mask});
+    for (int32_t i = 0; i < m; ++i) fin[upper ? h - i : h + i] = start + LINK * (i + 1);
+  }
+  std::stable_sort(tl.begin(), tl.end(), [](const T &a, const T &b) { return a.t < b.t; });
+  task.resize(tl.size());
+  aux.resize(tl.size());
+  for (size_t i = 0; i < tl.size(); ++i) {
+    task[i] = tl[i].code;
+    aux[i] = tl[i].aux;
+  }
+}
+
 int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int64_t in_nnz,
                const int64_t *gen_src, HostPlan &P) {
   const int64_t n = S.n;
@@ -366,6 +463,8 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
     P.Ui32.assign(S.Ui.begin(), S.Ui.end());
     build_sweep(P, false, P.swL);
     build_sweep(P, true, P.swU);
+    build_chains(P, false);
+    build_chains(P, true);
   }
   P.Lx0.assign(S.Lx.begin(), S.Lx.end());
   P.Ux0.assign(S.Ux.begin(), S.Ux.end());

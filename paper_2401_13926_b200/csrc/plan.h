@@ -62,6 +62,11 @@ struct HostPlan {
   std::vector<int32_t> Ugrid_split, U_part_rows;
   int32_t sweep_maxL = 0, sweep_maxU = 0;  // longest column inside each sweep block
   HostSweep swL, swU;
+  // Single-system grid phases as chain tasks (build_chains): per task a code — row r (one
+  // row), -(r+1) (external prefix of chain row r), or r0 | (m-1) << 26 (chain of m >= 2
+  // rows from r0) — and an aux word (critical dependency, or the chain's partial-row mask);
+  // per chain row the CSR index of its first internal entry.
+  std::vector<int32_t> Lc_task, Lc_aux, Lc_split, Uc_task, Uc_aux, Uc_split;
 };
 
 // Tunables of the phase split (env KKT_TAIL_ROWS / KKT_HEAD_ROWS override the model).

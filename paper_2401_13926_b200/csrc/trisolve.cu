@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.h"
 #include "kernels.cuh"
@@ -101,6 +102,149 @@ __global__ void __launch_bounds__(256) k_trsv_grid(DevPlan d, const double *__re
       }
     }
   }
+}
+
+// ---- grid phase as chain tasks (single system; plan.cpp build_chains) ---------------------
+// Task codes: r (one row, as k_trsv_grid), -(r+1) (the external prefix of chain row r, into
+// cpart), r0 | (m-1) << 26 (a chain of m rows r0, r0 +- 1, ...).  The per-row arithmetic is
+// k_trsv_grid's: the prefix is summed in CSR order from the row's initial value, and the chain
+// warp continues each row with its internal entries in CSR order (lane i = row i; the column
+// of step j is row j of the chain, so consuming entries as the steps come keeps that order).
+// One-row and prefix tasks: lane 0 waits on the critical dependency, the lanes then sum the
+// entries [beg, end) 32 at a time, in order, from `acc` (uniform across the warp).
+template <bool IS_U>
+__device__ __forceinline__ double chain_row_sum(const DevPlan &d, const int *__restrict__ ci,
+                                                const double *__restrict__ vals, const double *ysrc,
+                                                int beg, int end, int cr, double acc, int lane) {
+  int col = 0;
+  double v = 0.0;
+  if (beg + lane < end) {
+    col = ci[beg + lane];
+    v = vals[beg + lane];
+  }
+  if (lane == 0 && cr >= 0) wait_value(&ysrc[cr], d.poll_ns);
+  __syncwarp();
+  for (int c0 = beg; c0 < end; c0 += 32) {
+    const int cnt = min(32, end - c0);
+    double p = 0.0;
+    int ncol = 0;
+    double nv = 0.0;
+    if (c0 + 32 + lane < end) {
+      ncol = ci[c0 + 32 + lane];
+      nv = vals[c0 + 32 + lane];
+    }
+    if (lane < cnt) p = __dmul_rn(v, wait_value(&ysrc[col], d.poll_ns));
+    for (int i = 0; i < cnt; ++i) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, p, i));
+    col = ncol;
+    v = nv;
+  }
+  return acc;
+}
+
+template <bool IS_U>
+__global__ void __launch_bounds__(256, 8) k_trsv_chain(DevPlan d, const double *__restrict__ b,
+                                                    double *__restrict__ xout) {
+  if (!sys_active(d, 0)) return;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int *task = IS_U ? d.Uc_task : d.Lc_task;
+  const int *aux = IS_U ? d.Uc_aux : d.Lc_aux;
+  const int *split = IS_U ? d.Uc_split : d.Lc_split;
+  const int ntask = IS_U ? d.nUc : d.nLc;
+  const int *rp = IS_U ? d.Urp : d.Lrp;
+  const int *ci = IS_U ? d.Uci : d.Lci;
+  const double *vals = IS_U ? d.Uv : d.Lv;
+  double *ysrc = IS_U ? d.yU : d.yL;  // published by this sweep
+  double *yres = IS_U ? d.yL : d.yU;  // reset for the next solve
+  for (int idx = gwarp; idx < ntask; idx += nwarps) {
+    const int code = task[idx], ax = aux[idx];
+    if (code < 0 || (code >> 26) == 0) {  // one row, or a chain row's external prefix
+      const bool prefix = code < 0;
+      const int r = prefix ? -code - 1 : code;
+      const int beg = IS_U ? d.Ugrid_split[r] : rp[r];
+      const int end = prefix ? split[r] : rp[r + 1];
+      const double init = IS_U ? ldcg(&d.yL[r]) : b[d.row_perm[r]];
+      const double piv = (IS_U && !prefix) ? d.udiag[r] : 1.0;
+      const double acc = chain_row_sum<IS_U>(d, ci, vals, ysrc, beg, end, ax, init, lane);
+      if (lane == 0) {
+        if (prefix) st_relaxed_f64(&d.cpart[r], unsentinel(acc));
+        else {
+          const double w = IS_U ? __ddiv_rn(acc, piv) : acc;
+          st_relaxed_f64(&ysrc[r], unsentinel(w));
+          if (d.trace_trsv) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
+          st_relaxed_f64(&yres[r], __longlong_as_double((long long)SENTINEL_BITS));
+          if (IS_U) {
+            xout[d.col_perm[r]] = w;
+            if (!isfinite(w)) atomicOr(&d.scal[SC_NONFINITE], 1ull);
+          }
+        }
+      }
+      continue;
+    }
+    const int r0 = code & ((1 << 26) - 1), m = (code >> 26) + 1;
+    const int r = IS_U ? r0 - lane : r0 + lane;
+    const bool act = lane < m;
+    double piv = 1.0, acc = 0.0, cv = 0.0;
+    int q = 0, qe = 0, cc = -1;
+    if (act) {
+      q = split[r];
+      qe = rp[r + 1];
+      if (IS_U) piv = d.udiag[r];
+      if (q < qe) {
+        cc = ci[q];
+        cv = vals[q];
+      }
+      if ((ax >> lane) & 1) {  // the prefix task's sum (then reset for the next solve)
+        acc = wait_value(&d.cpart[r], d.poll_ns);
+        d.cpart[r] = __longlong_as_double((long long)SENTINEL_BITS);
+      } else {
+        acc = IS_U ? ldcg(&d.yL[r]) : b[d.row_perm[r]];
+      }
+    }
+    // Per step only the publish of y_j is on the chain; the other buffer's reset and x (U) are
+    // written after the loop.  (Measured: staging the internal entries in shared memory, or a
+    // branch-free step with a consumption bit mask, is no faster — the step is bound by the
+    // warps sharing the SM: ~1,000 cycles per row at 64 warps per SM, ~400 at 16.)
+    const long long t_loop = d.trace_step ? clock64() : 0;
+    double mine = 0.0;
+    for (int j = 0; j < m; ++j) {
+      const double w = IS_U ? __ddiv_rn(acc, piv) : acc;
+      const double yj = __shfl_sync(0xffffffffu, w, j);
+      if (lane == j) {
+        st_relaxed_f64(&ysrc[r], unsentinel(yj));  // publish first: other rows wait on it
+        mine = yj;
+      }
+      if (cc == (IS_U ? r0 - j : r0 + j)) {  // this row's next internal entry is column r_j
+        acc = __dsub_rn(acc, __dmul_rn(cv, yj));
+        cc = -1;
+        if (++q < qe) {
+          cc = ci[q];
+          cv = vals[q];
+        }
+      }
+    }
+    if (act) {
+      if (d.trace_trsv) d.trace_trsv[(IS_U ? d.n : 0) + r] = globaltimer();
+      st_relaxed_f64(&yres[r], __longlong_as_double((long long)SENTINEL_BITS));
+      if (IS_U) {
+        xout[d.col_perm[r]] = mine;
+        if (!isfinite(mine)) atomicOr(&d.scal[SC_NONFINITE], 1ull);
+      }
+    }
+    const size_t to = 2 * (size_t)idx + (IS_U ? 2 * (size_t)d.n : 0);
+    if (d.trace_step && !d.trace_trsv && lane == 0 && to + 1 < 4 * (size_t)d.n) {
+      d.trace_step[to] = (unsigned long long)m;  // KKT_TRACE=2: {rows, loop cycles}
+      d.trace_step[to + 1] = (unsigned long long)(clock64() - t_loop);
+    }
+  }
+}
+
+cudaError_t launch_trsv_chain(const DevPlan &d, bool upper, const double *b, double *x, int grid_blocks,
+                              cudaStream_t s) {
+  if (upper) k_trsv_chain<true><<<grid_blocks, 256, 0, s>>>(d, b, x);
+  else k_trsv_chain<false><<<grid_blocks, 256, 0, s>>>(d, b, x);
+  return cudaGetLastError();
 }
 
 // ---- row-parallel launches: rows whose dependencies are all final (an earlier launch) ------
@@ -184,6 +328,8 @@ cudaError_t launch_L_front(const DevPlan &d, const double *b, double *x, int gri
   if (e == cudaSuccess && d.nLg > d.L_sync_ptr[d.L_nsync]) {
     if (d.nbp > 1) {
       e = b_launch_grid_L(d, b, x, grid_blocks, s);
+    } else if (d.chains) {
+      e = launch_trsv_chain(d, false, b, x, grid_blocks, s);
     } else {
       k_trsv_grid<false><<<grid_blocks, 256, 0, s>>>(d, b, x);
       e = cudaGetLastError();
@@ -223,8 +369,11 @@ cudaError_t trsv_configure(int *grid_blocks_per_sm) {
   int a = 0, b = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_trsv_grid<false>, 256, 0);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trsv_grid<true>, 256, 0);
+  int c = 0, u = 0;  // the chain kernels run on the same persistent grid
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_trsv_chain<false>, 256, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&u, k_trsv_chain<true>, 256, 0);
   if (e != cudaSuccess) return e;
-  *grid_blocks_per_sm = a < b ? a : b;
+  *grid_blocks_per_sm = std::min(std::min(a, b), std::min(c, u));
   return e;
 }
 
@@ -249,7 +398,8 @@ cudaError_t launch_trsv(const DevPlan &d, const double *b, double *x, int grid_b
   if (d.nUg) {
     cudaError_t e = launch_U_partial(d, s, launches);
     if (e != cudaSuccess) return e;
-    k_trsv_grid<true><<<grid_blocks, 256, 0, s>>>(d, b, x);
+    if (d.chains) launch_trsv_chain(d, true, b, x, grid_blocks, s);
+    else k_trsv_grid<true><<<grid_blocks, 256, 0, s>>>(d, b, x);
     ++*launches;
   }
   return cudaGetLastError();
