@@ -474,12 +474,15 @@ int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int6
 
 // Cost model for the sweep-phase size T (the last T positions): each grid-phase level costs
 // ~GRID_HOP_US (an L2 round trip on the dependency chain), each sweep column ~SWEEP_COL_US
-// (one CTA barrier + shared RMW) plus ~SWEEP_NNZ_US per block entry of throughput.
+// (the blocked sweep's per-column chain) plus ~SWEEP_NNZ_US per block entry of throughput.
+// SWEEP_COL_US refitted after the grid phases got faster (batched without the up-front wait,
+// single-system chain tasks): measured optimum T = 256..768 at 10k (single 0.87-0.89 ms vs
+// 0.98 at the old choice 1,536; batch of 64 1.54 vs 1.72 ms) and 512 at 70k (2.83 vs 3.25).
 int choose_tail(const HostPlan &P, bool upper) {
   const char *env = std::getenv(upper ? "KKT_HEAD_ROWS" : "KKT_TAIL_ROWS");
   const int n = P.n;
   if (env) return std::max(0, std::min(n, std::min(atoi(env), KKT_CTA_PHASE_MAX_ROWS)));
-  const double GRID_HOP_US = 1.0, SWEEP_COL_US = 0.06, SWEEP_NNZ_US = 0.0003;
+  const double GRID_HOP_US = 1.0, SWEEP_COL_US = 0.2, SWEEP_NNZ_US = 0.0003;
   const std::vector<int32_t> &rp = upper ? P.Urp : P.Lrp;
   const std::vector<int32_t> &ci = upper ? P.Uci : P.Lci;
   double best = 1e30;
