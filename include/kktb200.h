@@ -132,6 +132,15 @@ int kkt_dev_create(const kkt_symbolic *s, const int64_t *A_row_ptr, const int64_
                    kkt_device **out);
 void kkt_dev_destroy(kkt_device *d);
 
+/* Host-only check of the execution plan kkt_dev_create would build (no GPU needed): the
+ * single-system grid phases' chain task lists.  out = {tasks L, tasks U, chains, chain rows,
+ * longest chain, order violations, coverage violations, 0}.  Zero order violations means
+ * every task reads only values published by tasks earlier in its list, which is what makes
+ * the persistent, sync-free grid deadlock-free.  Test/diagnostic entry, no reference
+ * counterpart. */
+int kkt_plan_check(const kkt_symbolic *s, const int64_t *A_row_ptr, const int64_t *A_col_idx,
+                   int64_t lower_nnz, const int64_t *gen_src, int64_t out[8]);
+
 /* Raw CUDA stream (cudaStream_t) the handle launches on. */
 void *kkt_dev_stream(kkt_device *d);
 

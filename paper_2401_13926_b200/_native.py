@@ -13,7 +13,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkktb200.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 KKT_OK = 0
 KKT_ERR_SINGULAR = 1
@@ -80,6 +80,7 @@ SIGNATURES = [
     ("kkt_symbolic_stats", C.c_int, [vp, i64p]),
     ("kkt_dev_create", C.c_int, [vp, i64p, i64p, i64, i64p, C.POINTER(DeviceOpts), C.POINTER(vp)]),
     ("kkt_dev_destroy", None, [vp]),
+    ("kkt_plan_check", C.c_int, [vp, i64p, i64p, i64, i64p, i64p]),
     ("kkt_dev_stream", vp, [vp]),
     ("kkt_dev_refactor", C.c_int, [vp, vp, C.c_int, C.c_int, f64p]),
     ("kkt_dev_set_operator_values", C.c_int, [vp, vp, C.c_int, C.c_int]),

@@ -924,6 +924,21 @@ int kkt_dev_create(const kkt_symbolic *s, const int64_t *A_row_ptr, const int64_
   }
 }
 
+int kkt_plan_check(const kkt_symbolic *s, const int64_t *A_row_ptr, const int64_t *A_col_idx,
+                   int64_t in_nnz, const int64_t *gen_src, int64_t out[8]) {
+  if (!s || !out || !A_row_ptr || !A_col_idx) return kkt::set_error(KKT_ERR_BAD_ARG, "NULL argument");
+  try {
+    kkt::HostPlan P;
+    const int rc = kkt::build_plan(*reinterpret_cast<const kkt::Symbolic *>(s), A_row_ptr, A_col_idx, in_nnz,
+                                   gen_src, P);
+    if (rc != KKT_OK) return rc;
+    kkt::check_chains(P, out);
+    return KKT_OK;
+  } catch (std::bad_alloc &) {
+    return kkt::set_error(KKT_ERR_OOM, "host allocation failed in kkt_plan_check");
+  }
+}
+
 void kkt_dev_destroy(kkt_device *d) { kkt::destroy(reinterpret_cast<Device *>(d)); }
 
 void *kkt_dev_stream(kkt_device *d) { return d ? (void *)reinterpret_cast<Device *>(d)->stream : nullptr; }

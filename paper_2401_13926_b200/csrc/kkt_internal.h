@@ -6,7 +6,7 @@
 
 #include "../../include/kktb200.h"
 
-#define KKT_ABI_VERSION 3
+#define KKT_ABI_VERSION 4
 
 namespace kkt {
 

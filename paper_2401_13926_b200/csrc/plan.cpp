@@ -180,6 +180,73 @@ static void build_chains(HostPlan &P, bool upper) {
   }
 }
 
+// Invariants of the chain task lists (kkt_plan_check; host only).  out: {tasks L, tasks U,
+// chains, chain rows, longest chain, order violations, coverage violations, 0}.  An order
+// violation is a task that reads a value (a y of the grid phase, or a chain row's prefix sum)
+// produced by a task at the same or a later position — the persistent grid is deadlock-free
+// exactly when there are none, since every warp takes its tasks in list order.
+void check_chains(const HostPlan &P, int64_t out[8]) {
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  for (int up = 0; up < 2; ++up) {
+    const bool upper = up != 0;
+    const int32_t p = upper ? P.pU : P.pL;
+    const std::vector<int32_t> &rp = upper ? P.Urp : P.Lrp, &ci = upper ? P.Uci : P.Lci;
+    const std::vector<int32_t> &task = upper ? P.Uc_task : P.Lc_task, &aux = upper ? P.Uc_aux : P.Lc_aux,
+                               &split = upper ? P.Uc_split : P.Lc_split;
+    out[up] = (int64_t)task.size();
+    if (p <= 0) continue;
+    std::vector<char> grid(p, 1);
+    if (!upper)
+      for (int32_t i = 0; i < P.L_sync_ptr.back(); ++i) grid[P.L_grid_order[i]] = 0;
+    auto gbeg = [&](int32_t r) { return upper ? P.Ugrid_split[r] : rp[r]; };
+    std::vector<int64_t> prod(p, -1), pre(p, -1);  // task publishing y[r] / r's prefix sum
+    for (size_t t = 0; t < task.size(); ++t) {
+      const int32_t c = task[t];
+      auto own = [&](int32_t r, std::vector<int64_t> &v) {
+        if (r < 0 || r >= p || !grid[r] || v[r] >= 0) ++out[6];
+        else v[r] = (int64_t)t;
+      };
+      if (c < 0) own(-c - 1, pre);
+      else if ((c >> 26) == 0) own(c, prod);
+      else {
+        const int32_t h = c & ((1 << 26) - 1), m = (c >> 26) + 1;
+        ++out[2];
+        out[3] += m;
+        out[4] = std::max<int64_t>(out[4], m);
+        for (int32_t i = 0; i < m; ++i) own(upper ? h - i : h + i, prod);
+      }
+    }
+    for (int32_t r = 0; r < p; ++r)
+      if (grid[r] && prod[r] < 0) ++out[6];  // a grid row nobody publishes
+    auto before = [&](int32_t col, int64_t t) {  // y[col] is published before task t
+      if (col >= p || !grid[col]) return true;    // head columns / row-parallel levels: earlier launches
+      return prod[col] >= 0 && prod[col] < t;
+    };
+    for (size_t t = 0; t < task.size(); ++t) {
+      const int32_t c = task[t];
+      if (c < 0 || (c >> 26) == 0) {
+        const int32_t r = c < 0 ? -c - 1 : c;
+        if (r < 0 || r >= p) continue;
+        const int32_t end = c < 0 ? split[r] : rp[r + 1];
+        for (int32_t q = gbeg(r); q < end; ++q) out[5] += !before(ci[q], (int64_t)t);
+        continue;
+      }
+      const int32_t h = c & ((1 << 26) - 1), m = (c >> 26) + 1;
+      const uint32_t mask = (uint32_t)aux[t];
+      for (int32_t i = 0; i < m; ++i) {
+        const int32_t r = upper ? h - i : h + i;
+        const bool ext = split[r] > gbeg(r);
+        if (ext != (((mask >> i) & 1u) != 0) || (ext && !(pre[r] >= 0 && pre[r] < (int64_t)t))) ++out[5];
+        for (int32_t q = split[r]; q < rp[r + 1]; ++q) {  // internal: earlier rows of this chain
+          const int32_t col = ci[q];
+          const bool inside = upper ? (col > r && col <= h) : (col < r && col >= h);
+          out[6] += !inside;
+        }
+      }
+    }
+  }
+}
+
 int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int64_t in_nnz,
                const int64_t *gen_src, HostPlan &P) {
   const int64_t n = S.n;

@@ -75,4 +75,7 @@ int choose_tail(const HostPlan &P, bool upper);
 int build_plan(const Symbolic &S, const int64_t *A_rp, const int64_t *A_ci, int64_t in_nnz,
                const int64_t *gen_src, HostPlan &P);
 
+// Invariants of the chain task lists (kkt_plan_check).
+void check_chains(const HostPlan &P, int64_t out[8]);
+
 }  // namespace kkt
