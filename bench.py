@@ -480,9 +480,11 @@ def main():
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
-    pipe.run([(hp[k][0], hp[k][1], hx[s % 2], policy(host[k][2])) for s, k in enumerate(ks)])
+    e2e_reps = pipe.run([(hp[k][0], hp[k][1], hx[s % 2], policy(host[k][2]))
+                         for s, k in enumerate(ks)])
     torch.cuda.synchronize()
     e2e_total = reduce_max((time.perf_counter() - t0) * 1e3, dist, dev.device)
+    e2e_conv = sum(int(bool(q.converged)) for rp in e2e_reps for q in rp)
     e2e_value = e2e_total / n_job
     # the PCIe floor of the e2e leg: this box's pinned H2D bandwidth (one step's input size)
     h2d_bytes = 8 * B * (nnz_lower + N)
@@ -688,7 +690,8 @@ def main():
                     "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": 8 * B * N,
                     "h2d_gbs_measured": h2d_gbs,
-                    "pcie_floor_ms_per_system": h2d_bytes / (h2d_gbs * 1e6) / B},
+                    "pcie_floor_ms_per_system": h2d_bytes / (h2d_gbs * 1e6) / B,
+                    "converged_rank0": e2e_conv, "systems_rank0": B * len(ks)},
             "sequence": sequence,
             "fixed_delta": fixed,
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": kd["GBs"], "peak": peak,

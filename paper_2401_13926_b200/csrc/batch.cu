@@ -632,13 +632,20 @@ __host__ __device__ constexpr int ts_slots(int stg) { return stg + 6 * 32 + 8; }
 
 size_t b_tma_smem_ns(int xp, int ns, int stg) {
   return (size_t)ns * stg * TS_SC * 8 + (size_t)ns * ts_slots(stg) * 4 + (size_t)ns * 33 * 16 + 2 * ns * 8 +
+         (size_t)ns * 32 * 4 +
          (size_t)xp * TS_SC * 8 + 64;
 }
-void b_tma_shape(int *ns, int *stg) {  // KKT_B_TMA=ns,rows among the instantiated shapes
+// Stage ring of the wide-column replay: 2 x 256 rows, unless the widest pattern then leaves
+// room for only one CTA per SM and 2 x 128 rows fit two (70k x 8: 47.7 -> 42.5 ms; at 10k,
+// 3 CTAs/SM either way, 128 rows measured slower: 5.91 -> 6.41 ms).
+// KKT_B_TMA=ns,rows picks among the instantiated shapes.
+void b_tma_shape(int xp, int *ns, int *stg) {
   int a = 2, b = 256;
+  constexpr size_t HALF_SM = 113 * 1024;
+  if (b_tma_smem_ns(xp, 2, 256) > HALF_SM && b_tma_smem_ns(xp, 2, 128) <= HALF_SM) b = 128;
   if (const char *e = std::getenv("KKT_B_TMA")) std::sscanf(e, "%d,%d", &a, &b);
   if (!((a == 2 && b == 256) || (a == 3 && b == 160) || (a == 4 && b == 128) || (a == 3 && b == 256) ||
-        (a == 2 && b == 384))) {
+        (a == 2 && b == 384) || (a == 2 && b == 128))) {
     a = 2;
     b = 256;
   }
@@ -695,8 +702,13 @@ template <int E>
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(E * TS_SC) : "memory"); }
 
 // TS_E entry lanes per system: 32 (3 CTAs/SM) or 64 (the 70k-class tail, one CTA per SM)
-template <int TS_NS, int TS_STG, int TS_E>
-__global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
+// FLAGS = false (KKT_B_TMA_DIRECT=3): no column flags at all — the producer stages every step
+// as soon as its metadata is in (no so_dep -> flag round trips per chunk) and every staged
+// value is checked by its consumer (a sentinel = staged before it was published: polled in
+// L2).  Default where the widest pattern leaves one or two CTAs per SM (70k x 8: 43.2 ->
+// 40.5 ms); at 10k (3 CTAs/SM) the flagged producer is faster (5.87 vs 6.09 ms).
+template <int TS_NS, int TS_STG, int TS_E, bool FLAGS = true>
+__global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? (TS_NS * TS_STG <= 384 ? 4 : 3) : 1)
     k_b_refactor_tma(const __grid_constant__ DevPlan d, const int2 *__restrict__ tasks, int ntask) {
   constexpr int TS_SLOTS = ts_slots(TS_STG);
   extern __shared__ __align__(1024) unsigned char tsm[];
@@ -708,6 +720,7 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(hdr + TS_NS);
   uint64_t *empty = full + TS_NS;
   double *x = reinterpret_cast<double *>(empty + TS_NS);                             // [xp][8]
+  int *lidx0 = reinterpret_cast<int *>(x + (size_t)d.h_xp * TS_SC);                  // [NS][32]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < TS_NS; ++i) {
@@ -718,6 +731,7 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
   }
   __syncthreads();
   const int G = d.nbp / TS_SC;
+  constexpr bool flags = FLAGS;
   int stage = 0;
   unsigned phase = 0;  // ring position: producer and consumers walk the same chunk sequence
   while (true) {
@@ -743,7 +757,7 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
       int pdep = -1, pfl = 1;
       if (t0 + lane < t_end) {
         pm = d.so_meta[t0 + lane];
-        pdep = d.so_dep[t0 + lane - d.so_dep0];
+        if (flags) pdep = d.so_dep[t0 + lane - d.so_dep0];
         if (pdep >= 0) pfl = ld_acquire_i32(d.cflag + (size_t)pdep * G + g);
       }
       while (t0 < t_end) {
@@ -785,7 +799,7 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
           pfl = 1;
           if (nt0 + lane < t_end) {
             pm = d.so_meta[nt0 + lane];
-            pdep = d.so_dep[nt0 + lane - d.so_dep0];
+            if (flags) pdep = d.so_dep[nt0 + lane - d.so_dep0];
           }
         }
         const bool mine = lane < nsteps;
@@ -814,7 +828,10 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
         if (mine && dep >= 0 && !(direct && lane == 0)) asm volatile("fence.proxy.async.global;" ::: "memory");
         mbar_wait(&empty[stage], phase ^ 1);
         int4 *meta = meta0 + stage * 32;
-        if (mine) meta[lane] = make_int4(m.x, m.y, (direct && lane == 0) ? -(m.w + 1) : incl - r, sincl - sw + mis);
+        if (mine) {
+          meta[lane] = make_int4(m.x, m.y, (direct && lane == 0) ? -(m.w + 1) : incl - r, sincl - sw + mis);
+          if (!flags) lidx0[stage * 32 + lane] = m.w;
+        }
         const int rows = __shfl_sync(FULL, incl, nsteps - 1) - (direct ? __shfl_sync(FULL, r, 0) : 0);
         const int ints = __shfl_sync(FULL, sincl, nsteps - 1);
         if (lane == 0) hdr[stage] = make_int4(nsteps, nt0 >= t_end ? 1 : 0, 0, 0);
@@ -871,6 +888,7 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
           const double *stv = stv0 + (size_t)stage * TS_STG * TS_SC;
           const int *sts = sts0 + stage * TS_SLOTS;
           const int4 *meta = meta0 + stage * 32;
+          const int *lidx = lidx0 + stage * 32;
           for (int i = 0; i < h.x; ++i) {
             const int4 m = meta[i];  // {slot of k, entries, first staged row, first staged slot}
             const double xk = x[m.x * TS_SC + s];
@@ -883,6 +901,8 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
                 if (idx < m.y) {
                   if (m.z >= 0) {
                     lv[q] = stv[(m.z + idx) * TS_SC + s];
+                    if (!flags && is_sentinel(lv[q]))  // staged before it was published
+                      lv[q] = wait_value_bo(&d.Lx[IL(d, lidx[i] + idx, sys)], 32);
                   } else {  // unstaged (late) step: straight from L2, each value its own flag
                     const double *p = &d.Lx[IL(d, -m.z - 1 + idx, sys)];
                     lv[q] = ld_relaxed_f64(p);
@@ -922,9 +942,11 @@ __global__ void __launch_bounds__(ts_threads(TS_E), TS_E == 32 ? 3 : 1)
         st_relaxed_f64(&d.Lx[IL(d, lb + i, sys)], unsentinel(__ddiv_rn(v, ujj)));
       }
       if (d.poll_ns < 0) __threadfence();  // (diagnostic: per-thread fences)
-      consumer_bar<TS_E>();  // every L(:,j) store of the CTA precedes the release below
-      if (trc && ct == 0) trc[6] = globaltimer();
-      if (ct == 0) st_release_i32(&d.cflag[(size_t)(j - d.J2) * G + g], 1);
+      if (flags) {
+        consumer_bar<TS_E>();  // every L(:,j) store of the CTA precedes the release below
+        if (trc && ct == 0) trc[6] = globaltimer();
+        if (ct == 0) st_release_i32(&d.cflag[(size_t)(j - d.J2) * G + g], 1);
+      }
       if (trc && ct == 0) trc[1] = globaltimer();
       for (int i = e; i < nl; i += TS_E)
         // (recomputed rather than parked in x: a shared-memory write-back on the chain's
@@ -972,20 +994,23 @@ cudaError_t b_tma_maps(DevPlan &d) {
   return cudaSuccess;
 }
 
-template <int NS, int STG, int E = 32>
+template <int NS, int STG, int E = 32, bool F = true>
 static cudaError_t tma_conf(size_t smem, int *blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_b_refactor_tma<NS, STG, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_b_refactor_tma<NS, STG, E, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_b_refactor_tma<NS, STG, E>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    e = cudaFuncSetAttribute(k_b_refactor_tma<NS, STG, E, F>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_tma<NS, STG, E>, ts_threads(E), smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_b_refactor_tma<NS, STG, E, F>, ts_threads(E), smem);
   return e;
 }
-cudaError_t b_tma_configure(int ns, int stg, int e, size_t smem, int *blocks_per_sm) {
+cudaError_t b_tma_configure(int ns, int stg, int e, bool flags, size_t smem, int *blocks_per_sm) {
+  if (!flags && e == 32 && ns == 2 && stg == 128) return tma_conf<2, 128, 32, false>(smem, blocks_per_sm);
+  if (!flags && e == 32 && ns == 2 && stg == 256) return tma_conf<2, 256, 32, false>(smem, blocks_per_sm);
   if (e == 64) return tma_conf<2, 256, 64>(smem, blocks_per_sm);
   if (ns == 3 && stg == 256) return tma_conf<3, 256>(smem, blocks_per_sm);
   if (ns == 2 && stg == 384) return tma_conf<2, 384>(smem, blocks_per_sm);
+  if (ns == 2 && stg == 128) return tma_conf<2, 128>(smem, blocks_per_sm);
   return ns == 4 ? tma_conf<4, 128>(smem, blocks_per_sm)
                  : ns == 3 ? tma_conf<3, 160>(smem, blocks_per_sm) : tma_conf<2, 256>(smem, blocks_per_sm);
 }
@@ -2027,6 +2052,11 @@ cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm, bool wide) 
                                                                      : cta_conf<4>(smem, blocks_per_sm, false);
 }
 
+// the wide-column replay runs its flag-free variant (no column flags to reset)
+static bool tma_flag_free(const DevPlan &d) {
+  return d.tma_direct == 3 && d.tma_e == 32 && d.tma_ns == 2 && (d.tma_stg == 128 || d.tma_stg == 256);
+}
+
 cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blocks2, size_t smem2,
                               cudaStream_t s, long long *launches, cudaStream_t s2, cudaEvent_t ev_a,
                               cudaEvent_t ev_b, int blocks_ov) {
@@ -2053,7 +2083,7 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blo
   const bool ov = two && d.n_btask1 && s2 && ev_a && ev_b && blocks_ov > 0;
   if (two) {
     cudaError_t e2 = cudaMemsetAsync(d.ticket2, 0, 4, s);
-    if (e2 == cudaSuccess && d.ct_mode == 3)
+    if (e2 == cudaSuccess && d.ct_mode == 3 && !tma_flag_free(d))
       e2 = cudaMemsetAsync(d.cflag, 0, 4 * (size_t)(d.n - d.J2) * (d.nbp / TS_SC), s);
     if (e2 != cudaSuccess) return e2;
   }
@@ -2061,9 +2091,13 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blo
     const int2 *t2 = d.btask + d.n_btask1;
     const int n2 = d.n_btask - d.n_btask1;
     if (d.ct_mode == 3) {
-      if (d.tma_e == 64) k_b_refactor_tma<2, 256, 64><<<blocks2, ts_threads(64), smem2, st>>>(d, t2, n2);
+      const bool nf = tma_flag_free(d);
+      if (nf && d.tma_stg == 128) k_b_refactor_tma<2, 128, 32, false><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else if (nf && d.tma_stg == 256) k_b_refactor_tma<2, 256, 32, false><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else if (d.tma_e == 64) k_b_refactor_tma<2, 256, 64><<<blocks2, ts_threads(64), smem2, st>>>(d, t2, n2);
       else if (d.tma_ns == 3 && d.tma_stg == 256) k_b_refactor_tma<3, 256, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
       else if (d.tma_ns == 2 && d.tma_stg == 384) k_b_refactor_tma<2, 384, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
+      else if (d.tma_ns == 2 && d.tma_stg == 128) k_b_refactor_tma<2, 128, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
       else if (d.tma_ns == 4) k_b_refactor_tma<4, 128, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
       else if (d.tma_ns == 3) k_b_refactor_tma<3, 160, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);
       else k_b_refactor_tma<2, 256, 32><<<blocks2, TS_THREADS, smem2, st>>>(d, t2, n2);

@@ -230,7 +230,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
       for (int j = 0; j < std::min(d.J0, h.n); ++j)
         maxnp = std::max<int>(maxnp, (int)((h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j])));
       int ns = 2, stg = 256;
-      b_tma_shape(&ns, &stg);
+      b_tma_shape(maxnp, &ns, &stg);
       if (mode == 3 && sc == 8 && b_tma_smem(maxnp, ns, stg) <= 74 * 1024) split_np = 144;
     }
     if (std::getenv("KKT_B_SPLIT_NP")) split_np = std::atoi(std::getenv("KKT_B_SPLIT_NP"));
@@ -613,7 +613,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
     int rbps = 0, tbps = 0;
     dev->refactor_smem = b_refactor_smem(d.b_xbudget, d.b_stage);
     if (d.ct_mode == 3) {
-      b_tma_shape(&d.tma_ns, &d.tma_stg);
+      b_tma_shape(std::max(d.h_xp, 1), &d.tma_ns, &d.tma_stg);
       // KKT_B_TMA_E=64: 16 consumer warps per CTA (measured at 70k, one CTA per SM: 96.6 ->
       // 98.0 ms, so 32 entry lanes stay the default everywhere)
       d.tma_e = std::getenv("KKT_B_TMA_E") ? std::atoi(std::getenv("KKT_B_TMA_E")) : 32;
@@ -623,6 +623,9 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
       } else {
         d.tma_e = 32;
       }
+      // flag-free producer where the stage ring was cut to 128 rows (wide patterns, one or
+      // two CTAs per SM: batch.cu k_b_refactor_tma FLAGS)
+      if (!std::getenv("KKT_B_TMA_DIRECT")) d.tma_direct = (d.tma_e == 32 && d.tma_stg == 128) ? 3 : 2;
     }
     const size_t smem2 = d.ct_mode == 3 ? b_tma_smem(std::max(d.h_xp, 1), d.tma_ns, d.tma_stg)
                                         : b_cta_smem(std::max(d.h_xp, 1), d.ct_sc);
@@ -630,7 +633,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
     d.b_gridv = b_grid_variant();
     CUDA_TRY(b_configure(nbp, dev->refactor_smem, d.b_gridv, &rbps, &tbps));
     if (d.ct_mode == 3) {
-      CUDA_TRY(b_tma_configure(d.tma_ns, d.tma_stg, d.tma_e, smem2, &rbps2));
+      CUDA_TRY(b_tma_configure(d.tma_ns, d.tma_stg, d.tma_e, d.tma_direct != 3, smem2, &rbps2));
       CUDA_TRY(b_tma_maps(d));
     } else {
       CUDA_TRY(b_cta_configure(d.ct_sc, smem2, &rbps2, d.ct_mode == 2));

@@ -218,9 +218,9 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blo
                               cudaEvent_t ev_a = nullptr, cudaEvent_t ev_b = nullptr, int blocks_ov = 0);
 cudaError_t b_refactor_occupancy(size_t smem, int *blocks_per_sm);
 size_t b_cta_smem(int xp, int sc);
-void b_tma_shape(int *ns, int *stg);
+void b_tma_shape(int xp, int *ns, int *stg);
 size_t b_tma_smem(int xp, int ns, int stg);
-cudaError_t b_tma_configure(int ns, int stg, int e, size_t smem, int *blocks_per_sm);
+cudaError_t b_tma_configure(int ns, int stg, int e, bool flags, size_t smem, int *blocks_per_sm);
 cudaError_t b_tma_maps(DevPlan &d);  // encode d.tmL over d.Lx
 cudaError_t b_cta_configure(int sc, size_t smem, int *blocks_per_sm, bool wide);
 cudaError_t b_launch_diag_stats(const DevPlan &d, cudaStream_t s);

@@ -27,6 +27,10 @@ pytestmark = pytest.mark.gpu
     ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TAIL_ORDER": "1"}),
     ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_DIRECT": "1"}),
     ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_E": "64"}),
+    # flag-free wide-column producer (default with the 128-row ring: 70k-class patterns)
+    ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_DIRECT": "3"}),
+    ("acopf_small", 40, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA": "2,128"}),
+    ("standard_trace", 9, {"KKT_B_SPLIT_NP": "4", "KKT_B_TMA": "2,128", "KKT_B_TMA_DIRECT": "2"}),
     # solve variants: grid-solve (chunk, CTAs/SM), sweep look-ahead / width, U head prefix
     ("acopf_small", 33, {"KKT_B_GRIDV": "0"}), ("standard_trace", 9, {"KKT_B_GRIDV": "1"}),
     ("acopf_small", 40, {"KKT_B_GRIDV": "2"}), ("acopf_small", 33, {"KKT_B_GRIDV": "4"}),

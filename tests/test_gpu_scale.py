@@ -86,13 +86,17 @@ def test_full_size_against_oracle(config, k):
 
 
 @pytest.mark.parametrize("config,nb", [("activsg200", 4), ("activsg10k", 4), ("activsg2000", 40),
-                                       ("activsg10k/0.95", 4),
+                                       ("activsg10k/0.95", 4), ("activsg10k/ring128", 8),
                                        pytest.param("activsg70k", 8, marks=pytest.mark.slow)])
-def test_full_size_batch_equals_single(config, nb):
+def test_full_size_batch_equals_single(config, nb, monkeypatch):
     """The interleaved batch reproduces each system's single-system factors and solve (nb = 40:
     8-system groups of the TMA wide-column pipeline, every group's done flags and the
-    padding systems of the last 32-block)."""
+    padding systems of the last 32-block; ring128: the 128-row stage ring with the flag-free
+    producer, the default for 70k-class patterns, forced at 10k)."""
     import torch
+    if config.endswith("/ring128"):
+        config = config[:-len("/ring128")]
+        monkeypatch.setenv("KKT_B_TMA", "2,128")
     import paper_2401_13926_b200._native as nat
     from paper_2401_13926_b200.acopf import system_rhs, system_values
     from paper_2401_13926_b200.device import DeviceSystem
