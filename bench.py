@@ -598,8 +598,10 @@ def main():
             sv_t = torch.from_numpy(sv).to(d1.device)
             sr_t = torch.from_numpy(sr).to(d1.device)
             sx_t = torch.empty(N, dtype=torch.float64, device=d1.device)
-        for k in range(3):
-            d1.step(sv_t[k], LOWER, sr_t[k], sx_t, True, 10, 10, sd[k])
+        # warm-up with the timed call's arguments: the last (IR-triggering) systems first, so
+        # every FGMRES graph variant the timed loop uses is captured before it
+        for k in (M - 2, M - 3, 0, 1, 2):
+            d1.step(sv_t[k], LOWER, sr_t[k], sx_t, True, 10, 10, sd[k], stats=True)
         lat, its1, rr1 = [], [], []
         for k in range(M - 1):
             with torch.cuda.stream(d1.stream):
