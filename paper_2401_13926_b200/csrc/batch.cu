@@ -33,6 +33,9 @@ namespace kkt {
 static int rowwise();  // KKT_B_SPMV_TILES (below)
 constexpr int BY = 8;            // rows (warps) per block of the 2-D row kernels
 constexpr int SMALL_PAT_B = 64;
+// refactor: A-scatter / finalize entries per lane per round of independent loads (the index
+// loads of a round, then its value loads, are in flight together: 5.87 -> 5.77 ms at 10k x 64)
+constexpr int B_AU = 4;  // (the same in k_b_refactor_small cost occupancy: 5.77 -> 5.83 ms)
 constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ double sentinel_value() {
@@ -332,8 +335,24 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d, const in
     for (int f = lane; f < np * S; f += 32) x[f] = 0.0;
     __syncwarp();
     // x[a_tgt] = avals[a_src]                                                 (:323)
-    for (int q = ti.a0 + e; q < ti.a1; q += E)
-      x[d.a_slot[q] * S + s] = d.A_vals[IL(d, d.a_src[q], sys)];
+    // (B_AU entries per lane per round: their index loads, then their value loads, are
+    // independent — two round trips per round instead of two per entry)
+    for (int q0 = ti.a0 + e; q0 < ti.a1; q0 += B_AU * E) {
+      int sl[B_AU], src[B_AU];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (q0 + u * E < ti.a1) {
+          sl[u] = d.a_slot[q0 + u * E];
+          src[u] = d.a_src[q0 + u * E];
+        }
+      double v[B_AU];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (q0 + u * E < ti.a1) v[u] = d.A_vals[IL(d, src[u], sys)];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (q0 + u * E < ti.a1) x[sl[u] * S + s] = v[u];
+    }
     __syncwarp();
     cur_task = __shfl_sync(FULL, ticket, 0);
     nt = load_task(d, tasks, ntask, cur_task);  // consumed next iteration
@@ -408,12 +427,32 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d, const in
       st_relaxed_f64(&d.Lx[IL(d, lb + idx, sys)], l);
       x[(nu + 1 + idx) * S + s] = l;  // (each lane rereads only its own entries below)
     }
-    for (int idx = e; idx < nl; idx += E) d.Lv[IL(d, d.Lmap[lb + idx], sys)] = x[(nu + 1 + idx) * S + s];
-    for (int idx = e; idx < nu; idx += E) {
-      const double v = x[idx * S + s];
-      d.Ux[IL(d, ub + idx, sys)] = v;
-      d.Uv[IL(d, d.Umap[ub + idx], sys)] = v;
-      gm = fmax(gm, fabs(v));
+    // scatter into the solve layouts: a round's map indices are loaded before its stores
+    // (the compiler may not hoist them over the possibly aliasing stores)
+    for (int i0 = e; i0 < nl; i0 += B_AU * E) {
+      int mp[B_AU];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (i0 + u * E < nl) mp[u] = d.Lmap[lb + i0 + u * E];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (i0 + u * E < nl) d.Lv[IL(d, mp[u], sys)] = x[(nu + 1 + i0 + u * E) * S + s];
+    }
+    for (int i0 = e; i0 < nu; i0 += B_AU * E) {
+      int mp[B_AU];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (i0 + u * E < nu) mp[u] = d.Umap[ub + i0 + u * E];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u) {
+        const int idx = i0 + u * E;
+        if (idx < nu) {
+          const double v = x[idx * S + s];
+          d.Ux[IL(d, ub + idx, sys)] = v;
+          d.Uv[IL(d, mp[u], sys)] = v;
+          gm = fmax(gm, fabs(v));
+        }
+      }
     }
     for (int o = S; o < 32; o <<= 1) gm = fmax(gm, __shfl_xor_sync(FULL, gm, o));
     if (e == 0) {

@@ -3,7 +3,7 @@ T=$1; C=$2; B=$3; shift 3
 L=paper_2401_13926_b200/libkktb200.so
 cp $L /tmp/keep.so
 for rep in 1 2; do
-  for lib in old new; do
+  for lib in ${LIBS:-old new}; do
     cp ablib/$lib.so $L
     for E in "$@"; do
       echo "== $lib $E" >> gpurun_out/${T}_libab.txt
