@@ -20,6 +20,7 @@ pytestmark = pytest.mark.gpu
 
 CONFIGS = [("activsg200", 19), ("activsg2000", 19), ("activsg10k", 19),
            ("activsg10k/0.95", 19),  # the off-diagonal pivoting regime at 238k (4,214 pivots)
+           ("activsg10k/0.9", 19),   # 8,336 pivots, 390M update pairs per refactorization
            pytest.param("activsg70k", 19, marks=pytest.mark.slow)]
 
 
@@ -86,7 +87,8 @@ def test_full_size_against_oracle(config, k):
 
 
 @pytest.mark.parametrize("config,nb", [("activsg200", 4), ("activsg10k", 4), ("activsg2000", 40),
-                                       ("activsg10k/0.95", 4), ("activsg10k/ring128", 8),
+                                       ("activsg10k/0.95", 4), ("activsg10k/0.9", 4),
+                                       ("activsg10k/ring128", 8),
                                        pytest.param("activsg70k", 8, marks=pytest.mark.slow)])
 def test_full_size_batch_equals_single(config, nb, monkeypatch):
     """The interleaved batch reproduces each system's single-system factors and solve (nb = 40:
