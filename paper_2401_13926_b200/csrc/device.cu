@@ -332,6 +332,46 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   d.n_small_levels = h.n_small_levels;
   for (int l = 0; l <= h.n_small_levels; ++l) d.lev_ptr[l] = h.small_lev_ptr[l];
   d.ref_start = h.small_lev_ptr[h.n_small_levels];
+  // Single system: the columns from the first pattern wider than KKT_REF_WIDE_NP slots (the
+  // separator tail) go to k_refactor_wide, a CTA per column; col_order past the small levels
+  // is uploaded as [warp-kernel columns | wide columns], each part in its level order (a wide
+  // column only depends on smaller columns, so the split is a valid kernel boundary).
+  d.ref_n1 = h.n - d.ref_start;
+  std::vector<int32_t> corder;
+  if (nbp == 1) {
+    const int wide_np = std::getenv("KKT_REF_WIDE_NP") ? std::atoi(std::getenv("KKT_REF_WIDE_NP")) : 128;
+    int JW = h.n;
+    for (int j = 0; wide_np > 0 && j < h.n; ++j)
+      if ((h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j]) > wide_np) {
+        JW = j;
+        break;
+      }
+    if (JW < h.n) {
+      std::vector<int32_t> light, wide;
+      int maxsteps = 0, maxcnt = 0;
+      for (int c = d.ref_start; c < h.n; ++c) {
+        const int j = h.col_order[c];
+        if (j < JW) {
+          light.push_back(j);
+          continue;
+        }
+        wide.push_back(j);
+        maxsteps = std::max<int>(maxsteps, (int)(h.so_ptr[j + 1] - h.so_ptr[j]));
+        for (int64_t t = h.so_ptr[j]; t < h.so_ptr[j + 1]; ++t) maxcnt = std::max<int>(maxcnt, h.so_meta[4 * t + 1]);
+      }
+      const int slot = std::max(1, std::min(maxcnt, 1024));  // wider steps: straight from L2
+      const size_t smem = refactor_wide_smem(h.maxpat, maxsteps, slot);
+      if (!wide.empty() && smem <= 200 * 1024) {
+        corder.assign(h.col_order.begin(), h.col_order.begin() + d.ref_start);
+        corder.insert(corder.end(), light.begin(), light.end());
+        corder.insert(corder.end(), wide.begin(), wide.end());
+        d.ref_n1 = (int)light.size();
+        d.ref_wslot = slot;
+        d.ref_wsteps = maxsteps;
+        d.ref_wsmem = smem;
+      }
+    }
+  }
   d.poll_ns = std::getenv("KKT_POLL_NS") ? std::atoi(std::getenv("KKT_POLL_NS")) : (nbp > 1 ? 64 : 0);
   // single system: one lane waits on the critical dependency before the row (without it the
   // lanes poll their unpublished columns at once: 1.27 -> 3.16 ms at 10k); batch: no up-front
@@ -510,7 +550,11 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   UP(d.so_ptr, to_i32(h.so_ptr));
   UP(d.ap_ptr, to_i32(h.ap_ptr));
   UP(d.a_src, h.a_src);
-  UP(d.col_order, h.col_order);
+  if (corder.empty()) {
+    UP(d.col_order, h.col_order);
+  } else {
+    UP(d.col_order, corder);
+  }
   UP(d.Lp, to_i32(h.Lp));
   UP(d.Up, to_i32(h.Up));
   UP(d.Lmap, h.Lmap);
@@ -685,6 +729,11 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   int bps = 0;
   CUDA_TRY(refactor_configure(dev->refactor_warps, dev->refactor_smem, d.ref_buf, &bps));
   dev->refactor_blocks = std::max(1, bps) * dev->sm_count;
+  if (d.ref_start + d.ref_n1 < n) {
+    int wb = 0;
+    CUDA_TRY(refactor_wide_configure(d.ref_wsmem, &wb));
+    d.ref_wblocks = std::max(1, wb) * dev->sm_count;
+  }
   int tb = 0;
   CUDA_TRY(trsv_configure(&tb));
   dev->trsv_blocks = std::max(1, tb) * dev->sm_count;

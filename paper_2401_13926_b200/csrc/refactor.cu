@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
   double *x = smem + (size_t)wib * wstride;
   double *st_l = x + d.maxpat;
   int *st_s = reinterpret_cast<int *>(st_l + 2 * BUF);
-  const int ntask = (d.n - d.ref_start) * d.nb;
+  const int ntask = d.ref_n1 * d.nb;  // (single system with wide columns: the light ones only)
   while (true) {
     int task = 0;
     if (lane == 0) task = atomicAdd(d.ticket, 1);
@@ -308,6 +308,137 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
 }
 
 // ----------------------------------------------------------------------------
+// Single system, wide columns (j >= JW, the separator tail; second launch): one CTA of
+// WIDE_NT threads per column instead of one warp, so a step's |L(:,k)| entries and the
+// column's divisions are spread over 256 lanes.  Columns are dispatched by ticket in DAG-level
+// order (a column only waits on columns of earlier tickets or of the first launch: deadlock-
+// free with any number of resident CTAs).  The column's step metadata is staged in shared
+// memory once; each step's L(:,k) values and slots are cp.async'ed WIDE_AHEAD steps ahead into
+// a ring of WIDE_AHEAD + 2 slots (the slot written at step t was last read at step t - 2, so
+// one barrier per step suffices).  A value staged before it was published is the sentinel and
+// is polled in L2 at use.  Steps wider than a ring slot are replayed straight from L2.
+// Every workspace entry still receives its updates in so(j) order => bitwise the same factors.
+// ----------------------------------------------------------------------------
+constexpr int WIDE_NT = 256;
+constexpr int WIDE_AHEAD = 3;
+constexpr int WIDE_Q = WIDE_AHEAD + 2;
+
+size_t refactor_wide_smem(int maxpat, int maxsteps, int slot) {
+  return ((size_t)maxpat + 1) / 2 * 16 + (size_t)maxsteps * 16 + (size_t)WIDE_Q * slot * 12 + 64;
+}
+
+__global__ void __launch_bounds__(WIDE_NT) k_refactor_wide(DevPlan d) {
+  extern __shared__ __align__(16) double wsm[];
+  __shared__ int s_task;
+  __shared__ double s_gm[WIDE_NT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int SL = d.ref_wslot;
+  double *x = wsm;                                                              // [maxpat]
+  int4 *meta = reinterpret_cast<int4 *>(wsm + ((d.maxpat + 1) & ~1));          // [maxsteps]
+  double *rv = reinterpret_cast<double *>(meta + d.ref_wsteps);                 // [Q][SL]
+  int *rs = reinterpret_cast<int *>(rv + (size_t)WIDE_Q * SL);                  // [Q][SL]
+  const int nw = d.n - d.ref_start - d.ref_n1;
+  const double eps = patch_floor(d, 0);
+  while (true) {
+    if (tid == 0) s_task = atomicAdd(d.ticket2, 1);
+    __syncthreads();
+    const int task = s_task;
+    if (task >= nw) break;
+    const int j = d.col_order[d.ref_start + d.ref_n1 + task];
+    const int ub = d.Up[j], nu = d.Up[j + 1] - ub;
+    const int lb = d.Lp[j], nl = d.Lp[j + 1] - lb;
+    const int np = nu + 1 + nl;
+    const int t0 = d.so_ptr[j], ns = d.so_ptr[j + 1] - t0;
+    for (int t = tid; t < ns; t += WIDE_NT) cp_async16(&meta[t], &d.so_meta[t0 + t]);
+    cp_async_commit();
+    for (int f = tid; f < np; f += WIDE_NT) x[f] = 0.0;
+    __syncthreads();
+    // x[a_tgt] = avals[a_src]                                                 (:323)
+    for (int q = d.ap_ptr[j] + tid; q < d.ap_ptr[j + 1]; q += WIDE_NT) x[d.a_slot[q]] = d.A_vals[d.a_src[q]];
+    cp_async_wait<0>();
+    __syncthreads();
+    // stage step t into ring slot t % Q (one commit group per step and thread, maybe empty)
+    auto issue = [&](int t) {
+      if (t < ns) {
+        const int4 m = meta[t];  // {slot of k, |L(:,k)|, first pair, first L index}
+        if (m.y <= SL) {
+          double *v = rv + (size_t)(t % WIDE_Q) * SL;
+          int *sl = rs + (size_t)(t % WIDE_Q) * SL;
+          for (int e = tid; e < m.y; e += WIDE_NT) {
+            cp_async8(&v[e], &d.Lx[m.w + e]);
+            cp_async4(&sl[e], &d.upd_slot32[m.z + e]);
+          }
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int a = 0; a < WIDE_AHEAD; ++a) issue(a);
+    // for k in so(j) (topological): x[Li(k)] -= Lx(k) * x[k]                  (:324-326)
+    for (int t = 0; t < ns; ++t) {
+      issue(t + WIDE_AHEAD);             // into the slot step t - 2 used (finished: barrier)
+      cp_async_wait<WIDE_AHEAD>();       // this thread's copies of step t have landed
+      __syncthreads();                   // everyone's, and step t - 1's updates of x
+      const int4 m = meta[t];
+      const double xk = x[m.x];
+      if (m.y <= SL) {
+        const double *v = rv + (size_t)(t % WIDE_Q) * SL;
+        const int *sl = rs + (size_t)(t % WIDE_Q) * SL;
+        for (int e = tid; e < m.y; e += WIDE_NT) {
+          double l = v[e];
+          if (is_sentinel(l)) l = wait_value(&d.Lx[m.w + e], d.poll_ns);  // staged before published
+          const int q = sl[e];
+          x[q] = __dsub_rn(x[q], __dmul_rn(l, xk));
+        }
+      } else {  // wider than a ring slot: straight from L2
+        for (int e = tid; e < m.y; e += WIDE_NT) {
+          const double l = wait_value_backoff(&d.Lx[m.w + e]);
+          const int q = d.upd_slot32[m.z + e];
+          x[q] = __dsub_rn(x[q], __dmul_rn(l, xk));
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj (published first); U(:,j) = x[Ui]  (:327-344)
+    double ujj = x[nu];
+    double gm = fabs(ujj);
+    const bool patched = fabs(ujj) < eps;
+    if (patched) ujj = (ujj >= 0.0) ? eps : -eps;
+    for (int q = tid; q < nl; q += WIDE_NT) {
+      const double v = x[nu + 1 + q];
+      gm = fmax(gm, fabs(v));
+      const double l = unsentinel(__ddiv_rn(v, ujj));
+      st_relaxed_f64(&d.Lx[lb + q], l);  // value == readiness
+      x[nu + 1 + q] = l;                 // (the same thread rereads it below)
+    }
+    for (int q = tid; q < nl; q += WIDE_NT) d.Lv[d.Lmap[lb + q]] = x[nu + 1 + q];
+    for (int q = tid; q < nu; q += WIDE_NT) {
+      const double v = x[q];
+      d.Ux[ub + q] = v;
+      d.Uv[d.Umap[ub + q]] = v;
+      gm = fmax(gm, fabs(v));
+    }
+    gm = warp_max(gm);
+    if (lane == 0) s_gm[warp] = gm;
+    __syncthreads();  // also: the workspace is reused by the next task
+    if (tid == 0) {
+      double g = 0.0;
+      for (int w = 0; w < WIDE_NT / 32; ++w) g = fmax(g, s_gm[w]);
+      d.udiag[j] = ujj;
+      if (patched) atomicAdd(&d.scal[SC_PATCHED], 1ull);
+      atomic_max_nonneg(&d.scal[SC_GMAX], g);
+    }
+  }
+}
+
+cudaError_t refactor_wide_configure(size_t smem, int *blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_refactor_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_refactor_wide, WIDE_NT, smem);
+}
+
+// ----------------------------------------------------------------------------
 // Wide leading levels (level 0: no replay steps; level 1: <= a few) hold most columns but
 // almost no work: one thread per (column, system), one launch per level (the kernel
 // boundary is the dependency), workspace in local memory.  Same arithmetic as k_refactor.
@@ -462,6 +593,12 @@ cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem
     if (d.ref_buf == 512) k_refactor<512><<<blocks, 32 * warps, smem, s>>>(d);
     else if (d.ref_buf == 128) k_refactor<128><<<blocks, 32 * warps, smem, s>>>(d);
     else k_refactor<256><<<blocks, 32 * warps, smem, s>>>(d);
+    ++*launches;
+  }
+  if (d.ref_start + d.ref_n1 < d.n) {  // single system: the wide columns, CTA per column
+    e = cudaMemsetAsync(d.ticket2, 0, 4, s);
+    if (e != cudaSuccess) return e;
+    k_refactor_wide<<<d.ref_wblocks, WIDE_NT, d.ref_wsmem, s>>>(d);
     ++*launches;
   }
   return cudaGetLastError();

@@ -15,7 +15,8 @@ from paper_2401_13926_b200.device import DeviceSystem
 cfg = sys.argv[1]
 B = int(sys.argv[2])
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-pat = build_pattern(ACOPF_CONFIGS[cfg], 0)
+cfg_name, _, frac = cfg.partition("/")  # CONFIG or CONFIG/imbalance_frac
+pat = build_pattern(ACOPF_CONFIGS[cfg_name], 0, imbalance_frac=float(frac or 1.0))
 f, _ = factorize(to_general(pat.K.with_values(system_values(pat, 0, 0))))
 dev = DeviceSystem(f, batch=B)
 ks = [1 + q % 19 for q in range(B)]
