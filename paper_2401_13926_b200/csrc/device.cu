@@ -349,6 +349,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
     if (JW < h.n) {
       std::vector<int32_t> light, wide;
       int maxsteps = 0, maxcnt = 0;
+      int64_t wsteps = 0, wpairs = 0;
       for (int c = d.ref_start; c < h.n; ++c) {
         const int j = h.col_order[c];
         if (j < JW) {
@@ -357,7 +358,11 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
         }
         wide.push_back(j);
         maxsteps = std::max<int>(maxsteps, (int)(h.so_ptr[j + 1] - h.so_ptr[j]));
-        for (int64_t t = h.so_ptr[j]; t < h.so_ptr[j + 1]; ++t) maxcnt = std::max<int>(maxcnt, h.so_meta[4 * t + 1]);
+        for (int64_t t = h.so_ptr[j]; t < h.so_ptr[j + 1]; ++t) {
+          maxcnt = std::max<int>(maxcnt, h.so_meta[4 * t + 1]);
+          wpairs += h.so_meta[4 * t + 1];
+          ++wsteps;
+        }
       }
       const int slot = std::max(1, std::min(maxcnt, 1024));  // wider steps: straight from L2
       const size_t smem = refactor_wide_smem(h.maxpat, maxsteps, slot);
@@ -369,6 +374,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
         d.ref_wslot = slot;
         d.ref_wsteps = maxsteps;
         d.ref_wsmem = smem;
+        d.ref_wnt = refactor_wide_nt(wsteps ? (double)wpairs / (double)wsteps : 0.0);
       }
     }
   }
@@ -731,7 +737,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   dev->refactor_blocks = std::max(1, bps) * dev->sm_count;
   if (d.ref_start + d.ref_n1 < n) {
     int wb = 0;
-    CUDA_TRY(refactor_wide_configure(d.ref_wsmem, &wb));
+    CUDA_TRY(refactor_wide_configure(d.ref_wnt, d.ref_wsmem, &wb));
     d.ref_wblocks = std::max(1, wb) * dev->sm_count;
   }
   int tb = 0;

@@ -80,7 +80,7 @@ struct DevPlan {
   // single-system refactor: col_order[ref_start, ref_start + ref_n1) = the columns of the warp
   // kernel (k_refactor), the rest (j >= JW, reordered after them, level order kept) the wide
   // columns of k_refactor_wide (KKT_REF_WIDE_NP; ring slot / staged steps / launch shape)
-  int ref_n1 = 0, ref_wslot = 0, ref_wsteps = 0, ref_wblocks = 0;
+  int ref_n1 = 0, ref_wslot = 0, ref_wsteps = 0, ref_wblocks = 0, ref_wnt = 256;
   size_t ref_wsmem = 0;
   int grid_wait = 0;  // sync-free grid solves: 1 = wait on a row's critical dependency first
   // operator (pattern shared; values per system)
@@ -191,7 +191,8 @@ cudaError_t launch_diag_stats(const DevPlan &d, int blocks, cudaStream_t s);
 cudaError_t refactor_configure(int warps, size_t smem, int buf, int *blocks_per_sm);
 size_t refactor_smem_bytes(int warps, int maxpat, int buf);
 size_t refactor_wide_smem(int maxpat, int maxsteps, int slot);
-cudaError_t refactor_wide_configure(size_t smem, int *blocks_per_sm);
+cudaError_t refactor_wide_configure(int nt, size_t smem, int *blocks_per_sm);
+int refactor_wide_nt(double mean_step);  // CTA width of k_refactor_wide (KKT_REF_WIDE_NT)
 int refactor_buf();  // KKT_REF_BUF (refactor.cu)
 
 cudaError_t launch_trsv(const DevPlan &d, const double *b, double *x, int grid_blocks,

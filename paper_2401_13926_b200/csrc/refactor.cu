@@ -319,7 +319,9 @@ __global__ void __launch_bounds__(256) k_refactor(DevPlan d) {
 // is polled in L2 at use.  Steps wider than a ring slot are replayed straight from L2.
 // Every workspace entry still receives its updates in so(j) order => bitwise the same factors.
 // ----------------------------------------------------------------------------
-constexpr int WIDE_NT = 256;
+// CTA width by the tail's mean step size (host: refactor_wide_nt): 10k (36 entries per step)
+// 128 threads 1.34 ms vs 256 1.38 vs 512 1.53; imbalance 0.9 (227 per step) 512 10.8 ms vs
+// 256 11.9 vs 128 15.5.  Steps staged 3 ahead (2: 1.38, 5: 1.48 ms at 10k).
 constexpr int WIDE_AHEAD = 3;
 constexpr int WIDE_Q = WIDE_AHEAD + 2;
 
@@ -327,6 +329,7 @@ size_t refactor_wide_smem(int maxpat, int maxsteps, int slot) {
   return ((size_t)maxpat + 1) / 2 * 16 + (size_t)maxsteps * 16 + (size_t)WIDE_Q * slot * 12 + 64;
 }
 
+template <int WIDE_NT>
 __global__ void __launch_bounds__(WIDE_NT) k_refactor_wide(DevPlan d) {
   extern __shared__ __align__(16) double wsm[];
   __shared__ int s_task;
@@ -432,10 +435,22 @@ __global__ void __launch_bounds__(WIDE_NT) k_refactor_wide(DevPlan d) {
   }
 }
 
-cudaError_t refactor_wide_configure(size_t smem, int *blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_refactor_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int NT>
+static cudaError_t wide_conf(size_t smem, int *blocks_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_refactor_wide<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_refactor_wide, WIDE_NT, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_refactor_wide<NT>, NT, smem);
+}
+cudaError_t refactor_wide_configure(int nt, size_t smem, int *blocks_per_sm) {
+  return nt == 512 ? wide_conf<512>(smem, blocks_per_sm)
+         : nt == 128 ? wide_conf<128>(smem, blocks_per_sm) : wide_conf<256>(smem, blocks_per_sm);
+}
+int refactor_wide_nt(double mean_step) {
+  if (const char *e = std::getenv("KKT_REF_WIDE_NT")) {
+    const int v = std::atoi(e);
+    return v >= 512 ? 512 : v <= 128 ? 128 : 256;
+  }
+  return mean_step <= 48 ? 128 : mean_step <= 160 ? 256 : 512;  // 70k (54): 256 6.87 vs 128 7.02 ms
 }
 
 // ----------------------------------------------------------------------------
@@ -598,7 +613,9 @@ cudaError_t launch_refactor(const DevPlan &d, int blocks, int warps, size_t smem
   if (d.ref_start + d.ref_n1 < d.n) {  // single system: the wide columns, CTA per column
     e = cudaMemsetAsync(d.ticket2, 0, 4, s);
     if (e != cudaSuccess) return e;
-    k_refactor_wide<<<d.ref_wblocks, WIDE_NT, d.ref_wsmem, s>>>(d);
+    if (d.ref_wnt == 512) k_refactor_wide<512><<<d.ref_wblocks, 512, d.ref_wsmem, s>>>(d);
+    else if (d.ref_wnt == 128) k_refactor_wide<128><<<d.ref_wblocks, 128, d.ref_wsmem, s>>>(d);
+    else k_refactor_wide<256><<<d.ref_wblocks, 256, d.ref_wsmem, s>>>(d);
     ++*launches;
   }
   return cudaGetLastError();
