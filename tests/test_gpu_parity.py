@@ -197,12 +197,18 @@ def test_harness_rows_device_mode(case):
 @pytest.mark.parametrize("env", [{"KKT_GRID_WAIT": "0"}, {"KKT_U_PARTIAL": "0"},
                                  {"KKT_SWEEP_AHEAD": "1"}, {"KKT_SWEEP_NOSTAGE": "1"},
                                  {"KKT_SWEEP_THREADS": "512"}, {"KKT_TRSV_BLOCKS": "148"},
-                                 {"KKT_REF_DIRECT": "0"}, {"KKT_REF_BUF": "128"}])
+                                 {"KKT_REF_DIRECT": "0"}, {"KKT_REF_BUF": "128"},
+                                 # separator tail: warp kernel only / CTA per column on most
+                                 # columns, every CTA width
+                                 {"KKT_REF_WIDE_NP": "0"}, {"KKT_REF_WIDE_NP": "8"},
+                                 {"KKT_REF_WIDE_NP": "4", "KKT_REF_WIDE_NT": "512"},
+                                 {"KKT_REF_WIDE_NP": "6", "KKT_REF_WIDE_NT": "256"}])
 @pytest.mark.parametrize("case", ["standard_trace", "acopf_small"])
 def test_single_system_solve_variants_bitwise(case, env, monkeypatch):
     """The single-system path's alternative schedules (grid critical wait, U head prefix,
     sweep variants, a reduced persistent grid as the straggler helpers use, the refactor's
-    staged-restage miss path and stage size) stay bitwise."""
+    staged-restage miss path and stage size, the CTA-per-column separator tail forced onto
+    most columns) stay bitwise."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     g = golden(case)
