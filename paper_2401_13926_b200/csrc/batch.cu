@@ -473,6 +473,181 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d, const in
 
 
 // ----------------------------------------------------------------------------
+// k_b_refactor2: the same light-column replay with TWO systems per lane (task of S systems:
+// S/2 system lanes x E = 64/S entry lanes).  Workspace, stage values, A values and the solve
+// layouts are read and written as 16-byte pairs of adjacent systems, so every loop of a task
+// (A scatter, staging, replay, finalize) runs half the iterations of k_b_refactor for the
+// same S; the per-system arithmetic and update order are unchanged (bitwise).  Needs S >= 2
+// for every task of the first launch (columns wider than the split go to the CTA kernels).
+// 10k x 64: 5.77 -> 5.52 ms (114 registers, four CTAs per SM; capped at 96 registers with
+// spills: 5.62); imbalance 0.95: 23.6 -> 22.6 ms.  The persistent grid is sized for the lower
+// occupancy of the two kernels.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ bool sent2(double2 v) { return is_sentinel(v.x) || is_sentinel(v.y); }
+
+__device__ __forceinline__ void chunk_issue2(const DevPlan &d, const Chunk &c, double *stv, int *sts,
+                                             int lgS, int sys0, int lane) {
+  const int lgH = lgS - 1, H = 1 << lgH;  // system pairs per task
+  for (int i = 0; i < c.nsteps; ++i) {
+    const int cnt = __shfl_sync(FULL, c.m.y, i);
+    const int off = __shfl_sync(FULL, c.incl - c.m.y, i);
+    const int lbk = __shfl_sync(FULL, c.m.w, i);
+    for (int f = lane; f < (cnt << lgH); f += 32)
+      cp_async16(&stv[(off << lgS) + 2 * f], &d.Lx[IL(d, lbk + (f >> lgH), sys0 + 2 * (f & (H - 1)))]);
+  }
+  const int pair0 = __shfl_sync(FULL, c.m.z, 0);
+  for (int p = lane; p < c.npairs; p += 32) cp_async4(&sts[p], &d.upd_slot32[pair0 + p]);
+  cp_async_commit();
+}
+
+__global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor2(DevPlan d, const int2 *__restrict__ tasks,
+                                                            int ntask, int XB, int STG) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  double *x = smem + (size_t)(threadIdx.x >> 5) * (XB + 3 * STG);
+  double *stv0 = x + XB;                                   // [2][STG] staged L values
+  int *sts0 = reinterpret_cast<int *>(stv0 + 2 * STG);     // [2][STG] staged slots
+  int ticket = 0;
+  if (lane == 0) ticket = atomicAdd(d.ticket, 1);
+  TaskInfo nt = load_task(d, tasks, ntask, __shfl_sync(FULL, ticket, 0));
+  while (nt.j >= 0) {
+    const TaskInfo ti = nt;
+    if (lane == 0) ticket = atomicAdd(d.ticket, 1);
+    const int j = ti.j, lgS = ti.lgS, sys0 = ti.sys0;
+    const int S = 1 << lgS, lgH = lgS - 1, H = S >> 1, E = 32 >> lgH;
+    const int h = lane & (H - 1), e = lane >> lgH;
+    const int sys = sys0 + 2 * h;  // this lane: systems sys, sys + 1
+    const int ub = ti.ub, nu = ti.nu, lb = ti.lb, nl = ti.nl;
+    const int np = nu + 1 + nl;
+    const int stp = STG >> lgS;  // pairs per stage buffer
+    const int t_end = ti.t_end;
+    Chunk cur = chunk_meta(d, ti.t0, 0, t_end, stp, lane);
+    int buf = 0;
+    chunk_issue2(d, cur, stv0, sts0, lgS, sys0, lane);
+    for (int f = lane; f < np * H; f += 32) *reinterpret_cast<double2 *>(&x[2 * f]) = make_double2(0.0, 0.0);
+    __syncwarp();
+    // x[a_tgt] = avals[a_src]                                                 (:323)
+    for (int q0 = ti.a0 + e; q0 < ti.a1; q0 += B_AU * E) {
+      int sl[B_AU], src[B_AU];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (q0 + u * E < ti.a1) {
+          sl[u] = d.a_slot[q0 + u * E];
+          src[u] = d.a_src[q0 + u * E];
+        }
+      double2 v[B_AU];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (q0 + u * E < ti.a1) v[u] = *reinterpret_cast<const double2 *>(&d.A_vals[IL(d, src[u], sys)]);
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (q0 + u * E < ti.a1) *reinterpret_cast<double2 *>(&x[sl[u] * S + 2 * h]) = v[u];
+    }
+    __syncwarp();
+    nt = load_task(d, tasks, ntask, __shfl_sync(FULL, ticket, 0));  // consumed next iteration
+    // for k in so(j) (topological): x[Li(k)] -= Lx(k) * x[k]                  (:324-326)
+    while (cur.t0 < t_end) {
+      const int tn = cur.next_t0;
+      Chunk nxt;
+      nxt.t0 = tn;
+      if (tn < t_end) {
+        nxt = chunk_meta(d, tn, cur.next_e0, t_end, stp, lane);
+        chunk_issue2(d, nxt, stv0 + (buf ^ 1) * STG, sts0 + (buf ^ 1) * STG, lgS, sys0, lane);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      const double *stv = stv0 + buf * STG;
+      const int *sts = sts0 + buf * STG;
+      for (int i = 0; i < cur.nsteps; ++i) {
+        const int kslot = __shfl_sync(FULL, cur.m.x, i);
+        const int cnt = __shfl_sync(FULL, cur.m.y, i);
+        const int off = __shfl_sync(FULL, cur.incl - cur.m.y, i);
+        const int lbk = __shfl_sync(FULL, cur.m.w, i);  // L(:,k) = Lx[lbk, lbk+cnt)
+        const double2 xk = *reinterpret_cast<const double2 *>(&x[kslot * S + 2 * h]);
+        for (int idx = e; idx < cnt; idx += E) {  // the targets of one step are distinct slots
+          double2 l = *reinterpret_cast<const double2 *>(&stv[((off + idx) << lgS) + 2 * h]);
+          const int sl = sts[off + idx] * S + 2 * h;
+          double2 xv = *reinterpret_cast<const double2 *>(&x[sl]);
+          if (sent2(l)) {  // staged before L(:,k) was published: wait for it
+            const double *p = &d.Lx[IL(d, lbk + idx, sys)];
+            if (is_sentinel(l.x)) l.x = wait_value_bo(p, d.poll_ns);
+            if (is_sentinel(l.y)) l.y = wait_value_bo(p + 1, d.poll_ns);
+          }
+          xv.x = __dsub_rn(xv.x, __dmul_rn(l.x, xk.x));
+          xv.y = __dsub_rn(xv.y, __dmul_rn(l.y, xk.y));
+          *reinterpret_cast<double2 *>(&x[sl]) = xv;
+        }
+        __syncwarp();
+      }
+      cur = nxt;
+      buf ^= 1;
+    }
+    cp_async_wait<0>();
+    // u_jj = x[j]; patch; L(:,j) = x[Li] / u_jj (published first); U(:,j) = x[Ui]  (:327-344)
+    double2 ujj = *reinterpret_cast<const double2 *>(&x[nu * S + 2 * h]);
+    double gmx = fabs(ujj.x), gmy = fabs(ujj.y);
+    const double epsx = patch_floor_b(d, sys), epsy = patch_floor_b(d, sys + 1);
+    const bool px = fabs(ujj.x) < epsx, py = fabs(ujj.y) < epsy;
+    if (px) ujj.x = (ujj.x >= 0.0) ? epsx : -epsx;
+    if (py) ujj.y = (ujj.y >= 0.0) ? epsy : -epsy;
+    for (int idx = e; idx < nl; idx += E) {
+      double2 v = *reinterpret_cast<const double2 *>(&x[(nu + 1 + idx) * S + 2 * h]);
+      gmx = fmax(gmx, fabs(v.x));
+      gmy = fmax(gmy, fabs(v.y));
+      v.x = unsentinel(__ddiv_rn(v.x, ujj.x));
+      v.y = unsentinel(__ddiv_rn(v.y, ujj.y));
+      double *p = &d.Lx[IL(d, lb + idx, sys)];
+      st_relaxed_f64(p, v.x);
+      st_relaxed_f64(p + 1, v.y);
+      *reinterpret_cast<double2 *>(&x[(nu + 1 + idx) * S + 2 * h]) = v;  // (reread by this lane)
+    }
+    for (int i0 = e; i0 < nl; i0 += B_AU * E) {
+      int mp[B_AU];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (i0 + u * E < nl) mp[u] = d.Lmap[lb + i0 + u * E];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (i0 + u * E < nl)
+          *reinterpret_cast<double2 *>(&d.Lv[IL(d, mp[u], sys)]) =
+              *reinterpret_cast<const double2 *>(&x[(nu + 1 + i0 + u * E) * S + 2 * h]);
+    }
+    for (int i0 = e; i0 < nu; i0 += B_AU * E) {
+      int mp[B_AU];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u)
+        if (i0 + u * E < nu) mp[u] = d.Umap[ub + i0 + u * E];
+#pragma unroll
+      for (int u = 0; u < B_AU; ++u) {
+        const int idx = i0 + u * E;
+        if (idx < nu) {
+          const double2 v = *reinterpret_cast<const double2 *>(&x[idx * S + 2 * h]);
+          *reinterpret_cast<double2 *>(&d.Ux[IL(d, ub + idx, sys)]) = v;
+          *reinterpret_cast<double2 *>(&d.Uv[IL(d, mp[u], sys)]) = v;
+          gmx = fmax(gmx, fabs(v.x));
+          gmy = fmax(gmy, fabs(v.y));
+        }
+      }
+    }
+    for (int o = H; o < 32; o <<= 1) {
+      gmx = fmax(gmx, __shfl_xor_sync(FULL, gmx, o));
+      gmy = fmax(gmy, __shfl_xor_sync(FULL, gmy, o));
+    }
+    if (e == 0) {
+      *reinterpret_cast<double2 *>(&d.udiag[IL(d, j, sys)]) = ujj;
+      unsigned long long *sx = d.scal + (size_t)sys * SCAL_STRIDE, *sy = sx + SCAL_STRIDE;
+      if (px) atomicAdd(&sx[SC_PATCHED], 1ull);
+      if (py) atomicAdd(&sy[SC_PATCHED], 1ull);
+      if (gmx > 0.0 && dbits(gmx) > __ldcg(&sx[SC_GMAX])) atomicMax(&sx[SC_GMAX], dbits(gmx));
+      if (gmy > 0.0 && dbits(gmy) > __ldcg(&sy[SC_GMAX])) atomicMax(&sy[SC_GMAX], dbits(gmy));
+    }
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Refactor, wide separator columns (j >= J2; second launch): a CTA of SC warps per
 // (column, SC systems; KKT_B_CT_SC, default 8).  Thread t serves entry lane e = t / SC and system s = t % SC, so
 // a warp access is 8 entries x 4 systems = 8 full 32-byte sectors (the one-system-per-warp
@@ -1913,6 +2088,16 @@ cudaError_t b_configure(int nbp, size_t refactor_smem, int gridv, int *refactor_
                              cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(refactor_blocks_per_sm, k_b_refactor, 32 * B_WARPS, sm);
+  if (e == cudaSuccess)  // the two-systems-per-lane variant shares the launch shape
+    e = cudaFuncSetAttribute(k_b_refactor2, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_b_refactor2, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) {
+    int b2 = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_b_refactor2, 32 * B_WARPS, sm);
+    if (b2 < *refactor_blocks_per_sm) *refactor_blocks_per_sm = b2;
+  }
   int m = 1 << 30;
   auto occ = [&](const void *f) {
     int a = 0;
@@ -2159,8 +2344,12 @@ cudaError_t b_launch_refactor(const DevPlan &d, int blocks, size_t smem, int blo
   }
   if (d.n_btask1) {
     if (d.prof) cudaMemsetAsync(d.prof, 0, 8 * 8 * (size_t)blocks * B_WARPS, s);
-    k_b_refactor<<<ov ? blocks_ov : blocks, 32 * B_WARPS, smem, s>>>(d, d.btask, d.n_btask1, d.b_xbudget,
-                                                                      d.b_stage);
+    if (d.b_v2 && !d.prof && !d.b_static)
+      k_b_refactor2<<<ov ? blocks_ov : blocks, 32 * B_WARPS, smem, s>>>(d, d.btask, d.n_btask1, d.b_xbudget,
+                                                                         d.b_stage);
+    else
+      k_b_refactor<<<ov ? blocks_ov : blocks, 32 * B_WARPS, smem, s>>>(d, d.btask, d.n_btask1, d.b_xbudget,
+                                                                        d.b_stage);
     ++*launches;
   }
   if (ov) {

@@ -200,7 +200,7 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   if (const char *e = std::getenv("KKT_B_SMEM")) std::sscanf(e, "%d,%d", &d.b_xbudget, &d.b_stage);
   if (const char *e = std::getenv("KKT_B_SMEM2")) std::sscanf(e, "%d,%d", &d.b_xbudget2, &d.b_stage2);
   d.b_static = std::getenv("KKT_B_STATIC") ? std::atoi(std::getenv("KKT_B_STATIC")) : 0;
-  d.b_xbudget = std::max(d.b_xbudget, h.maxpat);
+  d.b_xbudget = (std::max(d.b_xbudget, h.maxpat) + 1) & ~1;  // even: 16-byte pairs (k_b_refactor2)
   d.b_xbudget2 = std::max(d.b_xbudget2, h.maxpat);
   if (nb > 1) {
     // heavy tail: from the first column whose pattern exceeds KKT_B_HEAVY_NP slots
@@ -251,6 +251,11 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
       }
     }
     d.n_btask1 = (int)btask.size();
+    // two systems per lane needs every first-launch task to hold >= 2 systems
+    d.b_v2 = std::getenv("KKT_B_V2") ? std::atoi(std::getenv("KKT_B_V2")) : 1;
+    if (d.b_stage & 1) d.b_v2 = 0;  // (KKT_B_SMEM override: the stage must hold 16-byte pairs)
+    for (int t = 0; d.b_v2 && t < d.n_btask1; ++t)
+      if ((btask[t].y & 0xff) == 0) d.b_v2 = 0;
     d.ct_sc = std::getenv("KKT_B_CT_SC") ? std::atoi(std::getenv("KKT_B_CT_SC")) : 8;
     if (d.ct_sc != 2 && d.ct_sc != 8) d.ct_sc = 4;
     d.ct_mode = std::getenv("KKT_B_CT_MODE") ? std::atoi(std::getenv("KKT_B_CT_MODE")) : 3;

@@ -41,6 +41,7 @@ struct DevPlan {
   int2 *btask = nullptr;  // batched refactor tasks {column, sys0 << 8 | log2(systems)}
   int n_btask = 0;
   int b_xbudget = 0, b_stage = 0, b_static = 0;
+  int b_v2 = 0;  // light-column replay with two systems per lane (k_b_refactor2; KKT_B_V2)
   int b_xbudget2 = 0, b_stage2 = 0, n_btask1 = 0;  // second replay launch (wide columns)
   int ct_sc = 4;  // systems per k_b_refactor_cta task (KKT_B_CT_SC = 2 | 4 | 8)
   int ct_mode = 3;  // 3 (default): TMA pipeline; 0: entry x system lanes + CTA barrier per step;
