@@ -29,9 +29,6 @@ pytestmark = pytest.mark.gpu
     ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_E": "64"}),
     # one system per lane in the light-column replay (k_b_refactor; default: two per lane)
     ("acopf_small", 33, {"KKT_B_V2": "0"}), ("standard_trace", 9, {"KKT_B_V2": "0"}),
-    # wide-column replay with two systems per consumer thread (64 entry lanes)
-    ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_V2": "1"}),
-    ("standard_trace", 9, {"KKT_B_SPLIT_NP": "4", "KKT_B_TMA_V2": "1"}),
     # flag-free wide-column producer (default with the 128-row ring: 70k-class patterns)
     ("acopf_small", 33, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA_DIRECT": "3"}),
     ("acopf_small", 40, {"KKT_B_SPLIT_NP": "8", "KKT_B_TMA": "2,128"}),
