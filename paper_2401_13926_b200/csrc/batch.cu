@@ -34,8 +34,10 @@ static int rowwise();  // KKT_B_SPMV_TILES (below)
 constexpr int BY = 8;            // rows (warps) per block of the 2-D row kernels
 constexpr int SMALL_PAT_B = 64;
 // refactor: A-scatter / finalize entries per lane per round of independent loads (the index
-// loads of a round, then its value loads, are in flight together: 5.87 -> 5.77 ms at 10k x 64)
-constexpr int B_AU = 4;  // (the same in k_b_refactor_small cost occupancy: 5.77 -> 5.83 ms)
+// loads of a round, then its value loads, are in flight together: 5.87 -> 5.77 ms at 10k x 64
+// with 4; with two systems per lane, 2 keeps k_b_refactor2 at 95 registers and five CTAs per
+// SM: 5.52 -> 5.35 ms)
+constexpr int B_AU = 2;  // (the same in k_b_refactor_small cost occupancy: 5.77 -> 5.83 ms)
 constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ double sentinel_value() {
@@ -479,8 +481,8 @@ __global__ void __launch_bounds__(32 * B_WARPS) k_b_refactor(DevPlan d, const in
 // (A scatter, staging, replay, finalize) runs half the iterations of k_b_refactor for the
 // same S; the per-system arithmetic and update order are unchanged (bitwise).  Needs S >= 2
 // for every task of the first launch (columns wider than the split go to the CTA kernels).
-// 10k x 64: 5.77 -> 5.52 ms (114 registers, four CTAs per SM; capped at 96 registers with
-// spills: 5.62); imbalance 0.95: 23.6 -> 22.6 ms.  The persistent grid is sized for the lower
+// 10k x 64: 5.77 -> 5.52 ms (114 registers with B_AU = 4, four CTAs per SM) -> 5.35 ms with
+// B_AU = 2 (95 registers, five CTAs per SM); imbalance 0.95: 23.6 -> 22.6 ms.  The persistent grid is sized for the lower
 // occupancy of the two kernels.
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ bool sent2(double2 v) { return is_sentinel(v.x) || is_sentinel(v.y); }
