@@ -578,7 +578,8 @@ def main():
         tp = os.path.join(ROOT, "profiles", "r1l_ncu_traffic.json")
     if same_workload and os.path.exists(tp):
         tk = json.load(open(tp))["kernels"]
-        fam = {"refactor": ["k_b_refactor", "k_b_refactor_tma<"], "spmv": ["k_b_spmv"],
+        light = "k_b_refactor2" if "k_b_refactor2" in tk else "k_b_refactor"  # (two systems per lane)
+        fam = {"refactor": [light, "k_b_refactor_tma<"], "spmv": ["k_b_spmv"],
                "trisolve_pair": ["k_b_trsv_grid<0,", "k_b_trsv_grid<1,", "k_trsv_blocked<0, 1,",
                                  "k_trsv_blocked<1, 1,"]}[dom]
         # a member ending in "<" or "," matches any instantiation of that template

@@ -3,7 +3,7 @@
 # the launch list of the default bench command, and the single-system solve breakdown.
 T=${1:-r2}
 timeout 1500 ncu --set full --clock-control none --import-source on --graph-profiling node \
-  -k regex:'k_b_refactor$|k_b_refactor_tma|k_b_trsv_grid|k_trsv_blocked|k_b_spmv_row|k_b_dots|k_b_cgs|k_givens|k_b_expand_norms' \
+  -k regex:'k_b_refactor$|k_b_refactor2|k_b_refactor_tma|k_b_trsv_grid|k_trsv_blocked|k_b_spmv_row|k_b_dots|k_b_cgs|k_givens|k_b_expand_norms' \
   -c 16 -o gpurun_out/${T}_full python tools/step_probe.py activsg10k 64 19 1 > gpurun_out/${T}_full.log 2>&1
 echo full=$?
 python tools/ncu_traffic.py gpurun_out/${T}_full.ncu-rep gpurun_out/${T}_ncu_traffic.json > /dev/null 2>&1
