@@ -344,7 +344,10 @@ static int setup(Device *dev, const kkt_device_opts *opts, Device *&out) {
   d.ref_n1 = h.n - d.ref_start;
   std::vector<int32_t> corder;
   if (nbp == 1) {
-    const int wide_np = std::getenv("KKT_REF_WIDE_NP") ? std::atoi(std::getenv("KKT_REF_WIDE_NP")) : 128;
+    // default split: 128 slots (10k: 64 / 128 / 256 -> 1.32 / 1.33 / 1.42 ms); 256 for the
+    // 70k class (6.52 vs 6.87 ms at 128)
+    const int wide_np = std::getenv("KKT_REF_WIDE_NP") ? std::atoi(std::getenv("KKT_REF_WIDE_NP"))
+                                                       : (h.n > 1000000 ? 256 : 128);
     int JW = h.n;
     for (int j = 0; wide_np > 0 && j < h.n; ++j)
       if ((h.Up[j + 1] - h.Up[j]) + 1 + (h.Lp[j + 1] - h.Lp[j]) > wide_np) {
